@@ -1,0 +1,170 @@
+/* simsweep.h -- C-ABI of libsimsweep.so, the B200 (sm_100a) step-level
+ * simulator of multi-batch LLM-serving schedulers (arXiv 2411.07447).
+ *
+ * One SIMULATION = Algorithm 1 "Scheduler(M, C)" run on
+ * one workload until every request has generated its O tokens, under one
+ * scheduler preset (Table 2; Table "Schedulers used",
+ * PAPER.md:39-57), one replacement policy (NRF, Table 2; SRF / SRF+Hist,
+ * PAPER.md:647-653) and 1..4 batch-latency models.
+ * The semantics of every step are the readings Q1-Q38 of DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - plain pointers and sizes only; the CALLER owns every buffer.  The library
+ *    keeps no global state, allocates only transient device scratch, and is
+ *    reentrant.
+ *  - return value: 0 on success, < 0 on a call-level error (SIM_EINVAL ...;
+ *    sim_strerror() names it).  Problems of one simulation are reported in its
+ *    sim_result_t.status (SIM_S_*), never in the return value.
+ *  - results of failed simulations (status != SIM_S_OK) are zero-filled.
+ */
+#ifndef SIMSWEEP_H
+#define SIMSWEEP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* GroupRequests order (step 1; Table 2; App. D) */
+enum {
+  SIM_ORDER_PREFILL_FIRST = 0, /* vLLM {R_w, R_r} */
+  SIM_ORDER_DECODE_FIRST = 1,  /* Sarathi {R_r^d, R_r^p, R_w} */
+  SIM_ORDER_RANK_ORG = 2,      /* one group by (T, id) */
+  SIM_ORDER_RANK_I = 3,        /* one group by (I, T, id) */
+  SIM_ORDER_RANK_O = 4         /* one group by (O, T, id) -- hypothetical, reads O */
+};
+/* cache replacement policy on preemption */
+enum {
+  SIM_NRF = 0,     /* newest (most recently admitted) request first, Table 2 */
+  SIM_SRF = 1,     /* shortest (smallest m) request first */
+  SIM_SRF_HIST = 2 /* SRF + online output-length histogram deferral */
+};
+/* per-simulation status */
+enum {
+  SIM_S_OK = 0,
+  SIM_S_TOO_LONG = 1,   /* some request has I+O-1 > S */
+  SIM_S_NEVER_FITS = 2, /* I+O-1 > M, or > C without chunked prefill (reading Q35) */
+  SIM_S_MAX_STEPS = 3,  /* more than max_steps batches */
+  SIM_S_DEADLOCK = 4,   /* B empty, nothing arriving, requests unfinished (defensive) */
+  SIM_S_CAPACITY = 5    /* more than SIM_MAX_WINDOW arrived-but-unfinished requests */
+};
+/* call-level errors */
+enum {
+  SIM_EINVAL = -1,    /* NULL pointer, n <= 0, bad enum, C < 1, S < 1, n_cost not 1..4 */
+  SIM_EWORKLOAD = -2, /* I < 1, O < 1, T not sorted, or T != 0 with n_cost > 1 */
+  SIM_ECOST = -3,     /* cost-model index out of range or bad cost-model fields */
+  SIM_ECUDA = -4,     /* a CUDA runtime error (device, allocation, launch) */
+  SIM_ENODEV = -5     /* no sm_100 device */
+};
+
+#define SIM_MAX_COST 4
+/* largest simultaneously tracked request window (arrived and not finished,
+ * counted from the oldest unfinished request); larger -> SIM_S_CAPACITY */
+#define SIM_MAX_WINDOW 4096
+
+/* One simulation.  72 bytes, naturally aligned. */
+typedef struct {
+  int32_t order;       /* SIM_ORDER_* */
+  int32_t hybrid;      /* 0/1: hybrid prefill+decode batches (step 2) */
+  int32_t chunked;     /* 0/1: chunked prefill */
+  int32_t replacement; /* SIM_NRF / SIM_SRF / SIM_SRF_HIST */
+  int32_t S;           /* model context size; requests need I+O-1 <= S */
+  int32_t workload;    /* index into the workload table */
+  int64_t C;           /* token limit per batch (>= 1) */
+  int64_t M;           /* KV-cache capacity in tokens; < 0 = infinite (what-if) */
+  int64_t max_steps;   /* livelock guard (>= 1) */
+  int32_t n_cost;      /* 1..4 cost models charged on the same schedule; > 1 only for offline (all T = 0) */
+  int32_t cost[SIM_MAX_COST]; /* indices into the cost-model table; the clock of cost[0] drives arrivals */
+  int32_t reserved0;
+} sim_config_t;
+
+/* One workload: n requests sorted by (T, id).  The pointers are HOST memory
+ * for sim_sweep() and DEVICE memory for sim_sweep_device(). */
+typedef struct {
+  int32_t n;      /* >= 1 */
+  int32_t pad;
+  const int32_t* I; /* [n] input tokens, >= 1 */
+  const int32_t* O; /* [n] output tokens, >= 1 */
+  const double* T;  /* [n] arrival times in seconds, non-decreasing */
+} sim_workload_t;
+
+/* One batch-latency model (Sec. "Cost Models for Batch Times").  mode 0 =
+ * linear over the Table 3 variables, per layer
+ *   t = a0 + a1 N + [n_p>0](b0 + b1 sum c^2 + b2 sum mc + b3 sum c + b4 sum m)
+ *                 + [n_d>0](d0 + d1 sum m + d2 n_d),
+ * mode 1 = Eq. (3) roofline per operator with Eq. (1)-(2) for
+ * attention; batch time = layers * t.  flops / bw are aggregate over tp GPUs;
+ * link_bw is the per-GPU All_Reduce bandwidth.  Evaluation order: DESIGN.md 2. */
+typedef struct {
+  int32_t mode;
+  int32_t layers, h, f, H, NQ, NKV, e, tp;
+  int32_t pad;
+  double lin[10]; /* a0 a1 | b0 b1 b2 b3 b4 | d0 d1 d2, seconds per layer */
+  double flops, bw, link_bw;
+} sim_cost_model_t;
+
+/* Per-simulation result (one per config). */
+typedef struct {
+  int32_t status; /* SIM_S_* */
+  int32_t pad;
+  int64_t steps;            /* number of batches B_j */
+  int64_t preemptions;      /* including self-preemptions */
+  int64_t batch_entries;    /* sum_j |B_j| */
+  int64_t processed_tokens; /* sum_j sum_{B_j} c */
+  int64_t sum_U;            /* sum_j KV holdings right after admission (kv usage = sum_U / (steps M)) */
+  int64_t prefill_entries;  /* entries in the prefill phase */
+  int64_t idle_jumps;       /* clock jumps to the next arrival (not steps) */
+  double makespan[SIM_MAX_COST];     /* max t_done - min T, per cost model */
+  double mean_latency[SIM_MAX_COST]; /* mean t_done - T */
+  double mean_ttft[SIM_MAX_COST];    /* mean t_first - T */
+  double mean_tpot[SIM_MAX_COST];    /* mean (t_done - t_first)/(O-1) over O > 1 */
+} sim_result_t;
+
+/* Per-request outputs.  Config i owns rows [row_off[i], row_off[i] + n_i) of
+ * n_preempt / refill_tokens and rows [tim_off[i], tim_off[i] + n_cost_i * n_i)
+ * of t_first / t_done, k-major (t_first[tim_off[i] + k*n_i + r]).  Offsets are
+ * the exclusive prefix sums of n_i and n_cost_i * n_i in config order. */
+typedef struct {
+  double* t_first;        /* time the first token was generated */
+  double* t_done;         /* time the O-th token was generated */
+  int64_t* n_preempt;     /* times the request was preempted */
+  int64_t* refill_tokens; /* sum of m discarded at its preemptions */
+} sim_request_out_t;
+
+/* Simulate n_cfgs configurations.  HOST buffers: cfgs[n_cfgs], wls[n_wls]
+ * (with host arrays), cms[n_cms], results[n_cfgs] and req (sized by the
+ * offsets above; any member may be NULL to skip it).  Uses CUDA device
+ * `device` (or the current device if < 0); all device memory is transient.
+ * Returns 0 / SIM_E*.  Blocking. */
+int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
+              const sim_cost_model_t* cms, int32_t n_cms, sim_result_t* results, sim_request_out_t req,
+              int32_t device);
+
+/* Same computation with everything already resident on the device.
+ * d_cfgs[n_cfgs], d_wls[n_wls] (struct array in device memory whose I/O/T
+ * point to device memory), d_cms[n_cms], d_results[n_cfgs], d_row_off[n_cfgs],
+ * d_tim_off[n_cfgs] and the members of d_req are DEVICE pointers.  The host
+ * arrays h_cfgs / h_wls_n (n of each workload) describe the same configs and
+ * are used only to choose kernel variants and launch order; d_order[n_cfgs]
+ * (device, may be NULL) is a permutation giving the launch order (e.g.
+ * longest-first).  Launches asynchronously on `stream` (cudaStream_t, NULL =
+ * legacy default stream) and does not synchronize; validation of workload
+ * contents is the caller's responsibility (sim_sweep does it).  Returns the
+ * number of kernel launches issued (>= 1) or SIM_E*. */
+int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n,
+                     const sim_config_t* d_cfgs, const sim_workload_t* d_wls, const sim_cost_model_t* d_cms,
+                     int32_t n_cms, const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
+                     sim_result_t* d_results, sim_request_out_t d_req, void* stream);
+
+/* Scratch-free helper: total rows of the per-request outputs for n_cfgs configs
+ * (rows = sum n_i, tim_rows = sum n_cost_i * n_i).  Returns 0 / SIM_EINVAL. */
+int sim_request_rows(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
+                     int64_t* rows, int64_t* tim_rows);
+
+const char* sim_strerror(int code);
+const char* sim_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIMSWEEP_H */

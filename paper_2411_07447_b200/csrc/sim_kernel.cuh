@@ -1,0 +1,239 @@
+// sim_kernel.cuh -- the sm_100a step kernel: one CTA per simulation.
+//
+// Each CTA runs Algorithm 1 for one sim_config_t with the
+// request state as a structure of arrays in shared memory (a ring of CAP slots
+// indexed by request id mod CAP).  Per step (one batch B_j):
+//   a2  arrivals            binary search of the sorted T, slot init
+//   a3  GroupRequests       stream compactions build the visiting order P
+//   a4-a8 GetNextBatch      block-parallel "rounds": every remaining candidate is
+//                           classified against the current (tok, U); a 4-component
+//                           block prefix scan (tokens, KV delta, admissions, SRF+Hist
+//                           remainders) finds the first candidate whose admission is
+//                           not decided by the scan (a break); the prefix before it
+//                           is admitted in parallel and thread 0 resolves the break
+//                           literally (preemption victims = tail of the retention
+//                           list, self-preemption, chunk cropping, deferral)
+//   a9  batch latency       block reduction of exact int64 features, fp64 cost model
+//                           (__dadd_rn/__dmul_rn/__ddiv_rn: no contraction)
+//   a10 Process             parallel m += c, Eq. (6) token generation, completions
+//   run-list maintenance    stable compaction (NRF = admission order); SRF order is
+//                           re-sorted (bitonic) only when the compacted list is unsorted
+// Semantics: DESIGN.md readings Q1-Q38, identical to oracle/oracle.cpp.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "simsweep.h"
+
+namespace simsweep {
+
+constexpr uint8_t ST_WAIT = 1, ST_RUN = 2, ST_DONE = 3, ST_MASK = 3;
+constexpr uint8_t F_FILLED = 4, F_INB = 8, F_PRE = 16, F_FIRST = 32;
+constexpr int PH_DEC = 0, PH_PRE = 1;
+constexpr int IPT = 4;  // items per thread in block-wide passes (blocked layout)
+constexpr int NOBRK = 0x7fffffff;
+
+struct KParams {
+  const sim_config_t* cfgs;
+  const sim_workload_t* wls;
+  const sim_cost_model_t* cms;
+  const int32_t* order;
+  const int64_t* row_off;
+  const int64_t* tim_off;
+  sim_result_t* results;
+  sim_request_out_t req;
+  int32_t n_cfgs;
+  int32_t variant;
+};
+
+// exact integer features of one batch (Table 3 variables; Eq. (1)-(2) sums)
+struct Feat {
+  long long N, np, c2, mc, cp, mp, pcm, nd, md;
+  long long pceil[SIM_MAX_COST];
+};
+
+struct Scal {
+  double clock[SIM_MAX_COST];
+  sim_cost_model_t cm[SIM_MAX_COST];
+  long long U, tok, Rsum, seq;
+  long long steps, preempt, entries, processed, sumU, pentries, idle;
+  long long pref[4];  // exclusive prefixes (c, dKV, admitted-waiting, SRF+Hist rem) at the break
+  long long featsum[16];
+  long long wred[16][16];  // per-warp partial feature sums
+  int next, new_next, lo, n_done, n_run, n_running, nW, nP, len0, n_new, nrank;
+  int pos, bphase, vt, status, brk, any_pre, cur;
+  int wmin[32];
+  int wsum[32][4];
+  int wcnt[32];
+  int hist[18 * 18];
+  int pred[18];
+};
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double i2d(long long x) { return __ll2double_rn(x); }
+
+// Eq. (3): max(FLOPs / GPU_FLOPS, RW / GPU_bandwidth), RW bytes = e * elements (Q26)
+__device__ __forceinline__ double roof(long long F, long long R, const sim_cost_model_t& cm) {
+  return fmax(ddiv(i2d(F), cm.flops), ddiv(i2d(R * (long long)cm.e), cm.bw));
+}
+
+// batch time d_j of one cost model from the batch features
+__device__ double batch_time(const sim_cost_model_t& cm, const Feat& f, int k) {
+  if (cm.mode == 1) {
+    const long long h = cm.h, ff = cm.f, H = cm.H, NQ = cm.NQ, NKV = cm.NKV, N = f.N;
+    const long long qo = (NQ + 2 * NKV) * H, ao = NQ * H;
+    double t = 0.0;
+    t = dadd(t, roof(2 * N * h * qo, h * qo + N * h + N * qo, cm));                     // QKV_proj
+    t = dadd(t, roof(2 * N * ao * h, ao * h + N * ao + N * h, cm));                     // O_proj
+    t = dadd(t, roof(2 * N * h * (2 * ff), h * (2 * ff) + N * h + N * (2 * ff), cm));  // gate+up
+    t = dadd(t, roof(2 * N * ff * h, ff * h + N * ff + N * h, cm));                     // D_proj
+    if (f.np > 0)  // prefill attention, Eq. (1)-(2) summed per request with B = 1 (Q24)
+      t = dadd(t, roof(4 * H * NQ * f.pcm, 2 * H * NQ * f.cp + 2 * NQ * f.pcm + 2 * H * NKV * f.pceil[k], cm));
+    if (f.nd > 0) {  // decode attention: c = 1, ceil(1/H) = 1
+      const long long s1m = f.md + f.nd;
+      t = dadd(t, roof(4 * H * NQ * s1m, 2 * H * NQ * f.nd + 2 * NQ * s1m + 2 * H * NKV * s1m, cm));
+    }
+    if (cm.tp > 1) {  // two All_Reduce per layer
+      const double ar = ddiv(ddiv(i2d(2 * (long long)cm.e * N * h * (long long)(cm.tp - 1)), i2d(cm.tp)), cm.link_bw);
+      t = dadd(t, ar);
+      t = dadd(t, ar);
+    }
+    return dmul(i2d(cm.layers), t);
+  }
+  const double* a = cm.lin;
+  double t = dadd(a[0], dmul(a[1], i2d(f.N)));
+  if (f.np > 0)
+    t = dadd(t, dadd(dadd(dadd(dadd(a[2], dmul(a[3], i2d(f.c2))), dmul(a[4], i2d(f.mc))), dmul(a[5], i2d(f.cp))),
+                     dmul(a[6], i2d(f.mp))));
+  if (f.nd > 0) t = dadd(t, dadd(dadd(a[7], dmul(a[8], i2d(f.md))), dmul(a[9], i2d(f.nd))));
+  return dmul(i2d(cm.layers), t);
+}
+
+__device__ __forceinline__ int bucket_of(int x) {  // floor(log2 x), capped at 17
+  int b = 31 - __clz(x);
+  return b > 17 ? 17 : b;
+}
+
+// SRF+Hist predicted output length per I-bucket (reading Q31): nearest-rank p90 bucket edge
+__device__ int hist_pred_row(const int* H, int bi) {
+  long long n = 0;
+  for (int b = 0; b < 18; b++) n += H[bi * 18 + b];
+  if (n >= 8) {
+    long long target = (9 * n + 9) / 10, cum = 0;
+    for (int b = 0; b < 18; b++) {
+      cum += H[bi * 18 + b];
+      if (cum >= target) return (1 << (b + 1)) - 1;
+    }
+  }
+  long long col[18];
+  n = 0;
+  for (int b = 0; b < 18; b++) {
+    col[b] = 0;
+    for (int a = 0; a < 18; a++) col[b] += H[a * 18 + b];
+    n += col[b];
+  }
+  if (n >= 8) {
+    long long target = (9 * n + 9) / 10, cum = 0;
+    for (int b = 0; b < 18; b++) {
+      cum += col[b];
+      if (cum >= target) return (1 << (b + 1)) - 1;
+    }
+  }
+  return 256;
+}
+
+// block-wide exclusive scan of one int per thread; returns the prefix, total in *tot.
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, Scal& S, int* tot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) S.wcnt[wid] = x;
+  __syncthreads();
+  int off = 0, t = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; w++) {
+    int s = S.wcnt[w];
+    off += (w < wid) ? s : 0;
+    t += s;
+  }
+  __syncthreads();
+  *tot = t;
+  return off + x - v;
+}
+
+// stable stream compaction of positions [0, L) satisfying pred into out[base...]; returns count
+template <int NT, typename Pred, typename Val>
+__device__ int block_compact(int L, Pred pred, Val val, int16_t* out, Scal& S) {
+  int total = 0;
+  for (int base = 0; base < L; base += NT * IPT) {
+    int flags = 0, cnt = 0;
+#pragma unroll
+    for (int j = 0; j < IPT; j++) {
+      int q = base + threadIdx.x * IPT + j;
+      if (q < L && pred(q)) {
+        flags |= 1 << j;
+        cnt++;
+      }
+    }
+    int tot;
+    int w = total + block_excl_scan<NT>(cnt, S, &tot);
+#pragma unroll
+    for (int j = 0; j < IPT; j++)
+      if (flags >> j & 1) out[w++] = (int16_t)val(base + threadIdx.x * IPT + j);
+    total += tot;
+  }
+  return total;
+}
+
+// ascending bitonic sort of keys[0, L) (padded with ~0 to a power of two <= CAP)
+template <int NT>
+__device__ void block_bitonic(unsigned long long* keys, int L) {
+  int P2 = 1;
+  while (P2 < L) P2 <<= 1;
+  for (int i = L + threadIdx.x; i < P2; i += NT) keys[i] = ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P2; i += NT) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          unsigned long long a = keys[i], b = keys[ixj];
+          bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            keys[i] = b;
+            keys[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NT, int CAP>
+struct Smem {
+  static constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+  static constexpr size_t off_int = align16(sizeof(Scal));
+  static constexpr size_t n_int = 7;  // m g res seq I O c
+  static constexpr size_t off_rpos = off_int + n_int * 4 * CAP;
+  static constexpr size_t off_fl = off_rpos + 2 * CAP;
+  static constexpr size_t off_lists = align16(off_fl + CAP);  // run0 run1 rank (int16)
+  static constexpr size_t off_union = align16(off_lists + 3 * 2 * CAP);  // 8 B/slot: wl pl newadm tmp | u64 keys
+  static constexpr size_t bytes = off_union + 8 * CAP;
+};
+
+}  // namespace simsweep

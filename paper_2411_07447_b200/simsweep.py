@@ -1,0 +1,297 @@
+"""Python binding of libsimsweep.so (include/simsweep.h).  Argument marshalling only.
+
+Every step of the simulation runs in the CUDA kernel; there is no CPU
+fallback: if the shared library is missing or no sm_100 device is present the
+calls raise.  PyTorch is used only for device memory and streams (the
+``DeviceSweep`` path).
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import presets as _presets
+from .workloads import Workload
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB_PATH = os.path.join(PKG, "libsimsweep.so")
+
+SIM_MAX_COST = 4
+STATUS = {0: "ok", 1: "too_long", 2: "never_fits", 3: "max_steps", 4: "deadlock", 5: "capacity"}
+
+
+class SimConfig(ctypes.Structure):
+    _fields_ = [("order", ctypes.c_int32), ("hybrid", ctypes.c_int32), ("chunked", ctypes.c_int32),
+                ("replacement", ctypes.c_int32), ("S", ctypes.c_int32), ("workload", ctypes.c_int32),
+                ("C", ctypes.c_int64), ("M", ctypes.c_int64), ("max_steps", ctypes.c_int64),
+                ("n_cost", ctypes.c_int32), ("cost", ctypes.c_int32 * SIM_MAX_COST), ("reserved0", ctypes.c_int32)]
+
+
+class SimWorkload(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("pad", ctypes.c_int32), ("I", ctypes.c_void_p), ("O", ctypes.c_void_p),
+                ("T", ctypes.c_void_p)]
+
+
+class SimCostModel(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("layers", ctypes.c_int32), ("h", ctypes.c_int32), ("f", ctypes.c_int32),
+                ("H", ctypes.c_int32), ("NQ", ctypes.c_int32), ("NKV", ctypes.c_int32), ("e", ctypes.c_int32),
+                ("tp", ctypes.c_int32), ("pad", ctypes.c_int32), ("lin", ctypes.c_double * 10),
+                ("flops", ctypes.c_double), ("bw", ctypes.c_double), ("link_bw", ctypes.c_double)]
+
+
+class SimResult(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("pad", ctypes.c_int32), ("steps", ctypes.c_int64),
+                ("preemptions", ctypes.c_int64), ("batch_entries", ctypes.c_int64),
+                ("processed_tokens", ctypes.c_int64), ("sum_U", ctypes.c_int64), ("prefill_entries", ctypes.c_int64),
+                ("idle_jumps", ctypes.c_int64), ("makespan", ctypes.c_double * SIM_MAX_COST),
+                ("mean_latency", ctypes.c_double * SIM_MAX_COST), ("mean_ttft", ctypes.c_double * SIM_MAX_COST),
+                ("mean_tpot", ctypes.c_double * SIM_MAX_COST)]
+
+
+class SimRequestOut(ctypes.Structure):
+    _fields_ = [("t_first", ctypes.c_void_p), ("t_done", ctypes.c_void_p), ("n_preempt", ctypes.c_void_p),
+                ("refill_tokens", ctypes.c_void_p)]
+
+
+RESULT_DTYPE = np.dtype([("status", "<i4"), ("pad", "<i4"), ("steps", "<i8"), ("preemptions", "<i8"),
+                         ("batch_entries", "<i8"), ("processed_tokens", "<i8"), ("sum_U", "<i8"),
+                         ("prefill_entries", "<i8"), ("idle_jumps", "<i8"), ("makespan", "<f8", (4,)),
+                         ("mean_latency", "<f8", (4,)), ("mean_ttft", "<f8", (4,)), ("mean_tpot", "<f8", (4,))])
+assert RESULT_DTYPE.itemsize == ctypes.sizeof(SimResult)
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libsimsweep.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not found: run `python -m paper_2411_07447_b200.build` "
+                               "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        L.sim_sweep.restype = ctypes.c_int
+        L.sim_sweep.argtypes = [P(SimConfig), ctypes.c_int32, P(SimWorkload), ctypes.c_int32, P(SimCostModel),
+                                ctypes.c_int32, P(SimResult), SimRequestOut, ctypes.c_int32]
+        L.sim_sweep_device.restype = ctypes.c_int
+        L.sim_sweep_device.argtypes = [P(SimConfig), ctypes.c_int32, P(ctypes.c_int32), ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, SimRequestOut,
+                                       ctypes.c_void_p]
+        L.sim_request_rows.restype = ctypes.c_int
+        L.sim_request_rows.argtypes = [P(SimConfig), ctypes.c_int32, P(SimWorkload), ctypes.c_int32,
+                                       P(ctypes.c_int64), P(ctypes.c_int64)]
+        L.sim_strerror.restype = ctypes.c_char_p
+        L.sim_strerror.argtypes = [ctypes.c_int]
+        L.sim_version.restype = ctypes.c_char_p
+        L.sim_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = ["sim_sweep", "sim_sweep_device", "sim_request_rows", "sim_strerror", "sim_version"]
+
+
+def strerror(code: int) -> str:
+    return lib().sim_strerror(code).decode()
+
+
+class SimError(RuntimeError):
+    pass
+
+
+def _check(rc: int):
+    if rc < 0:
+        raise SimError(f"simsweep error {rc}: {strerror(rc)}")
+    return rc
+
+
+# ------------------------------------------------------------ cost models
+def load_cost_models(path: str | None = None) -> dict:
+    """Name -> SimCostModel from the frozen data file (input data, Q23)."""
+    path = path or os.path.join(ROOT, "data", "cost_models.json")
+    with open(path) as fh:
+        doc = json.load(fh)
+    out = {}
+    for c in doc["cost_models"]:
+        m = SimCostModel()
+        m.mode = int(c["mode"])
+        m.layers, m.h, m.f, m.H = int(c["layers"]), int(c["h"]), int(c["f"]), int(c["H"])
+        m.NQ, m.NKV, m.e, m.tp = int(c["NQ"]), int(c["NKV"]), int(c["e"]), int(c["tp"])
+        for j, v in enumerate(c["lin"]):
+            m.lin[j] = float(v)
+        m.flops, m.bw, m.link_bw = float(c["flops"]), float(c["bw"]), float(c["link_bw"])
+        out[c["name"]] = m
+    return out
+
+
+def unit_cost(d: float = 1.0) -> SimCostModel:
+    """Every batch costs d seconds (linear model, a0 = d, one layer)."""
+    m = SimCostModel()
+    m.mode, m.layers, m.h, m.f, m.H, m.NQ, m.NKV, m.e, m.tp = 0, 1, 1, 1, 1, 1, 1, 2, 1
+    m.lin[0] = d
+    m.flops = m.bw = m.link_bw = 1.0
+    return m
+
+
+# ------------------------------------------------------------ configs
+def make_config(order, hybrid, chunked, replacement, C, M, S=4096, workload=0, cost=(0,),
+                max_steps=10_000_000) -> SimConfig:
+    c = SimConfig()
+    c.order, c.hybrid, c.chunked, c.replacement = int(order), int(bool(hybrid)), int(bool(chunked)), int(replacement)
+    c.S, c.workload, c.C, c.M, c.max_steps = int(S), int(workload), int(C), int(M), int(max_steps)
+    cost = list(cost)
+    assert 1 <= len(cost) <= SIM_MAX_COST
+    c.n_cost = len(cost)
+    for k, v in enumerate(cost):
+        c.cost[k] = int(v)
+    return c
+
+
+def preset_config(name: str, M: int, S: int = 4096, workload: int = 0, cost=(0,), **kw) -> SimConfig:
+    p = _presets.preset(name, S=S)
+    return make_config(p["order"], p["hybrid"], p["chunked"], p["replacement"], C=kw.pop("C", p["C"]), M=M, S=S,
+                       workload=workload, cost=cost, **kw)
+
+
+@dataclass
+class SweepResult:
+    results: np.ndarray  # RESULT_DTYPE [n_cfgs]
+    t_first: np.ndarray  # float64 [tim_rows]
+    t_done: np.ndarray
+    n_preempt: np.ndarray  # int64 [rows]
+    refill: np.ndarray
+    row_off: np.ndarray
+    tim_off: np.ndarray
+    n_of: np.ndarray  # n of each config's workload
+    k_of: np.ndarray  # n_cost of each config
+
+    def status(self, i: int) -> str:
+        return STATUS.get(int(self.results["status"][i]), "?")
+
+    def request_times(self, i: int):
+        """-> (t_first [K, n], t_done [K, n]) of config i."""
+        n, K, o = int(self.n_of[i]), int(self.k_of[i]), int(self.tim_off[i])
+        return self.t_first[o:o + K * n].reshape(K, n), self.t_done[o:o + K * n].reshape(K, n)
+
+    def request_counts(self, i: int):
+        n, o = int(self.n_of[i]), int(self.row_off[i])
+        return self.n_preempt[o:o + n], self.refill[o:o + n]
+
+
+def _offsets(cfgs, wls):
+    n_of = np.array([wls[c.workload].n for c in cfgs], np.int64)
+    k_of = np.array([c.n_cost for c in cfgs], np.int64)
+    row_off = np.concatenate([[0], np.cumsum(n_of)[:-1]]).astype(np.int64)
+    tim_off = np.concatenate([[0], np.cumsum(n_of * k_of)[:-1]]).astype(np.int64)
+    return n_of, k_of, row_off, tim_off, int(n_of.sum()), int((n_of * k_of).sum())
+
+
+def _cfg_array(cfgs):
+    return (SimConfig * len(cfgs))(*cfgs)
+
+
+def _cm_array(cms):
+    return (SimCostModel * len(cms))(*cms)
+
+
+def sim_sweep(cfgs, wls: list[Workload], cms, device: int = -1) -> SweepResult:
+    """Host-buffer entry point: validates, copies in, simulates, copies out (blocking)."""
+    cfgs = list(cfgs)
+    n_of, k_of, row_off, tim_off, rows, trows = _offsets(cfgs, wls)
+    keep = []
+    warr = (SimWorkload * len(wls))()
+    for j, w in enumerate(wls):
+        I = np.ascontiguousarray(w.I, np.int32)
+        O = np.ascontiguousarray(w.O, np.int32)
+        T = np.ascontiguousarray(w.T, np.float64)
+        keep += [I, O, T]
+        warr[j].n = int(I.shape[0])
+        warr[j].I, warr[j].O, warr[j].T = I.ctypes.data, O.ctypes.data, T.ctypes.data
+    res = np.zeros(len(cfgs), RESULT_DTYPE)
+    tf = np.zeros(trows, np.float64)
+    td = np.zeros(trows, np.float64)
+    npre = np.zeros(rows, np.int64)
+    rf = np.zeros(rows, np.int64)
+    req = SimRequestOut(tf.ctypes.data, td.ctypes.data, npre.ctypes.data, rf.ctypes.data)
+    rc = lib().sim_sweep(_cfg_array(cfgs), len(cfgs), warr, len(wls), _cm_array(cms), len(cms),
+                         res.ctypes.data_as(ctypes.POINTER(SimResult)), req, int(device))
+    _check(rc)
+    return SweepResult(res, tf, td, npre, rf, row_off, tim_off, n_of, k_of)
+
+
+class DeviceSweep:
+    """All inputs and outputs resident in device memory (torch tensors); launch()
+    enqueues sim_sweep_device on a stream without synchronizing."""
+
+    def __init__(self, cfgs, wls: list[Workload], cms, device="cuda", order=None):
+        import torch
+
+        self.torch = torch
+        self.cfgs = list(cfgs)
+        self.wls = wls
+        self.dev = torch.device(device)
+        n_of, k_of, row_off, tim_off, rows, trows = _offsets(self.cfgs, wls)
+        self.n_of, self.k_of, self.row_off_np, self.tim_off_np = n_of, k_of, row_off, tim_off
+        self.h_cfgs = _cfg_array(self.cfgs)
+        self.h_wls_n = (ctypes.c_int32 * len(wls))(*[w.n for w in wls])
+        u8 = lambda a: torch.from_numpy(np.frombuffer(bytes(a), np.uint8).copy()).to(self.dev)
+        self.d_cfgs = u8(self.h_cfgs)
+        self.d_cms = u8(_cm_array(cms))
+        self.n_cms = len(cms)
+        self.I = torch.from_numpy(np.concatenate([np.asarray(w.I, np.int32) for w in wls])).to(self.dev)
+        self.O = torch.from_numpy(np.concatenate([np.asarray(w.O, np.int32) for w in wls])).to(self.dev)
+        self.T = torch.from_numpy(np.concatenate([np.asarray(w.T, np.float64) for w in wls])).to(self.dev)
+        warr = (SimWorkload * len(wls))()
+        off = 0
+        for j, w in enumerate(wls):
+            warr[j].n = w.n
+            warr[j].I = self.I.data_ptr() + 4 * off
+            warr[j].O = self.O.data_ptr() + 4 * off
+            warr[j].T = self.T.data_ptr() + 8 * off
+            off += w.n
+        self.d_wls = u8(warr)
+        if order is None:
+            order = np.arange(len(self.cfgs))
+        self.d_order = torch.from_numpy(np.ascontiguousarray(order, np.int32)).to(self.dev)
+        self.d_row_off = torch.from_numpy(row_off).to(self.dev)
+        self.d_tim_off = torch.from_numpy(tim_off).to(self.dev)
+        self.d_results = torch.zeros(len(self.cfgs) * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=self.dev)
+        self.t_first = torch.zeros(trows, dtype=torch.float64, device=self.dev)
+        self.t_done = torch.zeros(trows, dtype=torch.float64, device=self.dev)
+        self.n_preempt = torch.zeros(rows, dtype=torch.int64, device=self.dev)
+        self.refill = torch.zeros(rows, dtype=torch.int64, device=self.dev)
+
+    def launch(self, stream=None) -> int:
+        """Enqueue the sweep on `stream` (torch.cuda.Stream or None = current); returns #kernel launches."""
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.dev)
+        req = SimRequestOut(self.t_first.data_ptr(), self.t_done.data_ptr(), self.n_preempt.data_ptr(),
+                            self.refill.data_ptr())
+        rc = lib().sim_sweep_device(self.h_cfgs, len(self.cfgs), self.h_wls_n, self.d_cfgs.data_ptr(),
+                                    self.d_wls.data_ptr(), self.d_cms.data_ptr(), self.n_cms,
+                                    self.d_order.data_ptr(), self.d_row_off.data_ptr(), self.d_tim_off.data_ptr(),
+                                    self.d_results.data_ptr(), req, ctypes.c_void_p(s.cuda_stream))
+        return _check(rc)
+
+    def fetch(self) -> SweepResult:
+        res = np.frombuffer(self.d_results.cpu().numpy().tobytes(), RESULT_DTYPE).copy()
+        return SweepResult(res, self.t_first.cpu().numpy(), self.t_done.cpu().numpy(), self.n_preempt.cpu().numpy(),
+                           self.refill.cpu().numpy(), self.row_off_np, self.tim_off_np, self.n_of, self.k_of)
+
+
+def lpt_order(cfgs, wls) -> np.ndarray:
+    """Longest-processing-time-first launch order from a step-count estimate."""
+    est = []
+    for c in cfgs:
+        w = wls[c.workload]
+        I = np.asarray(w.I, np.float64)
+        O = np.asarray(w.O, np.float64)
+        Meff = float(max(c.M, 1)) if c.M >= 0 else 1e18
+        est.append(O.max() + float(((I + 0.5 * O) * O).sum()) / Meff + float(I.sum()) / float(c.C))
+    return np.argsort(-np.asarray(est), kind="stable").astype(np.int32)

@@ -1,0 +1,99 @@
+"""The C-ABI library builds, loads and exports every symbol include/simsweep.h
+declares; struct layouts agree between the header (compiled with gcc) and the
+ctypes binding.  No compute calls (no GPU here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2411_07447_b200 import build, simsweep
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "simsweep.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    build.build()
+    return simsweep.lib()
+
+
+def declared_functions():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(sim_\w+)\s*\(", txt, re.M)))
+
+
+def test_exports_every_declared_symbol(L):
+    decl = declared_functions()
+    assert set(decl) == set(simsweep.EXPORTED_SYMBOLS)
+    for name in decl:
+        assert hasattr(L, name), name
+    nm = subprocess.run(["nm", "-D", "--defined-only", simsweep.LIB_PATH], capture_output=True, text=True).stdout
+    for name in decl:
+        assert re.search(rf"\bT {name}\b", nm), name
+
+
+def test_struct_layout_matches_header(tmp_path):
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "simsweep.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(sim_config_t), '
+                   'sizeof(sim_workload_t), sizeof(sim_cost_model_t), sizeof(sim_result_t), '
+                   'sizeof(sim_request_out_t), offsetof(sim_config_t, n_cost), offsetof(sim_result_t, makespan));'
+                   'return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    want = [ctypes.sizeof(simsweep.SimConfig), ctypes.sizeof(simsweep.SimWorkload),
+            ctypes.sizeof(simsweep.SimCostModel), ctypes.sizeof(simsweep.SimResult),
+            ctypes.sizeof(simsweep.SimRequestOut), simsweep.SimConfig.n_cost.offset,
+            simsweep.SimResult.makespan.offset]
+    assert got == want
+    assert got[0] == 72
+
+
+def test_version_and_strerror(L):
+    assert b"sm_100a" in L.sim_version()
+    assert simsweep.strerror(-1).startswith("invalid")
+    assert simsweep.strerror(-5).startswith("no sm_100")
+
+
+def test_request_rows_host_helper(L):
+    from paper_2411_07447_b200 import workloads
+    wls = [workloads.fixed(4, 4, 10), workloads.fixed(2, 2, 3)]
+    cfgs = [simsweep.preset_config("vllm", 100, workload=0, cost=(0, 1)),
+            simsweep.preset_config("sarathi", 100, workload=1)]
+    warr = (simsweep.SimWorkload * 2)()
+    for j, w in enumerate(wls):
+        warr[j].n = w.n
+    r, t = ctypes.c_int64(), ctypes.c_int64()
+    rc = L.sim_request_rows((simsweep.SimConfig * 2)(*cfgs), 2, warr, 2, ctypes.byref(r), ctypes.byref(t))
+    assert rc == 0 and (r.value, t.value) == (13, 23)
+    cfgs[0].workload = 7
+    assert L.sim_request_rows((simsweep.SimConfig * 2)(*cfgs), 2, warr, 2, ctypes.byref(r), ctypes.byref(t)) == -1
+
+
+def test_no_gpu_fails_loudly(L):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2411_07447_b200 import workloads
+    wl = workloads.fixed(2, 2, 4)
+    with pytest.raises(simsweep.SimError, match="no sm_100"):
+        simsweep.sim_sweep([simsweep.preset_config("vllm", 100)], [wl], [simsweep.unit_cost()])
+
+
+def test_invalid_calls_rejected_before_device(L):
+    from paper_2411_07447_b200 import workloads
+    wl = workloads.fixed(2, 2, 4)
+    bad = simsweep.preset_config("vllm", 100)
+    bad.order = 9
+    with pytest.raises(simsweep.SimError, match="invalid argument"):
+        simsweep.sim_sweep([bad], [wl], [simsweep.unit_cost()])
+    wl2 = workloads.Workload(np.array([1, 1], np.int32), np.array([1, 1], np.int32), np.array([1.0, 0.0]))
+    with pytest.raises(simsweep.SimError, match="invalid workload"):
+        simsweep.sim_sweep([simsweep.preset_config("vllm", 100)], [wl2], [simsweep.unit_cost()])
+    with pytest.raises(simsweep.SimError, match="cost"):
+        simsweep.sim_sweep([simsweep.preset_config("vllm", 100, cost=(3,))], [wl], [simsweep.unit_cost()])

@@ -1,0 +1,146 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by
+element, on the same seeded inputs.  Integers bit-exact, per-request fp64
+times 0 ULP, means within 1e-9 relative."""
+import numpy as np
+import pytest
+
+from paper_2411_07447_b200 import presets, simsweep, workloads
+from parity import compare, run_case_list
+
+pytestmark = pytest.mark.gpu
+P = presets
+A100 = ["llama3-8b_a100_linear"]
+UNIT = [("unit", 1.0)]
+
+
+def cfg(order, hybrid, chunked, repl, C, M, S=4096, **kw):
+    return simsweep.make_config(order, hybrid, chunked, repl, C=C, M=M, S=S, **kw)
+
+
+def assert_parity(cases):
+    g, ors = run_case_list(cases)
+    bad = []
+    for i in range(len(cases)):
+        bad += compare(g, ors, i, label=f"case{i}:{cases[i][1].name}")
+    assert bad == [], "\n".join(bad[:40])
+    return g, ors
+
+
+def W(I, O, T=None, name="hand"):
+    T = [0.0] * len(I) if T is None else T
+    return workloads.Workload(np.array(I, np.int32), np.array(O, np.int32), np.array(T, np.float64), name)
+
+
+def test_hand_traces():
+    cases = [
+        (cfg(0, 0, 0, 0, 4096, 6), W([2, 2], [4, 4]), UNIT),  # A nrf
+        (cfg(0, 0, 0, 1, 4096, 6), W([2, 2], [4, 4]), UNIT),  # A srf
+        (cfg(0, 0, 0, 0, 4096, 12), W([1, 1, 5], [6, 6, 4]), UNIT),  # B nrf
+        (cfg(0, 0, 0, 1, 4096, 12), W([1, 1, 5], [6, 6, 4]), UNIT),  # B srf
+        (cfg(1, 1, 1, 0, 4, -1), W([6, 3], [2, 2]), UNIT),  # C
+        (cfg(0, 0, 0, 0, 4, -1), W([6, 3], [2, 2]), UNIT),  # C never fits
+        (cfg(0, 0, 0, 0, 4096, -1), W([2, 1], [2, 1], [0.0, 1.5]), UNIT),  # D1
+        (cfg(0, 0, 0, 0, 4096, -1), W([1, 1], [1, 1], [0.0, 5.0]), UNIT),  # D2
+        (cfg(0, 0, 0, 0, 4096, -1), W([2, 1], [2, 1], [0.0, 2.0]), UNIT),  # D3
+        (cfg(0, 0, 0, 2, 1000, 1000), W([10] * 5, [3] * 5), UNIT),  # SRF+Hist trace
+        (cfg(0, 0, 0, 0, 4096, 8), W([4, 2, 3], [1, 1, 1]), UNIT),  # Fig. 3
+    ]
+    for (o_, hy, ch) in [(0, 0, 0), (0, 1, 0), (1, 1, 0), (1, 0, 0), (1, 1, 1)]:  # E
+        cases.append((cfg(o_, hy, ch, 0, 4, -1), W([2, 3], [3, 1]), UNIT))
+    g, _ = assert_parity(cases)
+    assert g.status(5) == "never_fits"
+
+
+def test_config1_and_presets():
+    wl = workloads.fixed(16, 16, 32)
+    cases = [(simsweep.preset_config(nm + sfx, 100_000), wl, A100) for nm in P.GRID_PRESETS for sfx in ("", "-srf")]
+    g, _ = assert_parity(cases)
+    assert all(int(g.results["steps"][i]) == 16 for i in range(len(cases)))
+
+
+def test_status_codes_and_edges():
+    cases = [
+        (cfg(0, 0, 0, 0, 4096, -1), W([4096], [2]), UNIT),  # too long
+        (cfg(0, 0, 0, 0, 4096, 10), W([8], [4]), UNIT),  # never fits M
+        (cfg(1, 1, 1, 0, 4, -1), W([4096], [1]), UNIT),  # chunked long prompt, C = 4
+        (cfg(0, 0, 0, 0, 4096, -1, max_steps=2), W([1], [5]), UNIT),  # max steps
+        (cfg(1, 1, 1, 1, 1, 50), W([3, 5, 7], [4, 4, 4]), UNIT),  # C = 1
+        (cfg(0, 0, 0, 0, 4096, 100_000), W([1], [1]), A100),  # W = 1, O = 1
+        (cfg(0, 1, 0, 1, 4096, 100_000), workloads.fixed(1, 1, 1024), A100),  # all O = 1
+        (cfg(1, 1, 1, 0, 512, -1), workloads.fixed(1024, 1024, 1024), A100),  # infinite M, max grid cell
+        (cfg(0, 0, 0, 1, 4096, 2047), workloads.fixed(1024, 1024, 3), A100),  # M = exactly one peak
+    ]
+    g, _ = assert_parity(cases)
+    assert [g.status(i) for i in range(4)] == ["too_long", "never_fits", "ok", "max_steps"]
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_random_small(block):
+    orders_repl = [(o_, r) for o_ in range(5) for r in range(3)]
+    cases = []
+    for seed in range(block * 100, block * 100 + 100):
+        rng = np.random.default_rng(seed)
+        Wn = int(rng.integers(1, 40))
+        online = bool(rng.integers(0, 2))
+        wl = workloads.random_small(seed, Wn, max_len=int(rng.integers(2, 33)), online=online, S=128)
+        o_, r = orders_repl[seed % len(orders_repl)]
+        chunked = int(rng.integers(0, 2))
+        hybrid = int(rng.integers(0, 2)) if o_ < 2 else 1
+        peak = int((wl.I.astype(int) + wl.O - 1).max())
+        C = int(rng.integers(1, 3 * peak + 1)) if chunked else int(rng.integers(peak, 3 * peak + 1))
+        M = -1 if rng.random() < 0.1 else int(rng.integers(peak, 5 * peak + 1))
+        names = A100 if rng.random() < 0.5 else ["llama3-70b_h100x4_theoretical"]
+        cases.append((cfg(o_, hybrid, chunked, r, C, M, S=128), wl, names))
+    assert_parity(cases)
+
+
+GRID_SAMPLE = [(1, 1), (1, 1024), (1024, 1), (16, 16), (64, 256), (256, 64), (512, 1024), (1024, 1024),
+               (4, 512), (128, 1024)]
+
+
+@pytest.mark.parametrize("name", P.GRID_PRESETS)
+def test_grid_w1024_sample(name):
+    # BASELINE configs[1] at full size (W = 1024), in the launch configuration bench.py times
+    cases = []
+    for sfx in ("", "-srf"):
+        for (I, O) in GRID_SAMPLE:
+            cases.append((simsweep.preset_config(name + sfx, 100_000), workloads.fixed(I, O, 1024), A100))
+    assert_parity(cases)
+
+
+def test_offline_four_cost_models():
+    names = ["llama3-8b_a100_linear", "llama3-8b_h100_theoretical", "llama3-70b_a100x4_linear",
+             "llama3-70b_h100x4_theoretical"]
+    cases = [(simsweep.preset_config(nm, 100_000), workloads.fixed(64, 256, 1024), names)
+             for nm in ("vllm", "sarathi-srf")]
+    assert_parity(cases)
+
+
+def test_online_longform_and_hist():
+    cases = []
+    for seed in (0, 1):
+        wl = workloads.longform(seed)
+        for nm in ("vllm", "sarathi"):
+            for sfx in ("", "-srf", "-srf-hist"):
+                cases.append((simsweep.preset_config(nm + sfx, 100_000, S=131072), wl, A100))
+    assert_parity(cases)
+
+
+def test_online_70b_what_ifs():
+    wl = workloads.longform(3)
+    cases = []
+    for cm in ("llama3-70b_a100x4_linear", "llama3-70b_h100x4_theoretical"):
+        for sfx in ("", "-srf"):
+            for M in (100_000, -1):
+                cases.append((simsweep.preset_config("vllm" + sfx, M, S=131072), wl, [cm]))
+    assert_parity(cases)
+
+
+def test_hetero_rank():
+    cases = []
+    for gen in (lambda s: workloads.sharegpt(s), lambda s: workloads.table_qa(s, long_context=True),
+                lambda s: workloads.text_to_sql(s), lambda s: workloads.mix(("LILO", "SILO"), 1024, s)):
+        wl = gen(0)
+        for nm in ("rank-org", "rank-i", "rank-o"):
+            cases.append((simsweep.preset_config(nm, 100_000), wl, A100))
+    assert_parity(cases)
