@@ -114,6 +114,7 @@ typedef struct {
   int64_t sum_U;            /* sum_j KV holdings right after admission (kv usage = sum_U / (steps M)) */
   int64_t prefill_entries;  /* entries in the prefill phase */
   int64_t idle_jumps;       /* clock jumps to the next arrival (not steps) */
+  int64_t visits;           /* sum over GetNextBatch calls of |P| (candidates visited, Alg. 1 line 9) */
   double makespan[SIM_MAX_COST];     /* max t_done - min T, per cost model */
   double mean_latency[SIM_MAX_COST]; /* mean t_done - T */
   double mean_ttft[SIM_MAX_COST];    /* mean t_first - T */

@@ -50,7 +50,7 @@ class OracleSummary(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("pad", ctypes.c_int32), ("steps", ctypes.c_int64),
                 ("preemptions", ctypes.c_int64), ("batch_entries", ctypes.c_int64),
                 ("processed_tokens", ctypes.c_int64), ("sum_U", ctypes.c_int64), ("prefill_entries", ctypes.c_int64),
-                ("idle_jumps", ctypes.c_int64), ("makespan", ctypes.c_double * 4),
+                ("idle_jumps", ctypes.c_int64), ("visits", ctypes.c_int64), ("makespan", ctypes.c_double * 4),
                 ("mean_latency", ctypes.c_double * 4), ("mean_ttft", ctypes.c_double * 4),
                 ("mean_tpot", ctypes.c_double * 4)]
 
@@ -136,7 +136,7 @@ class OracleResult:
 
     def __getattr__(self, k):
         if k in ("steps", "preemptions", "batch_entries", "processed_tokens", "sum_U", "prefill_entries",
-                 "idle_jumps"):
+                 "idle_jumps", "visits"):
             return int(getattr(self.summary, k))
         if k in ("makespan", "mean_latency", "mean_ttft", "mean_tpot"):
             return list(getattr(self.summary, k))

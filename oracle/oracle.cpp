@@ -333,6 +333,7 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
     }
 
     // GetNextBatch (steps 2-4)
+    for (auto& grp : groups) out->visits += (int64_t)grp.size();
     std::vector<Entry> B;
     int64_t tok = 0;
     int bphase = PH_NONE;
@@ -489,7 +490,7 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
   }
   if (status != OR_OK) {  // failed simulations: zero-filled rows
     int st = status;
-    std::memset(out, 0, sizeof(*out));
+    std::memset(out, 0, sizeof(*out));  // (visits too)
     out->status = st;
     return 0;
   }

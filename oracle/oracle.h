@@ -40,7 +40,7 @@ typedef struct {
 
 typedef struct {
   int32_t status, pad;
-  int64_t steps, preemptions, batch_entries, processed_tokens, sum_U, prefill_entries, idle_jumps;
+  int64_t steps, preemptions, batch_entries, processed_tokens, sum_U, prefill_entries, idle_jumps, visits;
   double makespan[4], mean_latency[4], mean_ttft[4], mean_tpot[4];
 } oracle_summary_t;
 

@@ -27,16 +27,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
-        cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB] + SRC
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    """profile=True builds libsimsweep_prof.so with per-phase cycle counters (tools/probe.py)."""
+    lib = LIB.replace(".so", "_prof.so") if profile else LIB
+    if force or profile or needs_build():
+        cmd = ([NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + (["-DSIMSWEEP_PROFILE"] if profile else [])
+               + ["-o", lib] + SRC)
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc failed building libsimsweep.so")
         if verbose:
             sys.stderr.write(r.stdout + r.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -28,7 +28,7 @@
 namespace simsweep {
 
 constexpr uint8_t ST_WAIT = 1, ST_RUN = 2, ST_DONE = 3, ST_MASK = 3;
-constexpr uint8_t F_FILLED = 4, F_INB = 8, F_PRE = 16, F_FIRST = 32;
+constexpr uint8_t F_FILLED = 4, F_INB = 8, F_PRE = 16, F_FIRST = 32, F_LAST = 64;
 constexpr int PH_DEC = 0, PH_PRE = 1;
 constexpr int IPT = 4;  // items per thread in block-wide passes (blocked layout)
 constexpr int NOBRK = 0x7fffffff;
@@ -56,7 +56,9 @@ struct Scal {
   double clock[SIM_MAX_COST];
   sim_cost_model_t cm[SIM_MAX_COST];
   long long U, tok, Rsum, seq;
-  long long steps, preempt, entries, processed, sumU, pentries, idle;
+  long long steps, preempt, entries, processed, sumU, pentries, idle, visits;
+  long long runL, runMD, last_np, last_nd;
+  int runEx;
   long long pref[4];  // exclusive prefixes (c, dKV, admitted-waiting, SRF+Hist rem) at the break
   long long featsum[16];
   long long wred[16][16];  // per-warp partial feature sums

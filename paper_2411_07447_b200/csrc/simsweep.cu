@@ -16,6 +16,22 @@ namespace simsweep {
 
 enum { K_NONE = 0, K_MARK = 1, K_EVENT = 2 };
 
+#ifdef SIMSWEEP_PROFILE  // phase cycle counters of thread 0 (tools/probe.py); not in the product build
+constexpr int PROF_MAX_CFG = 8192;
+__device__ long long g_prof[PROF_MAX_CFG][16];
+#define PROF_MARK(i)                  \
+  if (tid == 0) {                     \
+    long long _t = clock64();         \
+    prof[i] += _t - prof_last;        \
+    prof_last = _t;                   \
+  }
+#define PROF_CNT(i, v) \
+  if (tid == 0) prof[i] += (v);
+#else
+#define PROF_MARK(i)
+#define PROF_CNT(i, v)
+#endif
+
 __host__ __device__ inline int variant_of(int n) { return n <= 1024 ? 0 : 1; }
 
 template <int NT>
@@ -102,7 +118,7 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
   if (tid == 0) {
     for (int k = 0; k < SIM_MAX_COST; k++) S.clock[k] = 0.0;
     S.U = S.tok = S.Rsum = S.seq = 0;
-    S.steps = S.preempt = S.entries = S.processed = S.sumU = S.pentries = S.idle = 0;
+    S.steps = S.preempt = S.entries = S.processed = S.sumU = S.pentries = S.idle = S.visits = 0;
     S.next = S.new_next = S.lo = S.n_done = S.n_run = S.n_running = 0;
     S.nrank = 0;
     S.status = 0;
@@ -111,8 +127,13 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
   if (tid < K) S.cm[tid] = p.cms[cfg.cost[tid]];
   for (int i = tid; i < 18 * 18; i += NT) S.hist[i] = 0;
   __syncthreads();
+#ifdef SIMSWEEP_PROFILE
+  long long prof[16] = {0};
+  long long prof_last = clock64();
+#endif
 
   for (;;) {
+    PROF_MARK(10);
     // ---- a2: GetNewRequests (Alg. 1 line 3): all T <= clock (inclusive, Q21) ----
     if (tid == 0) {
       int a = S.next, b = n;
@@ -157,6 +178,7 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
       s_fl[sl] = ST_WAIT;
     }
     __syncthreads();
+    PROF_MARK(0);
     // ---- a3: GroupRequests (step 1) ----
     if (rank) {  // one group sorted by (key, T, id) (App. D, Q20, Q37)
       for (int idx = nx0 + tid; idx < nx1; idx += NT) s_rank[nrank + idx - nx0] = (int16_t)(idx & (CAP - 1));
@@ -222,8 +244,10 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
       S.n_running = nrun;
       S.any_pre = 0;
       S.nrank = nrank;
+      S.visits += nP;
     }
 
+    PROF_MARK(1);
     // ---- a4-a8: GetNextBatch (steps 2-4), block-parallel rounds ----
     auto preempt = [&](int v) {  // thread 0 only (refill P:1570)
       const int m = s_m[v];
@@ -292,6 +316,7 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
       __syncthreads();
       const int pos = S.pos;
       if (pos >= nP) break;
+      PROF_CNT(6, 1);
       const long long tok = S.tok, U = S.U, Rs = S.Rsum;
       const int bph = S.bphase;
       const bool anyRun0 = S.n_running > 0;
@@ -416,6 +441,7 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
         S.n_running += (int)a2;
         S.Rsum += a3;
         if (real) {
+          PROF_CNT(7, 1);
           handle(cand(b));
           S.pos = b + 1;
         } else {
@@ -441,6 +467,7 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
       continue;
     }
 
+    PROF_MARK(2);
     // ---- a9: batch latency from exact integer features ----
     {
       long long v[9 + SIM_MAX_COST];
@@ -492,24 +519,28 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
         S.entries += f.np + f.nd;
         S.processed += f.N;
         S.pentries += f.np;
+        S.last_np = f.np;
+        S.last_nd = f.nd;
       }
       __syncthreads();
     }
 
+    PROF_MARK(3);
     // ---- a10: Process(B): token generation (Eq. 6), completions free KVs at batch end (Q14) ----
     {
-      long long freed = 0;
-      int ndone = 0;
+      long long freed = 0, mdn = 0;
+      int ndone = 0, minrem = NOBRK;
       for (int q = tid; q < nP; q += NT) {
         const int sl = cand(q);
         uint8_t fl = s_fl[sl];
         if (fl & F_INB) {
-          const int c = s_c[sl], m0 = s_m[sl], I = s_I[sl];
+          const int c = s_c[sl], m0 = s_m[sl], I = s_I[sl], O = s_O[sl];
           int g = s_g[sl];
           const int s = I + g, m = m0 + c;
           s_m[sl] = m;
           s_c[sl] = 0;
-          fl &= ~F_INB;
+          fl = (fl & ~F_INB) | F_LAST;
+          bool done = false;
           if (c == s - m0) {
             g++;
             s_g[sl] = g;
@@ -519,28 +550,136 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
               fl |= F_FIRST;
               for (int k = 0; k < K; k++) tf[(long long)k * n + idx] = S.clock[k];
             }
-            if (g == s_O[sl]) {
+            if (g == O) {
+              done = true;
               fl = (fl & ~ST_MASK) | ST_DONE;
               for (int k = 0; k < K; k++) td[(long long)k * n + idx] = S.clock[k];
               freed += max(s_res[sl], m);
               ndone++;
-              if (hist) atomicAdd(&S.hist[bucket_of(I) * 18 + bucket_of(s_O[sl])], 1);
+              if (hist) atomicAdd(&S.hist[bucket_of(I) * 18 + bucket_of(O)], 1);
             }
           }
+          if (!done) {
+            minrem = min(minrem, O - g);
+            mdn += m;
+          }
           s_fl[sl] = fl;
-        } else if (fl & F_PRE) {
-          s_fl[sl] = fl & ~F_PRE;
+        } else if (fl & (F_PRE | F_LAST)) {
+          s_fl[sl] = fl & ~(F_PRE | F_LAST);
         }
       }
-      const long long fr = block_sum_ll<NT>(freed, S);
-      const long long nd = block_sum_ll<NT>((long long)ndone, S);
+      freed = warp_sum(freed);
+      mdn = warp_sum(mdn);
+      ndone = warp_sum(ndone);
+      minrem = (int)__reduce_min_sync(0xffffffffu, (unsigned)minrem);
+      if (lane == 0) S.wred[wid][0] = freed, S.wred[wid][1] = mdn, S.wred[wid][2] = ndone, S.wred[wid][3] = minrem;
+      __syncthreads();
       if (tid == 0) {
+        long long fr = 0, md = 0, nd = 0, mr = NOBRK;
+        for (int w = 0; w < NW; w++) fr += S.wred[w][0], md += S.wred[w][1], nd += S.wred[w][2], mr = min(mr, S.wred[w][3]);
         S.U -= fr;
         S.n_done += (int)nd;
         S.n_running -= (int)nd;
+        // Steady decode run: step j had only decodes, no admission, preemption or completion.  Then step
+        // j+1 repeats it exactly (waiting candidates were rejected for reasons that persist: KV and SRF+Hist
+        // deferral are monotone in U, token/hybrid rejections are unchanged) until a completion, the KV
+        // limit (U + k n_d <= M) or an arrival.  Those steps are charged below without re-forming batches.
+        long long L = 0;
+        if (nd == 0 && S.last_np == 0 && !S.any_pre && S.last_nd > 0) {
+          L = mr;
+          if (finiteM) L = min(L, (M - S.U) / S.last_nd);
+          L = min(L, cfg.max_steps - S.steps);
+        }
+        S.runL = L;
+        S.runMD = md;
+      }
+      __syncthreads();
+      const long long L = S.runL;
+      if (L > 0) {
+        PROF_CNT(9, L);
+        // s_new + s_tmp half of the union area is free (no new admissions this step); the P segments
+        // (s_wl, s_pl) in the other half are still needed below
+        double* dbuf = reinterpret_cast<double*>(s_new);
+        constexpr int DB = CAP / 2;  // doubles available
+        const int cmax = min(NT, DB / K);
+        const long long ndd = S.last_nd, MD = S.runMD, U0 = S.U;
+        long long E = 0;
+        while (E < L) {
+          const int chunk = (int)min((long long)cmax, L - E);
+          if (tid < chunk) {  // features of run step E+tid+1 are affine in the step index
+            Feat f;
+            f.N = ndd, f.np = 0, f.c2 = 0, f.mc = 0, f.cp = 0, f.mp = 0, f.pcm = 0, f.nd = ndd;
+            f.md = MD + (E + tid) * ndd;
+            for (int k = 0; k < SIM_MAX_COST; k++) f.pceil[k] = 0;
+            for (int k = 0; k < K; k++) dbuf[k * cmax + tid] = batch_time(S.cm[k], f, k);
+          }
+          __syncthreads();
+          if (tid == 0) {  // the clock chain stays sequential: one fp64 add per step, as in the oracle (Q36)
+            int ex = chunk;
+            if (nx1 < n) {  // online (K == 1): stop before a step that would start at/after an arrival (Q21)
+              const double Tn = wl.T[nx1];
+              double clk = S.clock[0];
+              for (int t = 0; t < chunk; t++) {
+                if (Tn <= clk) {
+                  ex = t;
+                  break;
+                }
+                clk = dadd(clk, dbuf[t]);
+              }
+              S.clock[0] = clk;
+            } else {
+              for (int k = 0; k < K; k++) {
+                double clk = S.clock[k];
+                for (int t = 0; t < chunk; t++) clk = dadd(clk, dbuf[k * cmax + t]);
+                S.clock[k] = clk;
+              }
+            }
+            S.runEx = ex;
+          }
+          __syncthreads();
+          const int ex = S.runEx;
+          E += ex;
+          if (ex < chunk) break;
+        }
+        if (tid == 0) {
+          S.steps += E;
+          S.sumU += E * U0 + ndd * (E * (E + 1) / 2);
+          S.entries += E * ndd;
+          S.processed += E * ndd;
+          S.visits += E * nP;
+          S.U = U0 + E * ndd;
+        }
+        long long fr2 = 0;
+        int nd2 = 0;
+        if (E > 0) {
+          for (int q = tid; q < nP; q += NT) {
+            const int sl = cand(q);
+            uint8_t fl = s_fl[sl];
+            if (!(fl & F_LAST)) continue;
+            const int m = s_m[sl] + (int)E, g = s_g[sl] + (int)E, O = s_O[sl];
+            s_m[sl] = m;
+            s_g[sl] = g;
+            if (g == O) {  // completes at the last run step
+              const int idx = lo + ((sl - lo) & (CAP - 1));
+              s_fl[sl] = (fl & ~ST_MASK) | ST_DONE;
+              for (int k = 0; k < K; k++) td[(long long)k * n + idx] = S.clock[k];
+              fr2 += max(s_res[sl], m);
+              nd2++;
+              if (hist) atomicAdd(&S.hist[bucket_of(s_I[sl]) * 18 + bucket_of(O)], 1);
+            }
+          }
+        }
+        fr2 = block_sum_ll<NT>(fr2, S);
+        const long long nd2t = block_sum_ll<NT>((long long)nd2, S);
+        if (tid == 0) {
+          S.U -= fr2;
+          S.n_done += (int)nd2t;
+          S.n_running -= (int)nd2t;
+        }
       }
     }
 
+    PROF_MARK(4);
     // ---- run list (retention order) for the next step ----
     {
       int16_t* nrl = S.cur ? s_runA : s_runB;
@@ -559,6 +698,7 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
           if (key(nrl[q]) > key(nrl[q + 1])) ok = 0;
         ok = __syncthreads_and(ok);
         if (!ok) {
+          PROF_CNT(8, 1);
           for (int q = tid; q < cnt; q += NT) s_keys[q] = key(nrl[q]);
           block_bitonic<NT>(s_keys, cnt);
           for (int q = tid; q < cnt; q += NT) nrl[q] = (int16_t)(s_keys[q] & 0xFFF);
@@ -575,8 +715,13 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
         S.lo = l;
       }
       __syncthreads();
+      PROF_MARK(5);
     }
   }
+#ifdef SIMSWEEP_PROFILE
+  if (tid == 0 && ci < PROF_MAX_CFG)
+    for (int i = 0; i < 16; i++) g_prof[ci][i] = prof[i];
+#endif
 
   // ---- a11: metrics ----
   const int st = S.status == -1 ? SIM_S_OK : S.status;
@@ -630,6 +775,7 @@ __global__ void __launch_bounds__(NT) sim_kernel(KParams p) {
     r.sum_U = S.sumU;
     r.prefill_entries = S.pentries;
     r.idle_jumps = S.idle;
+    r.visits = S.visits;
     for (int k = K; k < SIM_MAX_COST; k++) r.makespan[k] = r.mean_latency[k] = r.mean_ttft[k] = r.mean_tpot[k] = 0.0;
   }
 }
@@ -655,6 +801,12 @@ static int check_cuda(cudaError_t e) { return e == cudaSuccess ? 0 : SIM_ECUDA; 
 using namespace simsweep;
 
 extern "C" {
+
+#ifdef SIMSWEEP_PROFILE
+int sim_debug_read(int64_t* out, int32_t n_cfgs) {
+  return cudaMemcpyFromSymbol(out, g_prof, sizeof(long long) * 16 * (size_t)n_cfgs) == cudaSuccess ? 0 : SIM_ECUDA;
+}
+#endif
 
 const char* sim_version(void) { return "simsweep 0.1 (sm_100a, CTA-per-simulation)"; }
 

@@ -19,7 +19,7 @@ from .workloads import Workload
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "libsimsweep.so")
+LIB_PATH = os.environ.get("SIMSWEEP_LIB") or os.path.join(PKG, "libsimsweep.so")
 
 SIM_MAX_COST = 4
 STATUS = {0: "ok", 1: "too_long", 2: "never_fits", 3: "max_steps", 4: "deadlock", 5: "capacity"}
@@ -48,7 +48,8 @@ class SimResult(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("pad", ctypes.c_int32), ("steps", ctypes.c_int64),
                 ("preemptions", ctypes.c_int64), ("batch_entries", ctypes.c_int64),
                 ("processed_tokens", ctypes.c_int64), ("sum_U", ctypes.c_int64), ("prefill_entries", ctypes.c_int64),
-                ("idle_jumps", ctypes.c_int64), ("makespan", ctypes.c_double * SIM_MAX_COST),
+                ("idle_jumps", ctypes.c_int64), ("visits", ctypes.c_int64),
+                ("makespan", ctypes.c_double * SIM_MAX_COST),
                 ("mean_latency", ctypes.c_double * SIM_MAX_COST), ("mean_ttft", ctypes.c_double * SIM_MAX_COST),
                 ("mean_tpot", ctypes.c_double * SIM_MAX_COST)]
 
@@ -60,7 +61,7 @@ class SimRequestOut(ctypes.Structure):
 
 RESULT_DTYPE = np.dtype([("status", "<i4"), ("pad", "<i4"), ("steps", "<i8"), ("preemptions", "<i8"),
                          ("batch_entries", "<i8"), ("processed_tokens", "<i8"), ("sum_U", "<i8"),
-                         ("prefill_entries", "<i8"), ("idle_jumps", "<i8"), ("makespan", "<f8", (4,)),
+                         ("prefill_entries", "<i8"), ("idle_jumps", "<i8"), ("visits", "<i8"), ("makespan", "<f8", (4,)),
                          ("mean_latency", "<f8", (4,)), ("mean_ttft", "<f8", (4,)), ("mean_tpot", "<f8", (4,))])
 assert RESULT_DTYPE.itemsize == ctypes.sizeof(SimResult)
 
@@ -201,8 +202,26 @@ def _cm_array(cms):
     return (SimCostModel * len(cms))(*cms)
 
 
-def sim_sweep(cfgs, wls: list[Workload], cms, device: int = -1) -> SweepResult:
-    """Host-buffer entry point: validates, copies in, simulates, copies out (blocking)."""
+def alloc_outputs(cfgs, wls, alloc=np.zeros):
+    """Output arrays for sim_sweep (alloc may return pinned host memory)."""
+    n_of, k_of, row_off, tim_off, rows, trows = _offsets(list(cfgs), wls)
+    res = np.frombuffer(alloc(len(cfgs) * RESULT_DTYPE.itemsize, np.uint8).data, RESULT_DTYPE)
+    return (res, alloc(trows, np.float64), alloc(trows, np.float64), alloc(rows, np.int64), alloc(rows, np.int64))
+
+
+def io_bytes(cfgs, wls, n_cms):
+    """(H2D, D2H) bytes one sim_sweep call moves (for the e2e accounting)."""
+    n_of, k_of, row_off, tim_off, rows, trows = _offsets(list(cfgs), wls)
+    n = len(cfgs)
+    h2d = (ctypes.sizeof(SimConfig) * n + ctypes.sizeof(SimWorkload) * len(wls) + ctypes.sizeof(SimCostModel) * n_cms
+           + 4 * n + 16 * n + sum(16 * w.n for w in wls))
+    d2h = RESULT_DTYPE.itemsize * n + 16 * trows + 16 * rows
+    return int(h2d), int(d2h)
+
+
+def sim_sweep(cfgs, wls: list[Workload], cms, device: int = -1, out=None) -> SweepResult:
+    """Host-buffer entry point: validates, copies in, simulates, copies out (blocking).
+    `out` = alloc_outputs(...) to reuse (e.g. pinned) output buffers."""
     cfgs = list(cfgs)
     n_of, k_of, row_off, tim_off, rows, trows = _offsets(cfgs, wls)
     keep = []
@@ -214,11 +233,7 @@ def sim_sweep(cfgs, wls: list[Workload], cms, device: int = -1) -> SweepResult:
         keep += [I, O, T]
         warr[j].n = int(I.shape[0])
         warr[j].I, warr[j].O, warr[j].T = I.ctypes.data, O.ctypes.data, T.ctypes.data
-    res = np.zeros(len(cfgs), RESULT_DTYPE)
-    tf = np.zeros(trows, np.float64)
-    td = np.zeros(trows, np.float64)
-    npre = np.zeros(rows, np.int64)
-    rf = np.zeros(rows, np.int64)
+    res, tf, td, npre, rf = out if out is not None else alloc_outputs(cfgs, wls)
     req = SimRequestOut(tf.ctypes.data, td.ctypes.data, npre.ctypes.data, rf.ctypes.data)
     rc = lib().sim_sweep(_cfg_array(cfgs), len(cfgs), warr, len(wls), _cm_array(cms), len(cms),
                          res.ctypes.data_as(ctypes.POINTER(SimResult)), req, int(device))

@@ -13,7 +13,7 @@ import numpy as np
 import oracle as o
 from paper_2411_07447_b200 import simsweep
 
-INT_FIELDS = ["steps", "preemptions", "batch_entries", "processed_tokens", "sum_U", "prefill_entries", "idle_jumps"]
+INT_FIELDS = ["steps", "preemptions", "batch_entries", "processed_tokens", "sum_U", "prefill_entries", "idle_jumps", "visits"]
 REL_TOL = 1e-9
 
 _OCMS = None
