@@ -50,7 +50,7 @@ enum {
 };
 /* call-level errors */
 enum {
-  SIM_EINVAL = -1,    /* NULL pointer, n <= 0, bad enum, C < 1, S < 1, n_cost not 1..4 */
+  SIM_EINVAL = -1,    /* NULL pointer, n <= 0, bad enum, C not in [1, 2^30], M > 2^30, S not in [1, 2^18), n_cost not 1..4 */
   SIM_EWORKLOAD = -2, /* I < 1, O < 1, T not sorted, or T != 0 with n_cost > 1 */
   SIM_ECOST = -3,     /* cost-model index out of range or bad cost-model fields */
   SIM_ECUDA = -4,     /* a CUDA runtime error (device, allocation, launch) */
@@ -70,8 +70,8 @@ typedef struct {
   int32_t replacement; /* SIM_NRF / SIM_SRF / SIM_SRF_HIST */
   int32_t S;           /* model context size; requests need I+O-1 <= S */
   int32_t workload;    /* index into the workload table */
-  int64_t C;           /* token limit per batch (>= 1) */
-  int64_t M;           /* KV-cache capacity in tokens; < 0 = infinite (what-if) */
+  int64_t C;           /* token limit per batch, 1 .. 2^30 */
+  int64_t M;           /* KV-cache capacity in tokens, <= 2^30; < 0 = infinite (what-if) */
   int64_t max_steps;   /* livelock guard (>= 1) */
   int32_t n_cost;      /* 1..4 cost models charged on the same schedule; > 1 only for offline (all T = 0) */
   int32_t cost[SIM_MAX_COST]; /* indices into the cost-model table; the clock of cost[0] drives arrivals */

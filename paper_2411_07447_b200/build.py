@@ -8,7 +8,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "simsweep.cu")]
-DEPS = SRC + [os.path.join(PKG, "csrc", "sim_kernel.cuh"), os.path.join(ROOT, "include", "simsweep.h")]
+HDRS = [os.path.join(PKG, "csrc", h) for h in ("sim_kernel.cuh", "sim_step.cuh")]
+DEPS = SRC + HDRS + [os.path.join(ROOT, "include", "simsweep.h")]
 LIB = os.path.join(PKG, "libsimsweep.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -30,7 +30,6 @@ namespace simsweep {
 constexpr uint8_t ST_WAIT = 1, ST_RUN = 2, ST_DONE = 3, ST_MASK = 3;
 constexpr uint8_t F_FILLED = 4, F_INB = 8, F_PRE = 16, F_FIRST = 32, F_LAST = 64;
 constexpr int PH_DEC = 0, PH_PRE = 1;
-constexpr int IPT = 4;  // items per thread in block-wide passes (blocked layout)
 constexpr int NOBRK = 0x7fffffff;
 
 struct KParams {
@@ -55,17 +54,21 @@ struct Feat {
 struct Scal {
   double clock[SIM_MAX_COST];
   sim_cost_model_t cm[SIM_MAX_COST];
-  long long U, tok, Rsum, seq;
+  long long U, seq;
   long long steps, preempt, entries, processed, sumU, pentries, idle, visits;
-  long long runL, runMD, last_np, last_nd;
+  long long runL, runMD, last_nd;
   int runEx;
-  long long pref[4];  // exclusive prefixes (c, dKV, admitted-waiting, SRF+Hist rem) at the break
+  long long pref[6];  // exclusive prefixes (c, dKV, admitted-waiting, admitted, SRF+Hist rem) at the break
   long long featsum[16];
-  long long wred[16][16];  // per-warp partial feature sums
-  int next, new_next, lo, n_done, n_run, n_running, nW, nP, len0, n_new, nrank;
-  int pos, bphase, vt, status, brk, any_pre, cur;
+  long long wred[16][18];  // per-warp partials of the process pass
+  int next, new_next, lo, n_done, n_run, nW, nrank, minSW, n_ev, n_vic, nB, nRd;
+  int cf_red[32][4];
+  int vt, status, any_pre, cur, wbuilt;
+  int w_dirty, p_dirty, r_dirty, o_dirty, rank_dirty, removals;
+  long long r_Rs;  // scalars handed back by thread 0 after a break
+  int r_tok, r_U, r_seq, r_new, r_running, r_bph, r_nB;
   int wmin[32];
-  int wsum[32][4];
+  int wsum[32][6];
   int wcnt[32];
   int hist[18 * 18];
   int pred[18];
@@ -170,15 +173,16 @@ __device__ __forceinline__ int block_excl_scan(int v, Scal& S, int* tot) {
   return off + x - v;
 }
 
-// stable stream compaction of positions [0, L) satisfying pred into out[base...]; returns count
-template <int NT, typename Pred, typename Val>
+// stable stream compaction of positions [0, L) satisfying pred into out[...]; returns the count.
+// Ends with a barrier: the output is visible to the whole block.
+template <int NT, int IPT_, typename Pred, typename Val>
 __device__ int block_compact(int L, Pred pred, Val val, int16_t* out, Scal& S) {
   int total = 0;
-  for (int base = 0; base < L; base += NT * IPT) {
+  for (int base = 0; base < L; base += NT * IPT_) {
     int flags = 0, cnt = 0;
 #pragma unroll
-    for (int j = 0; j < IPT; j++) {
-      int q = base + threadIdx.x * IPT + j;
+    for (int j = 0; j < IPT_; j++) {
+      int q = base + threadIdx.x * IPT_ + j;
       if (q < L && pred(q)) {
         flags |= 1 << j;
         cnt++;
@@ -187,11 +191,91 @@ __device__ int block_compact(int L, Pred pred, Val val, int16_t* out, Scal& S) {
     int tot;
     int w = total + block_excl_scan<NT>(cnt, S, &tot);
 #pragma unroll
-    for (int j = 0; j < IPT; j++)
-      if (flags >> j & 1) out[w++] = (int16_t)val(base + threadIdx.x * IPT + j);
+    for (int j = 0; j < IPT_; j++)
+      if (flags >> j & 1) out[w++] = (int16_t)val(base + threadIdx.x * IPT_ + j);
     total += tot;
   }
+  __syncthreads();
   return total;
+}
+
+// as block_compact, plus the minimum of key(val(q)) over the selected positions (INT_MAX if none)
+template <int NT, int IPT_, typename Pred, typename Val, typename Key>
+__device__ int block_compact_min(int L, Pred pred, Val val, Key key, int16_t* out, Scal& S, int* minv) {
+  int total = 0, mn = 0x7fffffff;
+  for (int base = 0; base < L; base += NT * IPT_) {
+    int flags = 0, cnt = 0;
+#pragma unroll
+    for (int j = 0; j < IPT_; j++) {
+      int q = base + threadIdx.x * IPT_ + j;
+      if (q < L && pred(q)) {
+        flags |= 1 << j;
+        cnt++;
+        mn = min(mn, key(val(q)));
+      }
+    }
+    int tot;
+    int w = total + block_excl_scan<NT>(cnt, S, &tot);
+#pragma unroll
+    for (int j = 0; j < IPT_; j++)
+      if (flags >> j & 1) out[w++] = (int16_t)val(base + threadIdx.x * IPT_ + j);
+    total += tot;
+  }
+  mn = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
+  if ((threadIdx.x & 31) == 0) S.wmin[threadIdx.x >> 5] = mn;
+  __syncthreads();
+  int m = 0x7fffffff;
+#pragma unroll
+  for (int w = 0; w < NT / 32; w++) m = min(m, S.wmin[w]);
+  __syncthreads();
+  *minv = m;
+  return total;
+}
+
+// stable partition of positions [0, L): pred-true items (in order), then the others (in order).
+// One 2-component scan when L fits one pass.  Ends with a barrier.
+template <int NT, int IPT_, typename Pred, typename Val>
+__device__ int block_partition(int L, Pred pred, Val val, int16_t* out, Scal& S) {
+  if (L > NT * IPT_) {
+    const int nt = block_compact<NT, IPT_>(L, pred, val, out, S);
+    block_compact<NT, IPT_>(L, [&](int q) { return !pred(q); }, val, out + nt, S);
+    return nt;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int flags = 0, ct = 0, cf = 0;
+#pragma unroll
+  for (int j = 0; j < IPT_; j++) {
+    const int q = threadIdx.x * IPT_ + j;
+    if (q < L) {
+      if (pred(q))
+        flags |= 1 << j, ct++;
+      else
+        cf++;
+    }
+  }
+  int xt = ct, xf = cf;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int yt = __shfl_up_sync(0xffffffffu, xt, o), yf = __shfl_up_sync(0xffffffffu, xf, o);
+    if (lane >= o) xt += yt, xf += yf;
+  }
+  if (lane == 31) S.wsum[wid][0] = xt, S.wsum[wid][1] = xf;
+  __syncthreads();
+  int ot = xt - ct, of = xf - cf, tt = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; w++) {
+    const int a = S.wsum[w][0], b = S.wsum[w][1];
+    if (w < wid) ot += a, of += b;
+    tt += a;
+  }
+  of += tt;
+#pragma unroll
+  for (int j = 0; j < IPT_; j++) {
+    const int q = threadIdx.x * IPT_ + j;
+    if (q < L) out[(flags >> j & 1) ? ot++ : of++] = (int16_t)val(q);
+  }
+  __syncthreads();
+  return tt;
 }
 
 // ascending bitonic sort of keys[0, L) (padded with ~0 to a power of two <= CAP)
@@ -229,12 +313,12 @@ __device__ __forceinline__ T warp_sum(T v) {
 template <int NT, int CAP>
 struct Smem {
   static constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-  static constexpr size_t off_int = align16(sizeof(Scal));
-  static constexpr size_t n_int = 7;  // m g res seq I O c
-  static constexpr size_t off_rpos = off_int + n_int * 4 * CAP;
-  static constexpr size_t off_fl = off_rpos + 2 * CAP;
-  static constexpr size_t off_lists = align16(off_fl + CAP);  // run0 run1 rank (int16)
-  static constexpr size_t off_union = align16(off_lists + 3 * 2 * CAP);  // 8 B/slot: wl pl newadm tmp | u64 keys
+  static constexpr size_t off_rec = align16(sizeof(Scal));          // int4 {I, g, m, res} per slot
+  static constexpr size_t off_int = off_rec + 16 * CAP;             // O, seq, c (int32)
+  static constexpr size_t off_rpos = off_int + 3 * 4 * CAP;         // position in the run list (int16)
+  static constexpr size_t off_fl = off_rpos + 2 * CAP;              // flags (uint8)
+  static constexpr size_t off_lists = align16(off_fl + CAP);        // runA runB rank wl pl blist (int16)
+  static constexpr size_t off_union = align16(off_lists + 6 * 2 * CAP);  // new ev vic | dbuf (upper half) | u64 keys
   static constexpr size_t bytes = off_union + 8 * CAP;
 };
 

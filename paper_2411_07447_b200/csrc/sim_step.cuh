@@ -1,0 +1,1145 @@
+// sim_step.cuh -- the step kernel body (included by simsweep.cu).
+//
+// One CTA = one simulation of Algorithm 1.  Request state
+// lives in shared memory as a ring of CAP slots (slot = request id mod CAP):
+// a 16-byte record {I, g, m, reserved} (one LDS.128 per candidate), O,
+// admission seq, c of the current batch, and a flag byte.  Per step:
+//   (1) a2 arrivals (thread 0 binary search over the sorted T) + slot init
+//   (2) a3 GroupRequests: run list (retention order) and Sarathi's
+//       decode/prefill split are rebuilt only when the previous step dirtied
+//       them; the waiting list (index order) is built lazily, only when a round
+//       reaches the waiting group and the group is not skippable
+//   (3) a4-a8 GetNextBatch in block-parallel rounds.  The step scalars (tok, U,
+//       seq, ...) live in registers, identical in every thread.  A round loads
+//       all its candidates first (ILP), classifies them against the current
+//       (tok, U), prefix-scans (tokens, KV delta, waiting admissions,
+//       admissions, SRF+Hist remainders), and admits the prefix before the first
+//       "break" -- a candidate the scan cannot decide: a preemption (running
+//       decode short of KV), a cumulative KV / deferral / token failure, a chunk
+//       crop, or the first admission when hybrid batching is off.  No break: 2
+//       barriers.  A break is resolved literally by thread 0 (+2 barriers).
+//       The waiting group is skipped whole when even its smallest request fails
+//       a monotone check (hybrid phase, KV, token budget).
+//   (4) a9+a10 one pass over the batch list B: Eq. (6) state update + exact
+//       integer features; warp REDUX reductions; thread 0 evaluates the cost
+//       models, advances the clocks, decides a steady decode run
+//   (5) t_first/t_done of this step's events; the steady decode run
+//   (6) run-list maintenance only when needed
+#pragma once
+
+namespace simsweep {
+
+enum { K_NONE = 0, K_MARK = 1, K_EVENT = 2 };
+constexpr int WARP_MAX = 256;  // at most this many candidates left in a group: warp-level admission
+
+template <int NT, int CAP, int IPT_>
+__global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams p) {
+  using L = Smem<NT, CAP>;
+  constexpr int NW = NT / 32;
+  constexpr int CH = NT * IPT_;  // candidates per round
+  constexpr unsigned FM = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char smem[];
+  Scal& S = *reinterpret_cast<Scal*>(smem);
+  int4* s_rec = reinterpret_cast<int4*>(smem + L::off_rec);  // {I, g, m, res}
+  int32_t* s_O = reinterpret_cast<int32_t*>(smem + L::off_int);
+  int32_t* s_seq = s_O + CAP;  // admission sequence number (Q6)
+  int32_t* s_c = s_seq + CAP;  // c of the current batch
+  int16_t* s_rpos = reinterpret_cast<int16_t*>(smem + L::off_rpos);
+  uint8_t* s_fl = smem + L::off_fl;
+  int16_t* s_runA = reinterpret_cast<int16_t*>(smem + L::off_lists);
+  int16_t* s_runB = s_runA + CAP;
+  int16_t* s_rank = s_runB + CAP;
+  int16_t* s_wl = s_rank + CAP;  // waiting list (index order)
+  int16_t* s_pl = s_wl + CAP;    // Sarathi split of the run list (decodes, then prefills)
+  int16_t* s_bl = s_pl + CAP;    // the batch B in admission order
+  int16_t* s_new = reinterpret_cast<int16_t*>(smem + L::off_union);  // admitted from waiting this step
+  int16_t* s_ev = s_new + CAP;                                          // first-token / completion events
+  int16_t* s_vic = s_ev + CAP;                                          // preempted this step
+  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem + L::off_union);
+  double* s_dbuf = reinterpret_cast<double*>(smem + L::off_union + 4 * CAP);  // CAP/2 doubles (vic | pad)
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int ci = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
+  const sim_config_t cfg = p.cfgs[ci];
+  const sim_workload_t wl = p.wls[cfg.workload];
+  const int n = wl.n;
+  if (variant_of(n) != p.variant) return;
+  const int K = cfg.n_cost;
+  const int M = cfg.M >= 0 ? (int)cfg.M : 0, C = (int)cfg.C;  // host-validated < 2^30
+  const bool finiteM = cfg.M >= 0, hybrid = cfg.hybrid != 0, chunked = cfg.chunked != 0;
+  const int order = cfg.order;
+  const bool srf = cfg.replacement != SIM_NRF;
+  const bool hist = cfg.replacement == SIM_SRF_HIST && finiteM;
+  const bool rank = order >= SIM_ORDER_RANK_ORG;
+  const long long row0 = p.row_off[ci], tim0 = p.tim_off[ci];
+  double* tf = p.req.t_first + tim0;
+  double* td = p.req.t_done + tim0;
+  unsigned long long* npre = reinterpret_cast<unsigned long long*>(p.req.n_preempt + row0);
+  unsigned long long* refill = reinterpret_cast<unsigned long long*>(p.req.refill_tokens + row0);
+
+  for (int i = tid; i < n; i += NT) {
+    npre[i] = 0;
+    refill[i] = 0;
+  }
+  for (int x = tid; x < K * n; x += NT) {
+    tf[x] = 0.0;
+    td[x] = 0.0;
+  }
+  // ---- a1: per-simulation validation (Q35) ----
+  int bad_long = 0, bad_fit = 0;
+  for (int i = tid; i < n; i += NT) {
+    long long pk = (long long)wl.I[i] + wl.O[i] - 1;  // peak KV usage
+    bad_long |= pk > cfg.S;
+    bad_fit |= (finiteM && pk > cfg.M) || (!chunked && pk > cfg.C);
+  }
+  bad_long = __syncthreads_or(bad_long);
+  bad_fit = __syncthreads_or(bad_fit);
+  if (bad_long || bad_fit) {
+    if (tid == 0) {
+      sim_result_t r;
+      memset(&r, 0, sizeof(r));
+      r.status = bad_long ? SIM_S_TOO_LONG : SIM_S_NEVER_FITS;
+      p.results[ci] = r;
+    }
+    return;
+  }
+  bool anyTheo = false;
+  for (int k = 0; k < K; k++) anyTheo |= p.cms[cfg.cost[k]].mode == 1;
+  if (tid == 0) {
+    for (int k = 0; k < SIM_MAX_COST; k++) S.clock[k] = 0.0;
+    S.U = S.seq = 0;
+    S.steps = S.preempt = S.entries = S.processed = S.sumU = S.pentries = S.idle = S.visits = 0;
+    S.next = S.new_next = S.lo = S.n_done = S.n_run = 0;
+    S.nrank = S.nW = S.minSW = S.n_ev = S.n_vic = S.nB = 0;
+    S.r_dirty = S.o_dirty = S.rank_dirty = S.removals = S.wbuilt = 0;
+    S.status = 0;
+    S.cur = 0;
+    S.w_dirty = S.p_dirty = 1;
+  }
+  if (tid < K) S.cm[tid] = p.cms[cfg.cost[tid]];
+  for (int i = tid; i < 18 * 18; i += NT) S.hist[i] = 0;
+  __syncthreads();
+#ifdef SIMSWEEP_PROFILE
+  long long prof[16] = {0};
+  long long prof_last = clock64();
+#endif
+
+  for (;;) {
+    PROF_MARK(10);
+    // ---- (1) a2: GetNewRequests (Alg. 1 line 3): all T <= clock, inclusive (Q21) ----
+    if (tid == 0) {
+      int a = S.next, b = n;
+      const double clk = S.clock[0];
+      while (a < b) {
+        int mid = (a + b) >> 1;
+        if (wl.T[mid] <= clk)
+          a = mid + 1;
+        else
+          b = mid;
+      }
+      S.new_next = a;
+      if (S.n_done == n)
+        S.status = -1;
+      else if (a - S.lo > CAP)
+        S.status = SIM_S_CAPACITY;
+      else if (S.steps >= cfg.max_steps)
+        S.status = SIM_S_MAX_STEPS;
+    }
+    __syncthreads();
+    if (S.status) break;
+    const int nx0 = S.next, nx1 = S.new_next, lo = S.lo;
+    const bool arrived = nx1 > nx0;
+    const int nrun = S.n_run;
+    int16_t* run = S.cur ? s_runB : s_runA;
+    int nrank = S.nrank;
+    if (rank && (arrived || S.rank_dirty) && nrank > 0) {  // drop finished entries before slot reuse
+      nrank = block_compact<NT, IPT_>(
+          nrank, [&](int q) { return (s_fl[s_rank[q]] & ST_MASK) != ST_DONE; }, [&](int q) { return s_rank[q]; },
+          s_new, S);
+      for (int q = tid; q < nrank; q += NT) s_rank[q] = s_new[q];
+    }
+    for (int idx = nx0 + tid; idx < nx1; idx += NT) {
+      const int sl = idx & (CAP - 1);
+      s_rec[sl] = make_int4(wl.I[idx], 0, 0, 0);
+      s_O[sl] = wl.O[idx];
+      s_seq[sl] = 0;
+      s_c[sl] = 0;
+      s_fl[sl] = ST_WAIT;
+    }
+    __syncthreads();
+    PROF_MARK(0);
+    // ---- (2) a3: GroupRequests (step 1) ----
+    if (rank && arrived) {  // one group sorted by (key, T, id) (App. D, Q20, Q37)
+      for (int idx = nx0 + tid; idx < nx1; idx += NT) s_rank[nrank + idx - nx0] = (int16_t)(idx & (CAP - 1));
+      const int nr = nrank + (nx1 - nx0);
+      __syncthreads();
+      for (int q = tid; q < nr; q += NT) {
+        const int sl = s_rank[q];
+        const unsigned idx = (unsigned)(lo + ((sl - lo) & (CAP - 1)));
+        const unsigned key = order == SIM_ORDER_RANK_I ? (unsigned)s_rec[sl].x
+                             : order == SIM_ORDER_RANK_O ? (unsigned)s_O[sl]
+                                                         : 0u;
+        s_keys[q] = ((unsigned long long)key << 32) | idx;
+      }
+      block_bitonic<NT>(s_keys, nr);
+      for (int q = tid; q < nr; q += NT) s_rank[q] = (int16_t)(s_keys[q] & (CAP - 1));
+      nrank = nr;
+      __syncthreads();
+    }
+    int nW = S.nW, minSW = S.minSW, wbuilt = S.wbuilt;
+    if (!rank && (S.w_dirty || arrived)) {  // |R_w| and its smallest s (the skip test); list built lazily
+      int cnt = 0, mn = 0x7fffffff;
+      for (int q = tid; q < nx1 - lo; q += NT) {
+        const int sl = (lo + q) & (CAP - 1);
+        if ((s_fl[sl] & ST_MASK) == ST_WAIT) {
+          const int4 r = s_rec[sl];
+          cnt++;
+          mn = min(mn, r.x + r.y);
+        }
+      }
+      cnt = (int)__reduce_add_sync(FM, (unsigned)cnt);
+      mn = (int)__reduce_min_sync(FM, (unsigned)mn);
+      if (lane == 0) S.wsum[wid][0] = cnt, S.wsum[wid][1] = mn;
+      __syncthreads();
+      nW = 0, minSW = 0x7fffffff;
+#pragma unroll
+      for (int w = 0; w < NW; w++) nW += S.wsum[w][0], minSW = min(minSW, S.wsum[w][1]);
+      wbuilt = 0;
+      __syncthreads();
+    }
+    if (order == SIM_ORDER_DECODE_FIRST && S.p_dirty) {  // {R_r^d, R_r^p, R_w}: stable split of the run list
+      const int nrd = block_partition<NT, IPT_>(
+          nrun, [&](int q) { return (s_fl[run[q]] & F_FILLED) != 0; }, [&](int q) { return run[q]; }, s_pl, S);
+      if (tid == 0) S.nRd = nrd;
+    }
+    __syncthreads();
+    const int nRd = order == SIM_ORDER_DECODE_FIRST ? S.nRd : 0;
+    const int16_t* seg0;
+    const int16_t* seg1;
+    int len0, len1;
+    if (order == SIM_ORDER_PREFILL_FIRST) {  // {R_w, R_r}
+      seg0 = s_wl, len0 = nW, seg1 = run, len1 = nrun;
+    } else if (order == SIM_ORDER_DECODE_FIRST) {
+      seg0 = s_pl, len0 = nrun, seg1 = s_wl, len1 = nW;
+    } else {
+      seg0 = s_rank, len0 = nrank, seg1 = s_rank, len1 = 0;
+    }
+    const int nP = len0 + len1;
+    auto cand = [&](int q) -> int { return q < len0 ? seg0[q] : seg1[q - len0]; };
+    // the waiting group's range in P
+    const int wbeg = order == SIM_ORDER_PREFILL_FIRST ? 0 : (order == SIM_ORDER_DECODE_FIRST ? len0 : nP);
+    const int wend = order == SIM_ORDER_PREFILL_FIRST ? nW : nP;
+
+    long long Rs = 0;
+    if (hist) {  // SRF+Hist: predictions of the current histogram; sum of remaining outputs of running requests
+      if (tid < 18) S.pred[tid] = hist_pred_row(S.hist, tid);
+      __syncthreads();
+      long long r = 0;
+      for (int q = tid; q < nrun; q += NT) {
+        const int4 rc = s_rec[run[q]];
+        const int rem = S.pred[bucket_of(rc.x)] - rc.y;
+        r += rem > 0 ? rem : 0;
+      }
+      Rs = block_sum_ll<NT>(r, S);
+    }
+    if (tid == 0) {
+      S.vt = nrun - 1;
+      S.any_pre = 0;
+      S.n_vic = 0;
+      S.nrank = nrank;
+      S.visits += nP;
+    }
+    PROF_MARK(1);
+
+    // ---- (3) a4-a8: GetNextBatch (steps 2-4) ----
+    int tok = 0, U = (int)S.U, n_new = 0, n_running = nrun, bph = -1, pos = 0, nB = 0;
+    int seq = (int)S.seq;
+
+    auto preempt = [&](int v) {  // thread 0 only (refill P:1570)
+      const int4 rc = s_rec[v];
+      U -= max(rc.w, rc.z);
+      if (hist) Rs -= max(S.pred[bucket_of(rc.x)] - rc.y, 0);
+      const int idx = lo + ((v - lo) & (CAP - 1));
+      atomicAdd(&npre[idx], 1ull);
+      atomicAdd(&refill[idx], (unsigned long long)rc.z);
+      s_rec[v] = make_int4(rc.x, rc.y, 0, 0);
+      s_fl[v] = ST_WAIT | F_PRE | (s_fl[v] & F_FIRST);
+      s_vic[S.n_vic++] = (int16_t)v;
+      n_running--;
+      S.preempt++;
+      S.any_pre = 1;
+    };
+    auto handle = [&](int sl) {  // literal sequential resolution of one candidate (thread 0)
+      uint8_t fl = s_fl[sl];
+      if (fl & F_PRE) return;  // Q9
+      const bool isW = (fl & ST_MASK) == ST_WAIT;
+      const int ph = (isW || !(fl & F_FILLED)) ? PH_PRE : PH_DEC;
+      if (!hybrid && bph >= 0 && ph != bph) return;  // step 2
+      const int4 rc = s_rec[sl];
+      const int s = rc.x + rc.y, avail = s - rc.z;
+      const int c = ph == PH_DEC ? 1 : (chunked ? min(avail, C - tok) : avail);
+      if (c == 0 || tok + c > C) return;  // token limit never preempts (Q11)
+      int rem = 0;
+      if (hist && isW) {
+        rem = max(S.pred[bucket_of(rc.x)] - rc.y, 0);
+        if (n_running > 0 && (long long)U + Rs + s + rem > M) return;  // deferred (Q31)
+      }
+      const int nh = max(isW ? s : rc.w, rc.z + c), held = isW ? 0 : max(rc.w, rc.z), delta = nh - held;
+      while (finiteM && U + delta > M) {
+        if (isW) return;  // holds no KVs: skipped (Q5)
+        const int pc = s_rpos[sl];
+        int vt = S.vt;
+        while (vt > pc) {  // lowest retention = tail of the retention-ordered run list
+          const uint8_t f = s_fl[run[vt]];
+          if (!(f & F_INB) && (f & ST_MASK) == ST_RUN) break;
+          vt--;
+        }
+        if (vt <= pc) {  // self-preemption (Q8)
+          S.vt = vt;
+          preempt(sl);
+          return;
+        }
+        preempt(run[vt]);
+        S.vt = vt - 1;
+      }
+      if (isW) {  // (re)admission reserves s = I + g (Table 2, Q13)
+        seq++;
+        s_seq[sl] = seq;
+        s_rec[sl] = make_int4(rc.x, rc.y, rc.z, s);
+        fl = ST_RUN | (fl & F_FIRST);
+        s_new[n_new++] = (int16_t)sl;
+        n_running++;
+        Rs += rem;
+      }
+      s_fl[sl] = fl | F_INB;
+      s_c[sl] = c;
+      s_bl[nB++] = (int16_t)sl;
+      U += delta;
+      tok += c;
+      if (bph < 0) bph = ph;
+    };
+
+    // Warp-level admission over [b0, b1) (warp 0 only): positions in P (overWin = false) or offsets in
+    // the waiting window (overWin = true: slot (lo + i) mod CAP, waiting and not preempted this step =
+    // R_w in index order).  32 candidates per chunk: classify, warp prefix scans, ballot the first break,
+    // admit the lanes before it, resolve the break on lane 0 (same handle() as the block path).
+    auto warp_run = [&](bool overWin, int b0, int b1) {
+      int i0 = b0;
+      while (i0 < b1) {
+        PROF_CNT(13, 1);
+        if (overWin) {  // the rest of R_w fails a monotone check: stop
+          const bool wrej = (!hybrid && bph == PH_DEC) || (finiteM && (long long)U + minSW > M) ||
+                            (chunked ? tok >= C : minSW > C - tok);
+          if (wrej) break;
+        }
+        const int i = i0 + lane;
+        int sl = -1;
+        if (i < b1) {
+          if (overWin) {
+            const int s2 = (lo + i) & (CAP - 1);
+            if ((s_fl[s2] & (ST_MASK | F_PRE)) == ST_WAIT) sl = s2;
+          } else {
+            sl = cand(i);
+          }
+        }
+        const int4 rc = s_rec[sl < 0 ? 0 : sl];
+        const uint8_t fl = s_fl[sl < 0 ? 0 : sl];
+        const bool anyRun0 = n_running > 0;
+        const bool isW = (fl & ST_MASK) == ST_WAIT;
+        const int ph = (isW || !(fl & F_FILLED)) ? PH_PRE : PH_DEC;
+        const int s = rc.x + rc.y, avail = s - rc.z;
+        const int rt0 = C - tok;
+        const int c = ph == PH_DEC ? 1 : (chunked ? min(avail, rt0) : avail);
+        int rem = 0;
+        bool ok = sl >= 0 && !(fl & F_PRE) && (hybrid || bph < 0 || ph == bph) && c >= 1 && c <= rt0;
+        if (hist && isW) {
+          rem = max(S.pred[bucket_of(rc.x)] - rc.y, 0);
+          ok = ok && !(anyRun0 && (long long)U + Rs + s + rem > M);
+        }
+        const int delta = max(isW ? s : rc.w, rc.z + c) - (isW ? 0 : max(rc.w, rc.z));
+        const bool kvfail = finiteM && U + delta > M;
+        const int kind = !ok ? K_NONE : (kvfail ? (isW ? K_NONE : K_EVENT) : K_MARK);
+        const bool mk = kind == K_MARK;
+        const int cc = mk ? (ph == PH_DEC ? 1 : avail) : 0, dd = mk ? delta : 0, ww = mk && isW, kk = mk;
+        const int rr = mk ? rem : 0;
+        int xc = cc, xd = dd, xw = ww, xk = kk, xr = rr;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int yc = __shfl_up_sync(FM, xc, o), yd = __shfl_up_sync(FM, xd, o);
+          const int yw = __shfl_up_sync(FM, xw, o), yk = __shfl_up_sync(FM, xk, o);
+          if (lane >= o) xc += yc, xd += yd, xw += yw, xk += yk;
+          if (hist) {
+            const int yr = __shfl_up_sync(FM, xr, o);
+            if (lane >= o) xr += yr;
+          }
+        }
+        const int ec = xc - cc, ed = xd - dd, ew = xw - ww, ek = xk - kk, er = xr - rr;  // exclusive
+        bool brk = false;
+        if (mk) {
+          const int pU = U + ed, rt = C - (tok + ec);
+          brk = !hybrid && bph < 0;  // the first admission fixes the batch phase (Q19)
+          if (ph == PH_PRE && chunked)
+            brk |= rt < avail;
+          else
+            brk |= cc > rt;
+          if (hist && isW) brk |= (anyRun0 || ew > 0) && (long long)pU + Rs + er + s + rem > M;
+          if (finiteM) brk |= pU + dd > M;
+        } else if (kind == K_EVENT) {
+          brk = tok + ec + 1 <= C;  // else a token reject (Q11)
+        }
+        const unsigned bm = __ballot_sync(FM, brk);
+        const int b = bm ? __ffs(bm) - 1 : 32;
+        if (mk && lane < b) {  // admitted: every check passed at its exact position
+          s_c[sl] = cc;
+          s_bl[nB + ek] = (int16_t)sl;
+          if (isW) {
+            s_seq[sl] = seq + ew + 1;
+            s_rec[sl] = make_int4(rc.x, rc.y, rc.z, s);
+            s_fl[sl] = ST_RUN | F_INB | (fl & F_FIRST);
+            s_new[n_new + ew] = (int16_t)sl;
+          } else {
+            s_fl[sl] = fl | F_INB;
+          }
+        }
+        const bool inner = b < 32;
+        const int src = inner ? b : 31;
+        const int ac = __shfl_sync(FM, inner ? ec : xc, src), ad = __shfl_sync(FM, inner ? ed : xd, src);
+        const int aw = __shfl_sync(FM, inner ? ew : xw, src), ak = __shfl_sync(FM, inner ? ek : xk, src);
+        const int ar = __shfl_sync(FM, inner ? er : xr, src);
+        tok += ac, U += ad, seq += aw, n_new += aw, n_running += aw, nB += ak, Rs += ar;
+        if (inner) {
+          PROF_CNT(14, 1);
+          const int bsl = __shfl_sync(FM, sl, b);
+          __syncwarp();
+          if (lane == 0) handle(bsl);
+          __syncwarp();
+          tok = __shfl_sync(FM, tok, 0), U = __shfl_sync(FM, U, 0), seq = __shfl_sync(FM, seq, 0);
+          n_new = __shfl_sync(FM, n_new, 0), n_running = __shfl_sync(FM, n_running, 0);
+          nB = __shfl_sync(FM, nB, 0), bph = __shfl_sync(FM, bph, 0), Rs = __shfl_sync(FM, Rs, 0);
+          i0 += b + 1;
+        } else {
+          i0 += 32;
+        }
+      }
+    };
+
+    // Closed form for a group of running decodes visited in retention order (all heads need one KV; the
+    // victim pool is the run-list tail, all running and not in B).  Head i (run position p_i) is admitted
+    // iff i <= C - tok and F + RS(p_i + 1) >= i, F = M - U, RS(q) = sum of held KVs at run positions >= q
+    // (monotone in i).  Admitting a heads evicts the minimal tail suffix [q*, n) with F + RS(q*) >= a;
+    // if head a+1 runs out of pool, everything behind it is evicted and it self-preempts (Q8).  This is
+    // exactly the sequential head/tail walk of steps (3)-(4), done in O(1) passes.
+    // pf: heads = run[0..k) (prefill-first, non-chunked: every running request decodes),
+    // else heads = s_pl[0..k) (R_r^d).  Requires nrun <= CH.
+    auto decode_group = [&](bool pf, int k) {
+      const int F = finiteM ? M - U : 0x3fffffff;
+      const int T = C - tok;
+      // (i) RS(q) by a reverse scan of held over the run list, parked in s_c[slot] (free until admission)
+      {
+        int hv[IPT_], ls = 0;
+#pragma unroll
+        for (int j = 0; j < IPT_; j++) {
+          const int q = nrun - 1 - (tid * IPT_ + j);
+          hv[j] = 0;
+          if (q >= 0) {
+            const int4 rc = s_rec[run[q]];
+            hv[j] = max(rc.w, rc.z);
+          }
+          ls += hv[j];
+        }
+        int x = ls;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FM, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) S.cf_red[wid][0] = x;
+        __syncthreads();
+        int off = x - ls;
+#pragma unroll
+        for (int w = 0; w < NW; w++) off += (w < wid) ? S.cf_red[w][0] : 0;
+#pragma unroll
+        for (int j = 0; j < IPT_; j++) {
+          const int q = nrun - 1 - (tid * IPT_ + j);
+          off += hv[j];
+          if (q >= 0) s_c[run[q]] = off;  // RS(q)
+        }
+        __syncthreads();
+      }
+      auto head = [&](int i) -> int { return pf ? run[i] : s_pl[i]; };  // 0-based head index
+      auto hpos = [&](int i) -> int { return pf ? i : s_rpos[s_pl[i]]; };
+      // (ii) a_kv = #{i : F + RS(p_i + 1) >= i} (1-based i)
+      int akv = k;
+      if (finiteM) {
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < IPT_; j++) {
+          const int i = tid * IPT_ + j;
+          if (i < k) {
+            const int p1 = hpos(i) + 1;
+            const int rsn = p1 < nrun ? s_c[run[p1]] : 0;
+            cnt += F + rsn >= i + 1;
+          }
+        }
+        cnt = (int)__reduce_add_sync(FM, (unsigned)cnt);
+        if (lane == 0) S.cf_red[wid][1] = cnt;
+        __syncthreads();
+        akv = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) akv += S.cf_red[w][1];
+      }
+      const int a = min(min(akv, T), k);
+      const bool meet = finiteM && a == akv && a < min(k, T);
+      int qs = nrun, selfp = -1;
+      if (meet) {
+        selfp = hpos(a);
+        qs = selfp + 1;
+      } else if (finiteM && F < a) {  // q* = max{q : F + RS(q) >= a} (RS strictly decreasing)
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < IPT_; j++) {
+          const int q = tid * IPT_ + j;
+          if (q < nrun) cnt += F + s_c[run[q]] >= a;
+        }
+        cnt = (int)__reduce_add_sync(FM, (unsigned)cnt);
+        if (lane == 0) S.cf_red[wid][2] = cnt;
+        __syncthreads();
+        int tot = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) tot += S.cf_red[w][2];
+        qs = tot - 1;
+      }
+      __syncthreads();  // every RS read is done before s_c is overwritten
+      // (iii) apply: evict [qs, nrun) (+ the self-preempted head), admit heads [0, a)
+      const int nvic0 = S.n_vic;
+      int ev = 0, eh = 0, er = 0;
+#pragma unroll
+      for (int j = 0; j < IPT_; j++) {
+        const int q = tid * IPT_ + j;
+        if (q < nrun && (q >= qs || q == selfp)) {
+          const int v = run[q];
+          const int4 rc = s_rec[v];
+          ev++;
+          eh += max(rc.w, rc.z);
+          if (hist) er += max(S.pred[bucket_of(rc.x)] - rc.y, 0);
+          const int idx = lo + ((v - lo) & (CAP - 1));
+          atomicAdd(&npre[idx], 1ull);
+          atomicAdd(&refill[idx], (unsigned long long)rc.z);
+          s_rec[v] = make_int4(rc.x, rc.y, 0, 0);
+          s_fl[v] = ST_WAIT | F_PRE | (s_fl[v] & F_FIRST);
+          s_vic[nvic0 + (q == selfp ? nrun - qs : q - qs)] = (int16_t)v;
+        }
+        if (q < a) {
+          const int h = head(q);
+          s_c[h] = 1;
+          s_fl[h] |= F_INB;
+          s_bl[nB + q] = (int16_t)h;
+        }
+      }
+      ev = (int)__reduce_add_sync(FM, (unsigned)ev);
+      eh = (int)__reduce_add_sync(FM, (unsigned)eh);
+      if (hist) er = (int)__reduce_add_sync(FM, (unsigned)er);
+      if (lane == 0) S.cf_red[wid][0] = ev, S.cf_red[wid][1] = eh, S.cf_red[wid][2] = er;
+      __syncthreads();
+      int tev = 0, teh = 0, ter = 0;
+#pragma unroll
+      for (int w = 0; w < NW; w++) tev += S.cf_red[w][0], teh += S.cf_red[w][1], ter += S.cf_red[w][2];
+      __syncthreads();
+      tok += a;
+      U += a - teh;
+      nB += a;
+      n_running -= tev;
+      Rs -= ter;
+      if (a > 0 && bph < 0) bph = PH_DEC;
+      if (tid == 0) {
+        S.n_vic = nvic0 + tev;
+        S.preempt += tev;
+        if (tev) S.any_pre = 1;
+        S.vt = min(S.vt, (meet ? selfp : qs) - 1);
+      }
+    };
+
+    while (pos < nP) {
+      // running decodes in closed form
+      if (order == SIM_ORDER_PREFILL_FIRST && pos == nW && nW < nP && !chunked && nrun <= CH) {
+        if (hybrid || bph != PH_PRE) decode_group(true, nrun);  // else every decode fails step 2
+        pos = nP;
+        PROF_CNT(12, 1);
+        continue;
+      }
+      if (order == SIM_ORDER_DECODE_FIRST && pos == 0 && nRd > 0 && nrun <= CH) {
+        decode_group(false, nRd);
+        pos = nRd;
+        PROF_CNT(12, 1);
+        continue;
+      }
+      {  // warp-level mode when few candidates need a decision
+        int mode = 0, lim = nP;
+        if (pos >= wbeg && pos < wend) {
+          const bool wrej = (!hybrid && bph == PH_DEC) || (finiteM && (long long)U + minSW > M) ||
+                            (chunked ? tok >= C : minSW > C - tok);
+          if (wrej) {  // every remaining waiting candidate fails a monotone check: skip the group
+            pos = wend;
+            continue;
+          }
+          if (pos == wbeg) {
+            long long amax = chunked ? (long long)(C - tok) : (long long)(C - tok) / max(minSW, 1);
+            if (finiteM) amax = min(amax, (long long)(M - U) / max(minSW, 1));
+            if (amax <= 32 || nx1 - lo <= WARP_MAX) mode = 2, lim = wend;
+          }
+        } else if (!rank) {
+          const int rend = order == SIM_ORDER_DECODE_FIRST ? len0 : nP;  // end of the running group(s)
+          if (rend - pos <= WARP_MAX) mode = 1, lim = rend;
+        }
+        if (mode) {
+          PROF_CNT(11, 1);
+          if (wid == 0) {
+            if (mode == 2)
+              warp_run(true, 0, nx1 - lo);
+            else
+              warp_run(false, pos, lim);
+            if (lane == 0) {
+              S.r_tok = tok, S.r_U = U, S.r_seq = seq, S.r_Rs = Rs, S.r_nB = nB;
+              S.r_new = n_new, S.r_running = n_running, S.r_bph = bph;
+            }
+          }
+          __syncthreads();
+          tok = S.r_tok, U = S.r_U, seq = S.r_seq, Rs = S.r_Rs, nB = S.r_nB;
+          n_new = S.r_new, n_running = S.r_running, bph = S.r_bph;
+          pos = lim;
+          __syncthreads();
+          continue;
+        }
+      }
+      if (pos >= wbeg && pos < wend) {
+        if (!wbuilt) {  // first use this step: build R_w in index order (Q1, Q2), as of the step's
+                               // start: requests preempted earlier in this step are not in it (Q9)
+          block_compact<NT, IPT_>(
+              nx1 - lo, [&](int q) { return (s_fl[(lo + q) & (CAP - 1)] & (ST_MASK | F_PRE)) == ST_WAIT; },
+              [&](int q) { return (lo + q) & (CAP - 1); }, s_wl, S);
+          wbuilt = 1;
+        }
+      }
+      PROF_CNT(6, 1);
+      const bool anyRun0 = n_running > 0;
+      int cend = min(pos + CH, nP);
+      if (!wbuilt && pos < wbeg && cend > wbeg) cend = wbeg;  // never read an unbuilt waiting list
+      if (order == SIM_ORDER_PREFILL_FIRST && pos < wend && cend > wend) cend = wend;  // R_r: closed form
+      int slv[IPT_];
+      int4 rcv[IPT_];
+      uint8_t flv[IPT_];
+#pragma unroll
+      for (int j = 0; j < IPT_; j++) {
+        const int q = pos + tid * IPT_ + j;
+        slv[j] = q < cend ? cand(q) : -1;
+      }
+#pragma unroll
+      for (int j = 0; j < IPT_; j++) {
+        const int sl = slv[j] < 0 ? 0 : slv[j];
+        rcv[j] = s_rec[sl];
+        flv[j] = s_fl[sl];
+      }
+      int kind[IPT_], cc[IPT_], dd[IPT_], rr[IPT_], av[IPT_], ss[IPT_];
+      bool ww[IPT_], pre[IPT_];
+#pragma unroll
+      for (int j = 0; j < IPT_; j++) {
+        const uint8_t fl = flv[j];
+        const int4 rc = rcv[j];
+        const bool isW = (fl & ST_MASK) == ST_WAIT;
+        const int ph = (isW || !(fl & F_FILLED)) ? PH_PRE : PH_DEC;
+        const int s = rc.x + rc.y, avail = s - rc.z;
+        const int rt = C - tok;
+        const int c = ph == PH_DEC ? 1 : (chunked ? min(avail, rt) : avail);
+        int rem = 0;
+        bool ok = slv[j] >= 0 && !(fl & F_PRE) && (hybrid || bph < 0 || ph == bph) && c >= 1 && c <= rt;
+        if (hist && isW) {
+          rem = max(S.pred[bucket_of(rc.x)] - rc.y, 0);
+          ok = ok && !(anyRun0 && (long long)U + Rs + s + rem > M);
+        }
+        const int delta = max(isW ? s : rc.w, rc.z + c) - (isW ? 0 : max(rc.w, rc.z));
+        const bool kvfail = finiteM && U + delta > M;
+        kind[j] = !ok ? K_NONE : (kvfail ? (isW ? K_NONE : K_EVENT) : K_MARK);
+        const bool mk = kind[j] == K_MARK;
+        cc[j] = mk ? (ph == PH_DEC ? 1 : avail) : 0;
+        dd[j] = mk ? delta : 0;
+        ww[j] = mk && isW;
+        rr[j] = mk ? rem : 0;
+        av[j] = avail;
+        ss[j] = s;
+        pre[j] = ph == PH_PRE;
+      }
+      int lc = 0, ld = 0, lw = 0, lk = 0, lr = 0;
+#pragma unroll
+      for (int j = 0; j < IPT_; j++) lc += cc[j], ld += dd[j], lw += ww[j], lk += kind[j] == K_MARK, lr += rr[j];
+      int xc = lc, xd = ld, xw = lw, xk = lk, xr = lr;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int yc = __shfl_up_sync(FM, xc, o), yd = __shfl_up_sync(FM, xd, o);
+        const int yw = __shfl_up_sync(FM, xw, o), yk = __shfl_up_sync(FM, xk, o);
+        if (lane >= o) xc += yc, xd += yd, xw += yw, xk += yk;
+        if (hist) {
+          const int yr = __shfl_up_sync(FM, xr, o);
+          if (lane >= o) xr += yr;
+        }
+      }
+      if (lane == 31)
+        S.wsum[wid][0] = xc, S.wsum[wid][1] = xd, S.wsum[wid][2] = xw, S.wsum[wid][3] = xk, S.wsum[wid][4] = xr;
+      __syncthreads();
+      int oc = xc - lc, od = xd - ld, ow = xw - lw, ok_ = xk - lk, orr = xr - lr;
+      int tc = 0, tdk = 0, tw = 0, tk = 0, tr = 0;
+#pragma unroll
+      for (int w = 0; w < NW; w++) {
+        const int a0 = S.wsum[w][0], a1 = S.wsum[w][1], a2 = S.wsum[w][2], a3 = S.wsum[w][3], a4 = S.wsum[w][4];
+        if (w < wid) oc += a0, od += a1, ow += a2, ok_ += a3, orr += a4;
+        tc += a0, tdk += a1, tw += a2, tk += a3, tr += a4;
+      }
+      int mybrk = NOBRK;
+      {
+        int pc = oc, pd = od, pw = ow, pr = orr;
+#pragma unroll
+        for (int j = 0; j < IPT_; j++) {
+          const int q = pos + tid * IPT_ + j;
+          if (kind[j] == K_MARK) {
+            const int ptok = tok + pc, pU = U + pd;
+            const int rt = C - ptok;
+            bool brk = !hybrid && bph < 0;  // the first admission fixes the batch phase (Q19)
+            if (pre[j] && chunked)
+              brk |= rt < av[j];  // cropped chunk (terminal) or budget exhausted
+            else
+              brk |= cc[j] > rt;
+            if (hist && ww[j]) {
+              const bool anyR = anyRun0 || pw > 0;
+              brk |= anyR && (long long)pU + Rs + pr + ss[j] + rr[j] > M;
+            }
+            if (finiteM) brk |= pU + dd[j] > M;
+            if (brk) mybrk = min(mybrk, q);
+            pc += cc[j], pd += dd[j], pw += ww[j], pr += rr[j];
+          } else if (kind[j] == K_EVENT) {
+            if (tok + pc + 1 <= C) mybrk = min(mybrk, q);  // else a token reject (Q11)
+          }
+        }
+      }
+      const int wm = (int)__reduce_min_sync(FM, (unsigned)mybrk);
+      if (lane == 0) S.wmin[wid] = wm;
+      __syncthreads();
+      int b = NOBRK;
+#pragma unroll
+      for (int w = 0; w < NW; w++) b = min(b, S.wmin[w]);
+      {
+        int pc = oc, pd = od, pw = ow, pk = ok_, pr = orr;
+#pragma unroll
+        for (int j = 0; j < IPT_; j++) {
+          const int q = pos + tid * IPT_ + j;
+          if (q == b) S.pref[0] = pc, S.pref[1] = pd, S.pref[2] = pw, S.pref[3] = pk, S.pref[4] = pr;
+          if (kind[j] == K_MARK) {
+            if (q < b) {  // admitted: every check passed at its exact position
+              const int sl = slv[j];
+              s_c[sl] = cc[j];
+              s_bl[nB + pk] = (int16_t)sl;
+              if (ww[j]) {
+                s_seq[sl] = seq + pw + 1;
+                const int4 rc = rcv[j];
+                s_rec[sl] = make_int4(rc.x, rc.y, rc.z, ss[j]);
+                s_fl[sl] = ST_RUN | F_INB | (flv[j] & F_FIRST);
+                s_new[n_new + pw] = (int16_t)sl;
+              } else {
+                s_fl[sl] = flv[j] | F_INB;
+              }
+            }
+            pc += cc[j], pd += dd[j], pw += ww[j], pk++, pr += rr[j];
+          }
+        }
+      }
+      if (b >= cend) {  // no break: every thread advances its copy of the scalars identically
+        tok += tc, U += tdk, seq += tw, n_new += tw, n_running += tw, nB += tk, Rs += tr;
+        pos = cend;
+        continue;
+      }
+      __syncthreads();  // admissions and the break's prefixes are visible
+      if (tid == 0) {
+        PROF_CNT(7, 1);
+        tok += (int)S.pref[0], U += (int)S.pref[1], seq += (int)S.pref[2], n_new += (int)S.pref[2];
+        n_running += (int)S.pref[2], nB += (int)S.pref[3], Rs += S.pref[4];
+        handle(cand(b));
+        S.r_tok = tok, S.r_U = U, S.r_seq = seq, S.r_Rs = Rs, S.r_nB = nB;
+        S.r_new = n_new, S.r_running = n_running, S.r_bph = bph;
+      }
+      __syncthreads();
+      tok = S.r_tok, U = S.r_U, seq = S.r_seq, Rs = S.r_Rs, nB = S.r_nB;
+      n_new = S.r_new, n_running = S.r_running, bph = S.r_bph;
+      pos = b + 1;
+    }
+    __syncthreads();  // admissions of the last round are visible
+    if (tok == 0) {   // B = {}: idle jump to the next arrival, not a step (Q21)
+      if (tid == 0) {
+        if (S.any_pre)
+          S.status = SIM_S_DEADLOCK;
+        else if (nx1 < n) {
+          S.clock[0] = fmax(S.clock[0], wl.T[nx1]);
+          S.idle++;
+          S.next = nx1;
+          S.w_dirty = 0;
+          S.nW = nW, S.minSW = minSW, S.wbuilt = wbuilt;
+          S.rank_dirty = 0;
+          S.p_dirty = 0;
+        } else
+          S.status = SIM_S_DEADLOCK;
+      }
+      __syncthreads();
+      if (S.status) break;
+      continue;
+    }
+    PROF_MARK(2);
+
+    // ---- (4) a9 + a10: Process(B) and the exact integer features in one pass over B ----
+    {
+      unsigned N = 0, np_ = 0, cp = 0, mp = 0, nd = 0, md = 0, freed = 0, ndone = 0, mdn = 0, nfill = 0;
+      int minrem = NOBRK;
+      long long c2 = 0, mc = 0, pcm = 0, pce[SIM_MAX_COST] = {0, 0, 0, 0};
+      for (int e = tid; e < nB; e += NT) {
+        const int sl = s_bl[e];
+        uint8_t fl = s_fl[sl];
+        const int4 rc = s_rec[sl];
+        const int c = s_c[sl], O = s_O[sl];
+        const int m0 = rc.z;
+        int g = rc.y;
+        const int s = rc.x + g, m = m0 + c;
+        N += c;
+        if (!(fl & F_FILLED)) {  // prefill entry (incl. refills and chunks)
+          np_++;
+          cp += c;
+          mp += m0;
+          c2 += (long long)c * c;
+          mc += (long long)m0 * c;
+          if (anyTheo) {
+            pcm += (long long)c * (c + m0);
+#pragma unroll
+            for (int k = 0; k < SIM_MAX_COST; k++)
+              if (k < K) {
+                const int H = S.cm[k].H;
+                pce[k] += (long long)((c + H - 1) / H) * (c + m0);
+              }
+          }
+        } else {  // decode entry (c = 1)
+          nd++;
+          md += m0;
+        }
+        fl &= ~F_INB;
+        bool done = false;
+        if (c == s - m0) {  // Eq. (6): all available tokens processed -> one token (Q18)
+          g++;
+          int evc = 0;
+          if (!(fl & F_FILLED)) nfill++;
+          fl |= F_FILLED;
+          if (!(fl & F_FIRST)) {
+            fl |= F_FIRST;
+            evc |= 1;
+          }
+          if (g == O) {
+            done = true;
+            fl = (fl & ~ST_MASK) | ST_DONE;
+            evc |= 2;
+            freed += max(rc.w, m);
+            ndone++;
+            if (hist) atomicAdd(&S.hist[bucket_of(rc.x) * 18 + bucket_of(O)], 1);
+          }
+          if (evc) s_ev[atomicAdd(&S.n_ev, 1)] = (int16_t)(sl | (evc << 12));
+        }
+        if (!done) {
+          minrem = min(minrem, O - g);
+          mdn += m;
+        }
+        s_rec[sl] = make_int4(rc.x, g, m, rc.w);
+        s_fl[sl] = fl;
+      }
+      N = __reduce_add_sync(FM, N), np_ = __reduce_add_sync(FM, np_), cp = __reduce_add_sync(FM, cp);
+      mp = __reduce_add_sync(FM, mp), nd = __reduce_add_sync(FM, nd), md = __reduce_add_sync(FM, md);
+      freed = __reduce_add_sync(FM, freed), ndone = __reduce_add_sync(FM, ndone);
+      mdn = __reduce_add_sync(FM, mdn), nfill = __reduce_add_sync(FM, nfill);
+      minrem = (int)__reduce_min_sync(FM, (unsigned)minrem);
+      if (np_ > 0) {  // prefill squares: 64-bit, only in warps holding prefill entries
+        c2 = warp_sum(c2);
+        mc = warp_sum(mc);
+        if (anyTheo) {
+          pcm = warp_sum(pcm);
+#pragma unroll
+          for (int k = 0; k < SIM_MAX_COST; k++) pce[k] = warp_sum(pce[k]);
+        }
+      }
+      if (lane == 0) {
+        long long* w = S.wred[wid];
+        w[0] = N, w[1] = np_, w[2] = cp, w[3] = mp, w[4] = nd, w[5] = md, w[6] = freed, w[7] = ndone;
+        w[8] = mdn, w[9] = nfill, w[10] = minrem, w[11] = c2, w[12] = mc, w[13] = pcm;
+        w[14] = pce[0], w[15] = pce[1], w[16] = pce[2], w[17] = pce[3];
+      }
+      // clear the preempted-this-step marks (Q9 applies within one step)
+      if (tid < 32) {
+        const int nv = S.n_vic;
+        for (int v = lane; v < nv; v += 32) s_fl[s_vic[v]] &= ~F_PRE;
+      }
+      __syncthreads();
+      if (wid == 0) {  // warp 0 folds the per-warp partials (lane z owns column z)
+        long long t = (lane == 10) ? NOBRK : 0;
+        if (lane < 18)
+          for (int w = 0; w < NW; w++) t = (lane == 10) ? min(t, S.wred[w][10]) : t + S.wred[w][lane];
+        long long tt[18];
+#pragma unroll
+        for (int z = 0; z < 18; z++) tt[z] = __shfl_sync(FM, t, z);
+        if (lane == 0) {
+          Feat f;
+          f.N = tt[0], f.np = tt[1], f.cp = tt[2], f.mp = tt[3], f.nd = tt[4], f.md = tt[5];
+          f.c2 = tt[11], f.mc = tt[12], f.pcm = tt[13];
+          f.pceil[0] = tt[14], f.pceil[1] = tt[15], f.pceil[2] = tt[16], f.pceil[3] = tt[17];
+          for (int k = 0; k < K; k++) S.clock[k] = dadd(S.clock[k], batch_time(S.cm[k], f, k));  // Q36
+          S.steps++;
+          S.sumU += U;
+          S.entries += f.np + f.nd;
+          S.processed += f.N;
+          S.pentries += f.np;
+          const long long fr = tt[6], ndn = tt[7];
+          const int Uafter = U - (int)fr;
+          S.n_done += (int)ndn;
+          // Steady decode run: step j had only decodes, no admission, preemption or completion.  Then step
+          // j+1 repeats it exactly (waiting candidates were rejected for reasons that persist: KV and SRF+Hist
+          // deferral are monotone in U, token/hybrid rejections are unchanged) until a completion, the KV
+          // limit (U + k n_d <= M) or an arrival.  Those steps are charged below without re-forming batches.
+          long long Lr = 0;
+          if (ndn == 0 && f.np == 0 && !S.any_pre && f.nd > 0) {
+            Lr = tt[10];
+            if (finiteM) Lr = min(Lr, (long long)(M - Uafter) / f.nd);
+            Lr = min(Lr, cfg.max_steps - S.steps);
+          }
+          S.runL = Lr;
+          S.runMD = tt[8];
+          S.last_nd = f.nd;
+          S.U = Uafter;
+          S.seq = seq;
+          S.nB = nB;
+          const bool changed = n_new > 0 || S.any_pre || ndn > 0;  // run-list membership changed
+          S.r_dirty = changed;
+          S.removals = S.any_pre || ndn > 0;
+          S.w_dirty = n_new > 0 || S.any_pre || arrived;
+          S.nW = nW, S.minSW = minSW, S.wbuilt = wbuilt;
+          S.rank_dirty = ndn > 0;
+          // SRF order can change unless every running request was a decode in B (all +1)
+          S.o_dirty = srf && (changed || f.np > 0 || f.nd != nrun);
+          S.p_dirty = changed || tt[9] > 0;
+          S.r_new = n_new;
+        }
+      }
+      __syncthreads();
+    }
+    PROF_MARK(3);
+
+    // ---- (5) event times; steady decode run ----
+    {
+      const int nev = S.n_ev;
+      for (int e = tid; e < nev; e += NT) {
+        const int code = s_ev[e], sl = code & 0xFFF;
+        const int idx = lo + ((sl - lo) & (CAP - 1));
+        if (code & (1 << 12))
+          for (int k = 0; k < K; k++) tf[(long long)k * n + idx] = S.clock[k];
+        if (code & (2 << 12))
+          for (int k = 0; k < K; k++) td[(long long)k * n + idx] = S.clock[k];
+      }
+      const long long Lr = S.runL;
+      if (Lr > 0) {
+        PROF_CNT(9, Lr);
+        constexpr int DB = CAP / 2;
+        const int cmax = min(NT, DB / K);
+        const long long ndd = S.last_nd, MD = S.runMD, U0 = S.U;
+        long long E = 0;
+        while (E < Lr) {
+          const int chunk = (int)min((long long)cmax, Lr - E);
+          if (tid < chunk) {  // features of run step E+tid+1 are affine in the step index
+            Feat f;
+            f.N = ndd, f.np = 0, f.c2 = 0, f.mc = 0, f.cp = 0, f.mp = 0, f.pcm = 0, f.nd = ndd;
+            f.md = MD + (E + tid) * ndd;
+            for (int k = 0; k < SIM_MAX_COST; k++) f.pceil[k] = 0;
+            for (int k = 0; k < K; k++) s_dbuf[k * cmax + tid] = batch_time(S.cm[k], f, k);
+          }
+          __syncthreads();
+          if (tid == 0) {  // the clock chain stays sequential: one fp64 add per step, as in the oracle (Q36)
+            int ex = chunk;
+            if (nx1 < n) {  // online (K == 1): stop before a step that would start at/after an arrival (Q21)
+              const double Tn = wl.T[nx1];
+              double clk = S.clock[0];
+              for (int t = 0; t < chunk; t++) {
+                if (Tn <= clk) {
+                  ex = t;
+                  break;
+                }
+                clk = dadd(clk, s_dbuf[t]);
+              }
+              S.clock[0] = clk;
+            } else {
+              for (int k = 0; k < K; k++) {
+                double clk = S.clock[k];
+                for (int t = 0; t < chunk; t++) clk = dadd(clk, s_dbuf[k * cmax + t]);
+                S.clock[k] = clk;
+              }
+            }
+            S.runEx = ex;
+          }
+          __syncthreads();
+          const int ex = S.runEx;
+          E += ex;
+          if (ex < chunk) break;
+        }
+        long long fr2 = 0;
+        int nd2 = 0;
+        if (E > 0) {
+          for (int e = tid; e < nB; e += NT) {  // every B entry is a decode of the steady step
+            const int sl = s_bl[e];
+            const int4 rc = s_rec[sl];
+            const int m = rc.z + (int)E, g = rc.y + (int)E, O = s_O[sl];
+            s_rec[sl] = make_int4(rc.x, g, m, rc.w);
+            if (g == O) {  // completes at the last run step
+              const int idx = lo + ((sl - lo) & (CAP - 1));
+              s_fl[sl] = (s_fl[sl] & ~ST_MASK) | ST_DONE;
+              for (int k = 0; k < K; k++) td[(long long)k * n + idx] = S.clock[k];
+              fr2 += max(rc.w, m);
+              nd2++;
+              if (hist) atomicAdd(&S.hist[bucket_of(rc.x) * 18 + bucket_of(O)], 1);
+            }
+          }
+        }
+        fr2 = block_sum_ll<NT>(fr2, S);
+        const long long nd2t = block_sum_ll<NT>((long long)nd2, S);
+        if (tid == 0) {
+          S.steps += E;
+          S.sumU += E * U0 + ndd * (E * (E + 1) / 2);
+          S.entries += E * ndd;
+          S.processed += E * ndd;
+          S.visits += E * nP;
+          S.U = U0 + E * ndd - fr2;
+          S.n_done += (int)nd2t;
+          if (nd2t > 0) S.r_dirty = 1, S.removals = 1, S.rank_dirty = 1, S.p_dirty = 1;
+          if (srf && E > 0 && ndd != nrun) S.o_dirty = 1;
+        }
+        __syncthreads();
+      }
+    }
+    PROF_MARK(4);
+
+    // ---- (6) run list (retention order) for the next step ----
+    {
+      const bool rd = S.r_dirty, od = S.o_dirty;
+      int16_t* rl = run;
+      int cnt = nrun;
+      bool moved = false;
+      if (rd) {
+        const int nnew = S.r_new;
+        if (S.removals) {
+          int16_t* nrl = S.cur ? s_runA : s_runB;
+          auto src = [&](int q) -> int { return q < nrun ? run[q] : s_new[q - nrun]; };
+          cnt = block_compact<NT, IPT_>(
+              nrun + nnew, [&](int q) { return (s_fl[src(q)] & ST_MASK) == ST_RUN; }, src, nrl, S);
+          rl = nrl;
+          if (tid == 0) S.cur ^= 1;
+          moved = true;
+        } else {  // only admissions: append them (admission order = NRF retention order)
+          for (int q = tid; q < nnew; q += NT) {
+            run[nrun + q] = s_new[q];
+            s_rpos[s_new[q]] = (int16_t)(nrun + q);
+          }
+          cnt = nrun + nnew;
+          __syncthreads();
+        }
+      }
+      if (od) {  // SRF retention order: m descending, then admission order (Q3, Q7)
+        auto key = [&](int sl) -> unsigned long long {
+          return ((unsigned long long)(0x3FFFF - s_rec[sl].z) << 46) |
+                 ((unsigned long long)(unsigned)s_seq[sl] << 12) | (unsigned long long)sl;
+        };
+        int okk = 1;
+        for (int q = tid; q + 1 < cnt; q += NT)
+          if (key(rl[q]) > key(rl[q + 1])) okk = 0;
+        okk = __syncthreads_and(okk);
+        if (!okk) {
+          PROF_CNT(8, 1);
+          for (int q = tid; q < cnt; q += NT) s_keys[q] = key(rl[q]);
+          block_bitonic<NT>(s_keys, cnt);
+          for (int q = tid; q < cnt; q += NT) rl[q] = (int16_t)(s_keys[q] & 0xFFF);
+          moved = true;
+          if (tid == 0) S.p_dirty = 1;
+          __syncthreads();
+        }
+      }
+      if (moved)
+        for (int q = tid; q < cnt; q += NT) s_rpos[rl[q]] = (int16_t)q;
+      if (tid == 0) {
+        S.n_run = cnt;
+        S.next = nx1;
+        S.n_ev = 0;
+        int l = lo;
+        while (l < nx1 && (s_fl[l & (CAP - 1)] & ST_MASK) == ST_DONE) l++;
+        S.lo = l;
+      }
+      __syncthreads();
+      PROF_MARK(5);
+    }
+  }
+#ifdef SIMSWEEP_PROFILE
+  if (tid == 0 && ci < PROF_MAX_CFG)
+    for (int i = 0; i < 16; i++) g_prof[ci][i] = prof[i];
+#endif
+
+  // ---- a11: metrics ----
+  const int st = S.status == -1 ? SIM_S_OK : S.status;
+  __threadfence();
+  __syncthreads();
+  if (st != SIM_S_OK) {  // failed simulations: zero-filled rows
+    for (int i = tid; i < n; i += NT) {
+      npre[i] = 0;
+      refill[i] = 0;
+    }
+    for (int x = tid; x < K * n; x += NT) {
+      tf[x] = 0.0;
+      td[x] = 0.0;
+    }
+    if (tid == 0) {
+      sim_result_t r;
+      memset(&r, 0, sizeof(r));
+      r.status = st;
+      p.results[ci] = r;
+    }
+    return;
+  }
+  if (tid < K) {  // sequential sums in request order (identical to the oracle)
+    const int k = tid;
+    double mx = 0.0, sl = 0.0, st1 = 0.0, stp = 0.0;
+    long long ntp = 0;
+    for (int i = 0; i < n; i++) {
+      const double a = tf[(long long)k * n + i], b = td[(long long)k * n + i], T = wl.T[i];
+      if (i == 0 || b > mx) mx = b;
+      sl = dadd(sl, b - T);
+      st1 = dadd(st1, a - T);
+      if (wl.O[i] > 1) {
+        stp = dadd(stp, ddiv(b - a, i2d(wl.O[i] - 1)));
+        ntp++;
+      }
+    }
+    sim_result_t& r = p.results[ci];
+    r.makespan[k] = mx - wl.T[0];
+    r.mean_latency[k] = ddiv(sl, i2d(n));
+    r.mean_ttft[k] = ddiv(st1, i2d(n));
+    r.mean_tpot[k] = ntp > 0 ? ddiv(stp, i2d(ntp)) : 0.0;
+  }
+  if (tid == 0) {
+    sim_result_t& r = p.results[ci];
+    r.status = SIM_S_OK;
+    r.pad = 0;
+    r.steps = S.steps;
+    r.preemptions = S.preempt;
+    r.batch_entries = S.entries;
+    r.processed_tokens = S.processed;
+    r.sum_U = S.sumU;
+    r.prefill_entries = S.pentries;
+    r.idle_jumps = S.idle;
+    r.visits = S.visits;
+    for (int k = K; k < SIM_MAX_COST; k++) r.makespan[k] = r.mean_latency[k] = r.mean_ttft[k] = r.mean_tpot[k] = 0.0;
+  }
+}
+
+}  // namespace simsweep
