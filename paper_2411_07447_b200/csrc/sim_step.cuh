@@ -559,6 +559,95 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
       }
     };
 
+    // Waiting group on warp 0 (window offsets [0, L) = R_w in index order).  Waiting candidates never
+    // preempt (Q5) and are all in the prefill phase, so a chunk of 32 is resolved in registers: repeat
+    // {ballot the lanes that fit alone; prefix-scan them; admit those before the first cumulative
+    // failure; drop that failure} -- rejections change no state.  A cropped chunk (chunked prefill)
+    // exhausts the token budget and ends the group.
+    auto warp_w = [&](int L) {
+      for (int i0 = 0; i0 < L; i0 += 32) {
+        if ((!hybrid && bph == PH_DEC) || (finiteM && (long long)U + minSW > M) ||
+            (chunked ? tok >= C : minSW > C - tok))
+          return;  // the rest of R_w fails a monotone check
+        PROF_CNT(13, 1);
+        const int i = i0 + lane;
+        int sl = -1;
+        if (i < L) {
+          const int s2 = (lo + i) & (CAP - 1);
+          if ((s_fl[s2] & (ST_MASK | F_PRE)) == ST_WAIT) sl = s2;
+        }
+        const int4 rc = s_rec[sl < 0 ? 0 : sl];
+        const uint8_t fl = s_fl[sl < 0 ? 0 : sl];
+        const int s = rc.x + rc.y;  // waiting: m = 0, avail = s, KV delta = s
+        const int rem = hist ? max(S.pred[bucket_of(rc.x)] - rc.y, 0) : 0;
+        bool alive = sl >= 0;
+        for (;;) {
+          const int rt = C - tok;
+          const bool anyRun0 = n_running > 0;
+          bool fit = alive && rt >= 1 && (chunked || s <= rt) && (!finiteM || U + s <= M);
+          if (hist) fit = fit && !(anyRun0 && (long long)U + Rs + s + rem > M);
+          if (!__any_sync(FM, fit)) break;
+          const int cc = fit ? s : 0, kk = fit, rr = fit ? rem : 0;
+          int xc = cc, xk = kk, xr = rr;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int yc = __shfl_up_sync(FM, xc, o), yk = __shfl_up_sync(FM, xk, o);
+            if (lane >= o) xc += yc, xk += yk;
+            if (hist) {
+              const int yr = __shfl_up_sync(FM, xr, o);
+              if (lane >= o) xr += yr;
+            }
+          }
+          const int ec = xc - cc, ek = xk - kk, er = xr - rr;  // KV delta = c for waiting (non-cropped)
+          bool brk = false, crop = false;
+          if (fit) {
+            const int prt = rt - ec;
+            if (chunked) {
+              crop = prt < s;  // cropped (c = prt >= 1) or exhausted (prt <= 0)
+            } else {
+              brk = s > prt;
+            }
+            if (finiteM) brk |= U + ec + s > M;
+            if (hist) brk |= (anyRun0 || ek > 0) && (long long)U + ec + Rs + er + s + rem > M;
+            if (crop && prt <= 0) brk = true;
+          }
+          const unsigned bm = __ballot_sync(FM, brk), cm = __ballot_sync(FM, crop && !brk);
+          const int b = bm ? __ffs(bm) - 1 : 32, cl = cm ? __ffs(cm) - 1 : 32;
+          const int stop = min(b, cl);  // lanes before stop are admitted in full
+          const bool adm = fit && lane < stop, adc = fit && lane == cl && cl < b;  // full / cropped admission
+          if (adm || adc) {
+            const int c = adm ? s : rt - ec;
+            s_c[sl] = c;
+            s_bl[nB + ek] = (int16_t)sl;
+            s_seq[sl] = seq + ek + 1;
+            s_rec[sl] = make_int4(rc.x, rc.y, 0, s);
+            s_fl[sl] = ST_RUN | F_INB | (fl & F_FIRST);
+            s_new[n_new + ek] = (int16_t)sl;
+            alive = false;
+          }
+          const int na = __popc(__ballot_sync(FM, adm || adc));
+          const int src = na > 0 ? (adc ? lane : 0) : 0;
+          // totals admitted: tokens and KV of the admitted prefix (+ the crop)
+          const int last = __shfl_sync(FM, xc, stop > 0 ? min(stop, 32) - 1 : 0);
+          const int addc = stop > 0 ? last : 0;
+          const int addr = stop > 0 ? __shfl_sync(FM, xr, min(stop, 32) - 1) : __shfl_sync(FM, 0, 0);
+          const bool cropped = cl < b && cl < 32;
+          const int cropc = cropped ? __shfl_sync(FM, rt - ec, cl) : 0;
+          const int crops = cropped ? __shfl_sync(FM, s, cl) : 0;
+          const int cropr = cropped ? __shfl_sync(FM, rem, cl) : 0;
+          (void)src;
+          tok += addc + cropc;
+          U += addc + crops;
+          seq += na, n_new += na, n_running += na, nB += na;
+          Rs += addr + cropr;
+          if (na > 0 && bph < 0) bph = PH_PRE;
+          if (cropped) return;  // the token budget is exhausted: every later candidate is rejected
+          if (b < 32 && lane == b) alive = false;  // rejected (no state change)
+          if (b >= 32) break;
+        }
+      }
+    };
+
     while (pos < nP) {
       // running decodes in closed form
       if (order == SIM_ORDER_PREFILL_FIRST && pos == nW && nW < nP && !chunked && nrun <= CH) {
@@ -585,7 +674,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
           if (pos == wbeg) {
             long long amax = chunked ? (long long)(C - tok) : (long long)(C - tok) / max(minSW, 1);
             if (finiteM) amax = min(amax, (long long)(M - U) / max(minSW, 1));
-            if (amax <= 32 || nx1 - lo <= WARP_MAX) mode = 2, lim = wend;
+            if (amax <= 128 || nx1 - lo <= WARP_MAX) mode = 2, lim = wend;
           }
         } else if (!rank) {
           const int rend = order == SIM_ORDER_DECODE_FIRST ? len0 : nP;  // end of the running group(s)
@@ -595,7 +684,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
           PROF_CNT(11, 1);
           if (wid == 0) {
             if (mode == 2)
-              warp_run(true, 0, nx1 - lo);
+              warp_w(nx1 - lo);
             else
               warp_run(false, pos, lim);
             if (lane == 0) {
