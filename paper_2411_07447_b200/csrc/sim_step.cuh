@@ -489,12 +489,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
         for (int w = 0; w < NW; w++) akv += S.cf_red[w][1];
       }
       const int a = min(min(akv, T), k);
-      const bool meet = finiteM && a == akv && a < min(k, T);
       int qs = nrun, selfp = -1;
-      if (meet) {
-        selfp = hpos(a);
-        qs = selfp + 1;
-      } else if (finiteM && F < a) {  // q* = max{q : F + RS(q) >= a} (RS strictly decreasing)
+      if (finiteM && F < a) {  // q* = max{q : F + RS(q) >= a} (RS strictly decreasing)
         int cnt = 0;
 #pragma unroll
         for (int j = 0; j < IPT_; j++) {
@@ -508,6 +504,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
 #pragma unroll
         for (int w = 0; w < NW; w++) tot += S.cf_red[w][2];
         qs = tot - 1;
+      }
+      // head a+1 (if the KV, not the token budget, stopped the walk): evicted as a victim if it lies in the
+      // suffix, else it runs out of pool behind it and self-preempts after evicting all of it (Q8)
+      if (finiteM && a == akv && a < min(k, T)) {
+        const int pa = hpos(a);
+        if (pa < qs) selfp = pa, qs = pa + 1;
       }
       __syncthreads();  // every RS read is done before s_c is overwritten
       // (iii) apply: evict [qs, nrun) (+ the self-preempted head), admit heads [0, a)
@@ -555,92 +557,103 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
         S.n_vic = nvic0 + tev;
         S.preempt += tev;
         if (tev) S.any_pre = 1;
-        S.vt = min(S.vt, (meet ? selfp : qs) - 1);
+        S.vt = min(S.vt, (selfp >= 0 ? selfp : qs) - 1);
       }
     };
 
-    // Waiting group on warp 0 (window offsets [0, L) = R_w in index order).  Waiting candidates never
-    // preempt (Q5) and are all in the prefill phase, so a chunk of 32 is resolved in registers: repeat
-    // {ballot the lanes that fit alone; prefix-scan them; admit those before the first cumulative
+    // Candidates that never preempt, on warp 0: the waiting group (overWin: window offsets [0, L) = R_w
+    // in index order; Q5) or running prefills (P positions [b0, b1) = R_r^p; their KV delta is 0 since
+    // reserved = s >= m + c).  All are in the prefill phase, so a chunk of 32 is resolved in registers:
+    // repeat {ballot the lanes that fit alone; prefix-scan them; admit those before the first cumulative
     // failure; drop that failure} -- rejections change no state.  A cropped chunk (chunked prefill)
     // exhausts the token budget and ends the group.
-    auto warp_w = [&](int L) {
-      for (int i0 = 0; i0 < L; i0 += 32) {
-        if ((!hybrid && bph == PH_DEC) || (finiteM && (long long)U + minSW > M) ||
-            (chunked ? tok >= C : minSW > C - tok))
-          return;  // the rest of R_w fails a monotone check
+    auto warp_np = [&](bool overWin, int b0, int b1) {
+      for (int i0 = b0; i0 < b1; i0 += 32) {
+        if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining one fails
+        if (overWin && ((finiteM && (long long)U + minSW > M) || (!chunked && minSW > C - tok))) return;
         PROF_CNT(13, 1);
         const int i = i0 + lane;
         int sl = -1;
-        if (i < L) {
-          const int s2 = (lo + i) & (CAP - 1);
-          if ((s_fl[s2] & (ST_MASK | F_PRE)) == ST_WAIT) sl = s2;
+        if (i < b1) {
+          if (overWin) {
+            const int s2 = (lo + i) & (CAP - 1);
+            if ((s_fl[s2] & (ST_MASK | F_PRE)) == ST_WAIT) sl = s2;
+          } else {
+            const int s2 = cand(i);
+            if (!(s_fl[s2] & F_PRE)) sl = s2;
+          }
         }
         const int4 rc = s_rec[sl < 0 ? 0 : sl];
         const uint8_t fl = s_fl[sl < 0 ? 0 : sl];
-        const int s = rc.x + rc.y;  // waiting: m = 0, avail = s, KV delta = s
-        const int rem = hist ? max(S.pred[bucket_of(rc.x)] - rc.y, 0) : 0;
+        const bool isW = (fl & ST_MASK) == ST_WAIT;
+        const int s = rc.x + rc.y, avail = s - rc.z;
+        const int dkv = isW ? s : 0;  // KV delta (Q13)
+        const int rem = (hist && isW) ? max(S.pred[bucket_of(rc.x)] - rc.y, 0) : 0;
         bool alive = sl >= 0;
         for (;;) {
           const int rt = C - tok;
           const bool anyRun0 = n_running > 0;
-          bool fit = alive && rt >= 1 && (chunked || s <= rt) && (!finiteM || U + s <= M);
-          if (hist) fit = fit && !(anyRun0 && (long long)U + Rs + s + rem > M);
+          bool fit = alive && rt >= 1 && (chunked || avail <= rt) && (!finiteM || U + dkv <= M);
+          if (hist && isW) fit = fit && !(anyRun0 && (long long)U + Rs + s + rem > M);
           if (!__any_sync(FM, fit)) break;
-          const int cc = fit ? s : 0, kk = fit, rr = fit ? rem : 0;
-          int xc = cc, xk = kk, xr = rr;
+          const int cc = fit ? avail : 0, dd = fit ? dkv : 0, kk = fit, ww = fit && isW, rr = fit ? rem : 0;
+          int xc = cc, xd = dd, xk = kk, xw = ww, xr = rr;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
-            const int yc = __shfl_up_sync(FM, xc, o), yk = __shfl_up_sync(FM, xk, o);
-            if (lane >= o) xc += yc, xk += yk;
+            const int yc = __shfl_up_sync(FM, xc, o), yd = __shfl_up_sync(FM, xd, o);
+            const int yk = __shfl_up_sync(FM, xk, o), yw = __shfl_up_sync(FM, xw, o);
+            if (lane >= o) xc += yc, xd += yd, xk += yk, xw += yw;
             if (hist) {
               const int yr = __shfl_up_sync(FM, xr, o);
               if (lane >= o) xr += yr;
             }
           }
-          const int ec = xc - cc, ek = xk - kk, er = xr - rr;  // KV delta = c for waiting (non-cropped)
+          const int ec = xc - cc, ed = xd - dd, ek = xk - kk, ew = xw - ww, er = xr - rr;
           bool brk = false, crop = false;
           if (fit) {
             const int prt = rt - ec;
-            if (chunked) {
-              crop = prt < s;  // cropped (c = prt >= 1) or exhausted (prt <= 0)
-            } else {
-              brk = s > prt;
-            }
-            if (finiteM) brk |= U + ec + s > M;
-            if (hist) brk |= (anyRun0 || ek > 0) && (long long)U + ec + Rs + er + s + rem > M;
+            if (chunked)
+              crop = prt < avail;  // cropped (c = prt >= 1) or exhausted (prt <= 0)
+            else
+              brk = avail > prt;
+            if (finiteM) brk |= U + ed + dkv > M;
+            if (hist && isW) brk |= (anyRun0 || ek > 0) && (long long)U + ed + Rs + er + s + rem > M;
             if (crop && prt <= 0) brk = true;
           }
           const unsigned bm = __ballot_sync(FM, brk), cm = __ballot_sync(FM, crop && !brk);
           const int b = bm ? __ffs(bm) - 1 : 32, cl = cm ? __ffs(cm) - 1 : 32;
-          const int stop = min(b, cl);  // lanes before stop are admitted in full
-          const bool adm = fit && lane < stop, adc = fit && lane == cl && cl < b;  // full / cropped admission
+          const int stop = min(b, cl);                                             // lanes < stop: in full
+          const bool adm = fit && lane < stop, adc = fit && lane == cl && cl < b;  // + the cropped one
           if (adm || adc) {
-            const int c = adm ? s : rt - ec;
-            s_c[sl] = c;
+            s_c[sl] = adm ? avail : rt - ec;
             s_bl[nB + ek] = (int16_t)sl;
-            s_seq[sl] = seq + ek + 1;
-            s_rec[sl] = make_int4(rc.x, rc.y, 0, s);
-            s_fl[sl] = ST_RUN | F_INB | (fl & F_FIRST);
-            s_new[n_new + ek] = (int16_t)sl;
+            if (isW) {
+              s_seq[sl] = seq + ew + 1;
+              s_rec[sl] = make_int4(rc.x, rc.y, 0, s);
+              s_fl[sl] = ST_RUN | F_INB | (fl & F_FIRST);
+              s_new[n_new + ew] = (int16_t)sl;
+            } else {
+              s_fl[sl] = fl | F_INB;
+            }
             alive = false;
           }
-          const int na = __popc(__ballot_sync(FM, adm || adc));
-          const int src = na > 0 ? (adc ? lane : 0) : 0;
-          // totals admitted: tokens and KV of the admitted prefix (+ the crop)
-          const int last = __shfl_sync(FM, xc, stop > 0 ? min(stop, 32) - 1 : 0);
-          const int addc = stop > 0 ? last : 0;
-          const int addr = stop > 0 ? __shfl_sync(FM, xr, min(stop, 32) - 1) : __shfl_sync(FM, 0, 0);
           const bool cropped = cl < b && cl < 32;
+          const int lastl = stop > 0 ? min(stop, 32) - 1 : 0;
+          const int addc = stop > 0 ? __shfl_sync(FM, xc, lastl) : 0;
+          const int addd = stop > 0 ? __shfl_sync(FM, xd, lastl) : 0;
+          const int addk = stop > 0 ? __shfl_sync(FM, xk, lastl) : 0;
+          const int addw = stop > 0 ? __shfl_sync(FM, xw, lastl) : 0;
+          const int addr = stop > 0 ? __shfl_sync(FM, xr, lastl) : 0;
           const int cropc = cropped ? __shfl_sync(FM, rt - ec, cl) : 0;
-          const int crops = cropped ? __shfl_sync(FM, s, cl) : 0;
+          const int cropd = cropped ? __shfl_sync(FM, dkv, cl) : 0;
+          const int cropw = cropped ? __shfl_sync(FM, (int)isW, cl) : 0;
           const int cropr = cropped ? __shfl_sync(FM, rem, cl) : 0;
-          (void)src;
           tok += addc + cropc;
-          U += addc + crops;
-          seq += na, n_new += na, n_running += na, nB += na;
+          U += addd + cropd;
+          seq += addw + cropw, n_new += addw + cropw, n_running += addw + cropw;
+          nB += addk + (cropped ? 1 : 0);
           Rs += addr + cropr;
-          if (na > 0 && bph < 0) bph = PH_PRE;
+          if ((addk > 0 || cropped) && bph < 0) bph = PH_PRE;
           if (cropped) return;  // the token budget is exhausted: every later candidate is rejected
           if (b < 32 && lane == b) alive = false;  // rejected (no state change)
           if (b >= 32) break;
@@ -678,13 +691,18 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
           }
         } else if (!rank) {
           const int rend = order == SIM_ORDER_DECODE_FIRST ? len0 : nP;  // end of the running group(s)
-          if (rend - pos <= WARP_MAX) mode = 1, lim = rend;
+          if (rend - pos <= WARP_MAX) {
+            mode = 1, lim = rend;
+            if (order == SIM_ORDER_DECODE_FIRST && pos >= nRd) mode = 3;  // R_r^p: running prefills only
+          }
         }
         if (mode) {
           PROF_CNT(11, 1);
           if (wid == 0) {
             if (mode == 2)
-              warp_w(nx1 - lo);
+              warp_np(true, 0, nx1 - lo);
+            else if (mode == 3)
+              warp_np(false, pos, lim);
             else
               warp_run(false, pos, lim);
             if (lane == 0) {
@@ -980,6 +998,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
           f.c2 = tt[11], f.mc = tt[12], f.pcm = tt[13];
           f.pceil[0] = tt[14], f.pceil[1] = tt[15], f.pceil[2] = tt[16], f.pceil[3] = tt[17];
           for (int k = 0; k < K; k++) S.clock[k] = dadd(S.clock[k], batch_time(S.cm[k], f, k));  // Q36
+#ifdef SIMSWEEP_PROFILE
+          if (ci == 0 && S.steps < DBG_STEPS) {
+            int* d = g_dbg[S.steps];
+            d[0] = (int)S.steps, d[1] = tok, d[2] = U, d[3] = nB, d[4] = (int)S.preempt, d[5] = S.n_vic;
+          }
+#endif
           S.steps++;
           S.sumU += U;
           S.entries += f.np + f.nd;
@@ -1096,6 +1120,14 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
         fr2 = block_sum_ll<NT>(fr2, S);
         const long long nd2t = block_sum_ll<NT>((long long)nd2, S);
         if (tid == 0) {
+#ifdef SIMSWEEP_PROFILE
+          if (ci == 0)
+            for (long long k = 1; k <= E && S.steps + k - 1 < DBG_STEPS; k++) {
+              int* d = g_dbg[S.steps + k - 1];
+              d[0] = (int)(S.steps + k - 1), d[1] = (int)ndd, d[2] = (int)(U0 + k * ndd), d[3] = (int)ndd;
+              d[4] = (int)S.preempt, d[5] = 0;
+            }
+#endif
           S.steps += E;
           S.sumU += E * U0 + ndd * (E * (E + 1) / 2);
           S.entries += E * ndd;

@@ -18,6 +18,8 @@ namespace simsweep {
 #ifdef SIMSWEEP_PROFILE  // phase cycle counters of thread 0 (tools/probe.py); not in the product build
 constexpr int PROF_MAX_CFG = 8192;
 __device__ long long g_prof[PROF_MAX_CFG][16];
+constexpr int DBG_STEPS = 1 << 16;
+__device__ int g_dbg[DBG_STEPS][6];  // config 0 only: per full step (steps, tok, U, nB, preemptions, n_vic)
 #define PROF_MARK(i)                  \
   if (tid == 0) {                     \
     long long _t = clock64();         \
@@ -80,6 +82,9 @@ extern "C" {
 #ifdef SIMSWEEP_PROFILE
 int sim_debug_read(int64_t* out, int32_t n_cfgs) {
   return cudaMemcpyFromSymbol(out, g_prof, sizeof(long long) * 16 * (size_t)n_cfgs) == cudaSuccess ? 0 : SIM_ECUDA;
+}
+int sim_debug_steps(int32_t* out, int32_t n) {
+  return cudaMemcpyFromSymbol(out, g_dbg, sizeof(int) * 6 * (size_t)n) == cudaSuccess ? 0 : SIM_ECUDA;
 }
 #endif
 
