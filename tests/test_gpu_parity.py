@@ -144,3 +144,79 @@ def test_hetero_rank():
         for nm in ("rank-org", "rank-i", "rank-o"):
             cases.append((simsweep.preset_config(nm, 100_000), wl, A100))
     assert_parity(cases)
+
+
+def _oracle_grid_job(args):
+    name, I, O, M = args
+    import oracle as o2
+    from paper_2411_07447_b200 import presets as pr
+    from paper_2411_07447_b200 import workloads as wk
+    p = pr.preset(name)
+    wl = wk.fixed(I, O, 1024)
+    r = o2.run(o2.make_config(p["order"], p["hybrid"], p["chunked"], p["replacement"], C=p["C"], M=M), wl.I, wl.O,
+               wl.T, o2.load_cost_models()["llama3-8b_a100_linear"])
+    return (r.status, [getattr(r, f) for f in ("steps", "preemptions", "batch_entries", "processed_tokens", "sum_U",
+                                               "prefill_entries", "idle_jumps", "visits")],
+            r.t_first[0].copy(), r.t_done[0].copy(), r.n_preempt.copy(), r.refill.copy(), r.makespan[0])
+
+
+@pytest.mark.parametrize("M", [100_000])
+def test_full_grid_bench_launch(M):
+    """BASELINE configs[1] at full size: all 1452 simulations, one sim_sweep_device launch in bench.py's
+    configuration (device-resident inputs, LPT order), every output compared with the oracle."""
+    import multiprocessing as mp
+    import os
+
+    import torch
+
+    from paper_2411_07447_b200 import sweep
+    cfgs, wls, cms, labels = sweep.grid_sweep(M=M)
+    order = sweep.partition_lpt(sweep.estimate(cfgs, wls), 1)[0]
+    ds = simsweep.DeviceSweep(cfgs, wls, cms, device="cuda", order=np.asarray(order, np.int32))
+    ds.launch()
+    torch.cuda.synchronize()
+    g = ds.fetch()
+    jobs = [(nm, I, O, M) for (nm, I, O) in labels]
+    with mp.get_context("fork").Pool(min(len(os.sched_getaffinity(0)), 64)) as pool:
+        ref = pool.map(_oracle_grid_job, jobs, chunksize=4)
+    bad = []
+    names = ["steps", "preemptions", "batch_entries", "processed_tokens", "sum_U", "prefill_entries", "idle_jumps",
+             "visits"]
+    for i, (st, ints, tf, td, npre, rf, mk) in enumerate(ref):
+        lab = labels[i]
+        if g.status(i) != st:
+            bad.append(f"{lab} status {g.status(i)} vs {st}")
+            continue
+        for f, v in zip(names, ints):
+            if int(g.results[f][i]) != v:
+                bad.append(f"{lab} {f} {int(g.results[f][i])} vs {v}")
+        gtf, gtd = g.request_times(i)
+        gnp, grf = g.request_counts(i)
+        if not (np.array_equal(gtf[0], tf) and np.array_equal(gtd[0], td)):
+            bad.append(f"{lab} per-request times differ")
+        if not (np.array_equal(gnp, npre) and np.array_equal(grf, rf)):
+            bad.append(f"{lab} per-request preemption counts differ")
+        if not np.isclose(g.results["makespan"][i][0], mk, rtol=1e-9, atol=0):
+            bad.append(f"{lab} makespan")
+    assert bad == [], "\n".join(bad[:30])
+
+
+@pytest.mark.parametrize("block", range(3))
+def test_random_medium_contention(block):
+    """Larger W and tight M: many preemptions, SRF/NRF, decode-first chunked (R_r^p interleaved with
+    R_r^d in the retention order) -- stresses the closed-form decode group."""
+    cases = []
+    for seed in range(5000 + block * 60, 5000 + block * 60 + 60):
+        rng = np.random.default_rng(seed)
+        Wn = int(rng.integers(32, 400))
+        wl = workloads.random_small(seed, Wn, max_len=int(rng.integers(4, 200)), online=bool(rng.integers(0, 2)),
+                                    S=512)
+        o_ = int(rng.integers(0, 2))
+        r = int(rng.integers(0, 3))
+        chunked = int(rng.integers(0, 2))
+        hybrid = int(rng.integers(0, 2))
+        peak = int((wl.I.astype(int) + wl.O - 1).max())
+        C = int(rng.integers(max(1, peak // 4), 2 * peak + 1)) if chunked else int(rng.integers(peak, 3 * peak + 1))
+        M = int(rng.integers(peak, 6 * peak + 1))
+        cases.append((cfg(o_, hybrid, chunked, r, C, M, S=512), wl, A100))
+    assert_parity(cases)
