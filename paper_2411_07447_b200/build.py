@@ -28,11 +28,11 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, profile: bool = False, defines=()) -> str:
     """profile=True builds libsimsweep_prof.so with per-phase cycle counters (tools/probe.py)."""
     lib = LIB.replace(".so", "_prof.so") if profile else LIB
     if force or profile or needs_build():
-        cmd = ([NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + (["-DSIMSWEEP_PROFILE"] if profile else [])
+        cmd = ([NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + (["-DSIMSWEEP_PROFILE"] if profile else []) + ["-D" + d for d in defines]
                + ["-o", lib] + SRC)
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -62,11 +62,12 @@ struct Scal {
   long long featsum[16];
   long long wred[16][18];  // per-warp partials of the process pass
   int next, new_next, lo, n_done, n_run, nW, nrank, minSW, n_ev, n_vic, nB, nRd;
-  int cf_red[32][4];
+  int cf_red[32][8];
+  int pa, cut, h_pre;
   int vt, status, any_pre, cur, wbuilt;
   int w_dirty, p_dirty, r_dirty, o_dirty, rank_dirty, removals;
   long long r_Rs;  // scalars handed back by thread 0 after a break
-  int r_tok, r_U, r_seq, r_new, r_running, r_bph, r_nB;
+  int r_tok, r_U, r_seq, r_new, r_running, r_bph, r_nB, r_wdone;
   int wmin[32];
   int wsum[32][6];
   int wcnt[32];

@@ -33,7 +33,7 @@ enum { K_NONE = 0, K_MARK = 1, K_EVENT = 2 };
 constexpr int WARP_MAX = 256;  // at most this many candidates left in a group: warp-level admission
 
 template <int NT, int CAP, int IPT_>
-__global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams p) {
+__global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) : 1)) sim_kernel(KParams p) {
   using L = Smem<NT, CAP>;
   constexpr int NW = NT / 32;
   constexpr int CH = NT * IPT_;  // candidates per round
@@ -60,6 +60,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int ci = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
+#ifdef SIMSWEEP_PROFILE
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   const sim_config_t cfg = p.cfgs[ci];
   const sim_workload_t wl = p.wls[cfg.workload];
   const int n = wl.n;
@@ -124,30 +128,41 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
   long long prof_last = clock64();
 #endif
 
+  int exit_status = 0;
   for (;;) {
     PROF_MARK(10);
     // ---- (1) a2: GetNewRequests (Alg. 1 line 3): all T <= clock, inclusive (Q21) ----
-    if (tid == 0) {
-      int a = S.next, b = n;
-      const double clk = S.clock[0];
-      while (a < b) {
-        int mid = (a + b) >> 1;
-        if (wl.T[mid] <= clk)
-          a = mid + 1;
-        else
-          b = mid;
+    int nx1;
+    if (S.next >= n) {  // everything has arrived (offline after step 1): uniform checks, no barrier
+      nx1 = n;
+      exit_status = S.n_done == n ? -1 : (S.steps >= cfg.max_steps ? SIM_S_MAX_STEPS : 0);
+    } else {
+      if (tid == 0) {
+        int a = S.next, b = n;
+        const double clk = S.clock[0];
+        while (a < b) {
+          int mid = (a + b) >> 1;
+          if (wl.T[mid] <= clk)
+            a = mid + 1;
+          else
+            b = mid;
+        }
+        S.new_next = a;
+        int st = 0;
+        if (S.n_done == n)
+          st = -1;
+        else if (a - S.lo > CAP)
+          st = SIM_S_CAPACITY;
+        else if (S.steps >= cfg.max_steps)
+          st = SIM_S_MAX_STEPS;
+        S.status = st;
       }
-      S.new_next = a;
-      if (S.n_done == n)
-        S.status = -1;
-      else if (a - S.lo > CAP)
-        S.status = SIM_S_CAPACITY;
-      else if (S.steps >= cfg.max_steps)
-        S.status = SIM_S_MAX_STEPS;
+      __syncthreads();
+      nx1 = S.new_next;
+      exit_status = S.status;
     }
-    __syncthreads();
-    if (S.status) break;
-    const int nx0 = S.next, nx1 = S.new_next, lo = S.lo;
+    if (exit_status) break;
+    const int nx0 = S.next, lo = S.lo;
     const bool arrived = nx1 > nx0;
     const int nrun = S.n_run;
     int16_t* run = S.cur ? s_runB : s_runA;
@@ -166,7 +181,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
       s_c[sl] = 0;
       s_fl[sl] = ST_WAIT;
     }
-    __syncthreads();
+    if (arrived) __syncthreads();
     PROF_MARK(0);
     // ---- (2) a3: GroupRequests (step 1) ----
     if (rank && arrived) {  // one group sorted by (key, T, id) (App. D, Q20, Q37)
@@ -207,13 +222,16 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
       wbuilt = 0;
       __syncthreads();
     }
-    if (order == SIM_ORDER_DECODE_FIRST && S.p_dirty) {  // {R_r^d, R_r^p, R_w}: stable split of the run list
-      const int nrd = block_partition<NT, IPT_>(
-          nrun, [&](int q) { return (s_fl[run[q]] & F_FILLED) != 0; }, [&](int q) { return run[q]; }, s_pl, S);
-      if (tid == 0) S.nRd = nrd;
+    int nRd = 0;
+    if (order == SIM_ORDER_DECODE_FIRST && nrun > CH) {  // fallback path only: stable split of the run list
+      if (S.p_dirty) {
+        const int nrd = block_partition<NT, IPT_>(
+            nrun, [&](int q) { return (s_fl[run[q]] & F_FILLED) != 0; }, [&](int q) { return run[q]; }, s_pl, S);
+        if (tid == 0) S.nRd = nrd;
+        __syncthreads();
+      }
+      nRd = S.nRd;
     }
-    __syncthreads();
-    const int nRd = order == SIM_ORDER_DECODE_FIRST ? S.nRd : 0;
     const int16_t* seg0;
     const int16_t* seg1;
     int len0, len1;
@@ -245,6 +263,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
     if (tid == 0) {
       S.vt = nrun - 1;
       S.any_pre = 0;
+      S.h_pre = 0;
+      S.cut = nrun;
       S.n_vic = 0;
       S.nrank = nrank;
       S.visits += nP;
@@ -268,6 +288,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
       n_running--;
       S.preempt++;
       S.any_pre = 1;
+      S.h_pre = 1;  // a preemption outside the closed form: the run list needs a full compaction
     };
     auto handle = [&](int sl) {  // literal sequential resolution of one candidate (thread 0)
       uint8_t fl = s_fl[sl];
@@ -431,122 +452,119 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
     // exactly the sequential head/tail walk of steps (3)-(4), done in O(1) passes.
     // pf: heads = run[0..k) (prefill-first, non-chunked: every running request decodes),
     // else heads = s_pl[0..k) (R_r^d).  Requires nrun <= CH.
-    auto decode_group = [&](bool pf, int k) {
+    auto decode_group = [&](bool tail_sync) {  // heads = decodes (F_FILLED) of the run list, retention order
       const int F = finiteM ? M - U : 0x3fffffff;
       const int T = C - tok;
-      // (i) RS(q) by a reverse scan of held over the run list, parked in s_c[slot] (free until admission)
-      {
-        int hv[IPT_], ls = 0;
+      // (i) reverse scan over run positions of (held, is-head): RS(q) = sum held at >= q, HS(q) = heads at >= q
+      int hv[IPT_], rsv[IPT_], hsv[IPT_], ls = 0, lh = 0;
+      bool hh[IPT_];
 #pragma unroll
-        for (int j = 0; j < IPT_; j++) {
-          const int q = nrun - 1 - (tid * IPT_ + j);
-          hv[j] = 0;
-          if (q >= 0) {
-            const int4 rc = s_rec[run[q]];
-            hv[j] = max(rc.w, rc.z);
-          }
-          ls += hv[j];
+      for (int j = 0; j < IPT_; j++) {
+        const int q = nrun - 1 - (tid * IPT_ + j);
+        hv[j] = 0, hh[j] = false;
+        if (q >= 0) {
+          const int sl = run[q];
+          const int4 rc = s_rec[sl];
+          hv[j] = max(rc.w, rc.z);
+          hh[j] = (s_fl[sl] & F_FILLED) != 0;
         }
-        int x = ls;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(FM, x, o);
-          if (lane >= o) x += y;
-        }
-        if (lane == 31) S.cf_red[wid][0] = x;
-        __syncthreads();
-        int off = x - ls;
-#pragma unroll
-        for (int w = 0; w < NW; w++) off += (w < wid) ? S.cf_red[w][0] : 0;
-#pragma unroll
-        for (int j = 0; j < IPT_; j++) {
-          const int q = nrun - 1 - (tid * IPT_ + j);
-          off += hv[j];
-          if (q >= 0) s_c[run[q]] = off;  // RS(q)
-        }
-        __syncthreads();
+        ls += hv[j], lh += hh[j];
       }
-      auto head = [&](int i) -> int { return pf ? run[i] : s_pl[i]; };  // 0-based head index
-      auto hpos = [&](int i) -> int { return pf ? i : s_rpos[s_pl[i]]; };
-      // (ii) a_kv = #{i : F + RS(p_i + 1) >= i} (1-based i)
-      int akv = k;
+      int xs = ls, xh = lh;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ys = __shfl_up_sync(FM, xs, o), yh = __shfl_up_sync(FM, xh, o);
+        if (lane >= o) xs += ys, xh += yh;
+      }
+      if (lane == 31) S.cf_red[wid][0] = xs, S.cf_red[wid][1] = xh;
+      __syncthreads();
+      int os = xs - ls, oh = xh - lh, k = 0;
+#pragma unroll
+      for (int w = 0; w < NW; w++) {
+        const int a0 = S.cf_red[w][0], a1 = S.cf_red[w][1];
+        if (w < wid) os += a0, oh += a1;
+        k += a1;
+      }
+#pragma unroll
+      for (int j = 0; j < IPT_; j++) os += hv[j], oh += hh[j], rsv[j] = os, hsv[j] = oh;
+      // (ii) a_kv = #{heads i : F + RS(p_i + 1) >= i}, i = k - HS(p_i) + 1 (monotone in i)
+      int cnt = 0;
       if (finiteM) {
-        int cnt = 0;
 #pragma unroll
-        for (int j = 0; j < IPT_; j++) {
-          const int i = tid * IPT_ + j;
-          if (i < k) {
-            const int p1 = hpos(i) + 1;
-            const int rsn = p1 < nrun ? s_c[run[p1]] : 0;
-            cnt += F + rsn >= i + 1;
-          }
-        }
-        cnt = (int)__reduce_add_sync(FM, (unsigned)cnt);
-        if (lane == 0) S.cf_red[wid][1] = cnt;
-        __syncthreads();
-        akv = 0;
-#pragma unroll
-        for (int w = 0; w < NW; w++) akv += S.cf_red[w][1];
+        for (int j = 0; j < IPT_; j++)
+          if (hh[j]) cnt += F + (rsv[j] - hv[j]) >= k - hsv[j] + 1;
       }
-      const int a = min(min(akv, T), k);
-      int qs = nrun, selfp = -1;
-      if (finiteM && F < a) {  // q* = max{q : F + RS(q) >= a} (RS strictly decreasing)
-        int cnt = 0;
+      cnt = (int)__reduce_add_sync(FM, (unsigned)cnt);
+      if (lane == 0) S.cf_red[wid][2] = cnt;
+      __syncthreads();
+      int akv = 0;
 #pragma unroll
-        for (int j = 0; j < IPT_; j++) {
-          const int q = tid * IPT_ + j;
-          if (q < nrun) cnt += F + s_c[run[q]] >= a;
+      for (int w = 0; w < NW; w++) akv += S.cf_red[w][2];
+      if (!finiteM) akv = k;
+      const int a = min(min(akv, T), k);
+      // (iii) q* = max{q : F + RS(q) >= a}; the position of head a+1
+      const bool needq = finiteM && F < a;
+      int cq = 0;
+#pragma unroll
+      for (int j = 0; j < IPT_; j++) {
+        const int q = nrun - 1 - (tid * IPT_ + j);
+        if (q >= 0) {
+          if (needq) cq += F + rsv[j] >= a;
+          if (hh[j] && k - hsv[j] + 1 == a + 1) S.pa = q;
         }
-        cnt = (int)__reduce_add_sync(FM, (unsigned)cnt);
-        if (lane == 0) S.cf_red[wid][2] = cnt;
-        __syncthreads();
+      }
+      cq = (int)__reduce_add_sync(FM, (unsigned)cq);
+      if (lane == 0) S.cf_red[wid][3] = cq;
+      __syncthreads();
+      int qs = nrun, selfp = -1;
+      if (needq) {
         int tot = 0;
 #pragma unroll
-        for (int w = 0; w < NW; w++) tot += S.cf_red[w][2];
+        for (int w = 0; w < NW; w++) tot += S.cf_red[w][3];
         qs = tot - 1;
       }
-      // head a+1 (if the KV, not the token budget, stopped the walk): evicted as a victim if it lies in the
-      // suffix, else it runs out of pool behind it and self-preempts after evicting all of it (Q8)
+      // head a+1, when the KV (not the token budget) stopped the walk: a victim if it lies in the evicted
+      // suffix, else it runs out of pool, evicts everything behind it and self-preempts (Q8)
       if (finiteM && a == akv && a < min(k, T)) {
-        const int pa = hpos(a);
+        const int pa = S.pa;
         if (pa < qs) selfp = pa, qs = pa + 1;
       }
-      __syncthreads();  // every RS read is done before s_c is overwritten
-      // (iii) apply: evict [qs, nrun) (+ the self-preempted head), admit heads [0, a)
+      // (iv) apply: evict [qs, nrun) (+ the self-preempted head), admit heads 1..a
       const int nvic0 = S.n_vic;
       int ev = 0, eh = 0, er = 0;
 #pragma unroll
       for (int j = 0; j < IPT_; j++) {
-        const int q = tid * IPT_ + j;
-        if (q < nrun && (q >= qs || q == selfp)) {
-          const int v = run[q];
-          const int4 rc = s_rec[v];
+        const int q = nrun - 1 - (tid * IPT_ + j);
+        if (q < 0) continue;
+        const int sl = run[q];
+        if (q >= qs || q == selfp) {
+          const int4 rc = s_rec[sl];
           ev++;
-          eh += max(rc.w, rc.z);
+          eh += hv[j];
           if (hist) er += max(S.pred[bucket_of(rc.x)] - rc.y, 0);
-          const int idx = lo + ((v - lo) & (CAP - 1));
+          const int idx = lo + ((sl - lo) & (CAP - 1));
           atomicAdd(&npre[idx], 1ull);
           atomicAdd(&refill[idx], (unsigned long long)rc.z);
-          s_rec[v] = make_int4(rc.x, rc.y, 0, 0);
-          s_fl[v] = ST_WAIT | F_PRE | (s_fl[v] & F_FIRST);
-          s_vic[nvic0 + (q == selfp ? nrun - qs : q - qs)] = (int16_t)v;
-        }
-        if (q < a) {
-          const int h = head(q);
-          s_c[h] = 1;
-          s_fl[h] |= F_INB;
-          s_bl[nB + q] = (int16_t)h;
+          s_rec[sl] = make_int4(rc.x, rc.y, 0, 0);
+          s_fl[sl] = ST_WAIT | F_PRE | (s_fl[sl] & F_FIRST);
+          s_vic[nvic0 + (q == selfp ? nrun - qs : q - qs)] = (int16_t)sl;
+        } else if (hh[j]) {
+          const int i = k - hsv[j] + 1;
+          if (i <= a) {
+            s_c[sl] = 1;
+            s_fl[sl] |= F_INB;
+            s_bl[nB + i - 1] = (int16_t)sl;
+          }
         }
       }
       ev = (int)__reduce_add_sync(FM, (unsigned)ev);
       eh = (int)__reduce_add_sync(FM, (unsigned)eh);
       if (hist) er = (int)__reduce_add_sync(FM, (unsigned)er);
-      if (lane == 0) S.cf_red[wid][0] = ev, S.cf_red[wid][1] = eh, S.cf_red[wid][2] = er;
+      if (lane == 0) S.cf_red[wid][4] = ev, S.cf_red[wid][5] = eh, S.cf_red[wid][6] = er;
       __syncthreads();
       int tev = 0, teh = 0, ter = 0;
 #pragma unroll
-      for (int w = 0; w < NW; w++) tev += S.cf_red[w][0], teh += S.cf_red[w][1], ter += S.cf_red[w][2];
-      __syncthreads();
+      for (int w = 0; w < NW; w++) tev += S.cf_red[w][4], teh += S.cf_red[w][5], ter += S.cf_red[w][6];
       tok += a;
       U += a - teh;
       nB += a;
@@ -558,7 +576,9 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
         S.preempt += tev;
         if (tev) S.any_pre = 1;
         S.vt = min(S.vt, (selfp >= 0 ? selfp : qs) - 1);
+        S.cut = selfp >= 0 ? selfp : qs;  // run positions >= cut were evicted (a suffix)
       }
+      if (tail_sync) __syncthreads();  // evictions and admissions are visible; cf_red may be reused
     };
 
     // Candidates that never preempt, on warp 0: the waiting group (overWin: window offsets [0, L) = R_w
@@ -567,7 +587,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
     // repeat {ballot the lanes that fit alone; prefix-scan them; admit those before the first cumulative
     // failure; drop that failure} -- rejections change no state.  A cropped chunk (chunked prefill)
     // exhausts the token budget and ends the group.
-    auto warp_np = [&](bool overWin, int b0, int b1) {
+    auto warp_np = [&](int src, int b0, int b1) {
+      const bool overWin = src == 1;
       for (int i0 = b0; i0 < b1; i0 += 32) {
         if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining one fails
         if (overWin && ((finiteM && (long long)U + minSW > M) || (!chunked && minSW > C - tok))) return;
@@ -578,6 +599,9 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
           if (overWin) {
             const int s2 = (lo + i) & (CAP - 1);
             if ((s_fl[s2] & (ST_MASK | F_PRE)) == ST_WAIT) sl = s2;
+          } else if (src == 2) {  // running prefills (not evicted) in retention order
+            const int s2 = run[i];
+            if ((s_fl[s2] & (ST_MASK | F_PRE | F_FILLED)) == ST_RUN) sl = s2;
           } else {
             const int s2 = cand(i);
             if (!(s_fl[s2] & F_PRE)) sl = s2;
@@ -661,18 +685,46 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
       }
     };
 
+    bool rfast = false;  // the decode-first running groups were resolved (once per step)
     while (pos < nP) {
       // running decodes in closed form
       if (order == SIM_ORDER_PREFILL_FIRST && pos == nW && nW < nP && !chunked && nrun <= CH) {
-        if (hybrid || bph != PH_PRE) decode_group(true, nrun);  // else every decode fails step 2
+        if (hybrid || bph != PH_PRE) decode_group(false);  // else every decode fails step 2 (no running prefills)
         pos = nP;
         PROF_CNT(12, 1);
         continue;
       }
-      if (order == SIM_ORDER_DECODE_FIRST && pos == 0 && nRd > 0 && nrun <= CH) {
-        decode_group(false, nRd);
-        pos = nRd;
+      if (order == SIM_ORDER_DECODE_FIRST && pos == 0 && !rfast && nrun <= CH) {
+        rfast = true;
+        // {R_r^d, R_r^p, R_w}: decodes in closed form, then running prefills and (if warp-suitable) the
+        // waiting group in one pass of warp 0
+        if (nrun > 0) decode_group(true);
         PROF_CNT(12, 1);
+        if (wid == 0) {
+          if (nrun > 0) warp_np(2, 0, nrun);
+          int wdone = nW == 0;
+          if (!wdone) {
+            const bool wrej = (!hybrid && bph == PH_DEC) || (finiteM && (long long)U + minSW > M) ||
+                              (chunked ? tok >= C : minSW > C - tok);
+            long long amax = chunked ? (long long)(C - tok) : (long long)(C - tok) / max(minSW, 1);
+            if (finiteM) amax = min(amax, (long long)(M - U) / max(minSW, 1));
+            if (wrej) {
+              wdone = 1;
+            } else if (amax <= 128 || nx1 - lo <= WARP_MAX) {
+              warp_np(1, 0, nx1 - lo);
+              wdone = 1;
+            }
+          }
+          if (lane == 0) {
+            S.r_tok = tok, S.r_U = U, S.r_seq = seq, S.r_Rs = Rs, S.r_nB = nB;
+            S.r_new = n_new, S.r_running = n_running, S.r_bph = bph, S.r_wdone = wdone;
+          }
+        }
+        __syncthreads();
+        tok = S.r_tok, U = S.r_U, seq = S.r_seq, Rs = S.r_Rs, nB = S.r_nB;
+        n_new = S.r_new, n_running = S.r_running, bph = S.r_bph;
+        pos = S.r_wdone ? nP : len0;
+        __syncthreads();
         continue;
       }
       {  // warp-level mode when few candidates need a decision
@@ -700,9 +752,9 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
           PROF_CNT(11, 1);
           if (wid == 0) {
             if (mode == 2)
-              warp_np(true, 0, nx1 - lo);
+              warp_np(1, 0, nx1 - lo);
             else if (mode == 3)
-              warp_np(false, pos, lim);
+              warp_np(0, pos, lim);
             else
               warp_run(false, pos, lim);
             if (lane == 0) {
@@ -893,7 +945,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
           S.status = SIM_S_DEADLOCK;
       }
       __syncthreads();
-      if (S.status) break;
+      exit_status = S.status;
+      if (exit_status) break;
       continue;
     }
     PROF_MARK(2);
@@ -986,6 +1039,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
       }
       __syncthreads();
       if (wid == 0) {  // warp 0 folds the per-warp partials (lane z owns column z)
+        int vmin = 0x7fffffff;  // smallest s among this step's victims (they join R_w)
+        for (int v = lane; v < S.n_vic; v += 32) {
+          const int4 rc = s_rec[s_vic[v]];
+          vmin = min(vmin, rc.x + rc.y);
+        }
+        vmin = (int)__reduce_min_sync(FM, (unsigned)vmin);
         long long t = (lane == 10) ? NOBRK : 0;
         if (lane < 18)
           for (int w = 0; w < NW; w++) t = (lane == 10) ? min(t, S.wred[w][10]) : t + S.wred[w][lane];
@@ -1030,9 +1089,11 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
           S.nB = nB;
           const bool changed = n_new > 0 || S.any_pre || ndn > 0;  // run-list membership changed
           S.r_dirty = changed;
-          S.removals = S.any_pre || ndn > 0;
-          S.w_dirty = n_new > 0 || S.any_pre || arrived;
-          S.nW = nW, S.minSW = minSW, S.wbuilt = wbuilt;
+          // removals only as the closed form's evicted suffix: the run list is cut, not compacted
+          S.removals = S.h_pre || ndn > 0 ? 2 : (S.any_pre ? 1 : 0);
+          // R_w gains this step's victims (exact min update) and loses admissions (full recount)
+          S.w_dirty = n_new > 0 || arrived;
+          S.nW = nW + S.n_vic, S.minSW = min(minSW, vmin), S.wbuilt = wbuilt && S.n_vic == 0;
           S.rank_dirty = ndn > 0;
           // SRF order can change unless every running request was a decode in B (all +1)
           S.o_dirty = srf && (changed || f.np > 0 || f.nd != nrun);
@@ -1057,7 +1118,6 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
       }
       const long long Lr = S.runL;
       if (Lr > 0) {
-        PROF_CNT(9, Lr);
         constexpr int DB = CAP / 2;
         const int cmax = min(NT, DB / K);
         const long long ndd = S.last_nd, MD = S.runMD, U0 = S.U;
@@ -1135,7 +1195,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
           S.visits += E * nP;
           S.U = U0 + E * ndd - fr2;
           S.n_done += (int)nd2t;
-          if (nd2t > 0) S.r_dirty = 1, S.removals = 1, S.rank_dirty = 1, S.p_dirty = 1;
+          if (nd2t > 0) S.r_dirty = 1, S.removals = 2, S.rank_dirty = 1, S.p_dirty = 1;
           if (srf && E > 0 && ndd != nrun) S.o_dirty = 1;
         }
         __syncthreads();
@@ -1151,7 +1211,15 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
       bool moved = false;
       if (rd) {
         const int nnew = S.r_new;
-        if (S.removals) {
+        if (S.removals == 1) {  // the evicted suffix is cut off, admissions are appended
+          const int cut = S.cut;
+          for (int q = tid; q < nnew; q += NT) {
+            run[cut + q] = s_new[q];
+            s_rpos[s_new[q]] = (int16_t)(cut + q);
+          }
+          cnt = cut + nnew;
+          __syncthreads();
+        } else if (S.removals) {
           int16_t* nrl = S.cur ? s_runA : s_runB;
           auto src = [&](int q) -> int { return q < nrun ? run[q] : s_new[q - nrun]; };
           cnt = block_compact<NT, IPT_>(
@@ -1202,12 +1270,18 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? 2 : 1)) sim_kernel(KParams 
     }
   }
 #ifdef SIMSWEEP_PROFILE
-  if (tid == 0 && ci < PROF_MAX_CFG)
+  if (tid == 0 && ci < PROF_MAX_CFG) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    prof[14] = (long long)t_start, prof[15] = (long long)t_end, prof[9] = smid;
     for (int i = 0; i < 16; i++) g_prof[ci][i] = prof[i];
+  }
 #endif
 
   // ---- a11: metrics ----
-  const int st = S.status == -1 ? SIM_S_OK : S.status;
+  const int st = exit_status == -1 ? SIM_S_OK : exit_status;
   __threadfence();
   __syncthreads();
   if (st != SIM_S_OK) {  // failed simulations: zero-filled rows

@@ -144,6 +144,8 @@ int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* 
     if (cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V.smem) !=
         cudaSuccess)
       return SIM_ECUDA;
+    // state is shared-memory resident: take the largest carveout so that more CTAs fit per SM
+    cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     kp.variant = v;
     void* args[] = {&kp};
     if (cudaLaunchKernel((const void*)V.fn, dim3(n_cfgs), dim3(V.nt), args, V.smem, (cudaStream_t)stream) !=

@@ -16,8 +16,8 @@ from paper_2411_07447_b200 import build  # noqa: E402
 
 PRODUCT = "--product" in sys.argv  # use the product library (no phase counters), e.g. under ncu
 if not PRODUCT:
-    prof_lib = build.LIB.replace(".so", "_prof.so")
-    if not os.path.exists(prof_lib) or "--rebuild" in sys.argv:
+    prof_lib = os.environ.get("PROBE_LIB") or build.LIB.replace(".so", "_prof.so")
+    if not os.path.exists(prof_lib) or "--rebuild" in sys.argv:  # noqa
         build.build(profile=True)
     os.environ["SIMSWEEP_LIB"] = prof_lib
 

@@ -1,0 +1,32 @@
+"""Per-simulation start/end timeline of one grid sweep (profiling build): is the sweep bound by its
+critical path or by aggregate work?   python tools/timeline.py"""
+import ctypes, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2411_07447_b200 import build
+os.environ["SIMSWEEP_LIB"] = os.environ.get("PROBE_LIB") or build.LIB.replace(".so", "_prof.so")
+import numpy as np, torch
+from paper_2411_07447_b200 import simsweep, sweep
+L = simsweep.lib()
+L.sim_debug_read.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+cfgs, wls, cms, labels = sweep.grid_sweep()
+order = sweep.partition_lpt(sweep.estimate(cfgs, wls), 1)[0]
+ds = simsweep.DeviceSweep(cfgs, wls, cms, order=np.asarray(order, np.int32))
+ds.launch(); torch.cuda.synchronize(); ds.launch(); torch.cuda.synchronize()
+prof = np.zeros((len(cfgs), 16), np.int64)
+L.sim_debug_read(prof.ctypes.data, len(cfgs))
+res = ds.fetch().results
+t0 = prof[:, 14].min()
+st = (prof[:, 14] - t0) / 1e6
+en = (prof[:, 15] - t0) / 1e6
+du = en - st
+print(f"sweep makespan {en.max():.2f} ms; sum of sim durations {du.sum():.1f} ms; "
+      f"mean concurrency {du.sum() / en.max():.0f}; longest sim {du.max():.2f} ms")
+idx = np.argsort(-en)[:25]
+print("latest-finishing simulations:  label  start  duration  end  steps  launch-rank  est")
+est = sweep.estimate(cfgs, wls)
+rank = {c: r for r, c in enumerate(order)}
+for i in idx:
+    print(f"  {labels[i]!s:32s} {st[i]:7.2f} {du[i]:7.2f} {en[i]:7.2f} {int(res['steps'][i]):7d} {rank[i]:5d} {est[i]:9.0f}")
+hist = np.histogram(st, bins=[0, 1, 5, 10, 20, 40, 80])[0]
+print("start-time histogram [0,1,5,10,20,40,80] ms:", hist)
