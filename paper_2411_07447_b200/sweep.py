@@ -72,7 +72,7 @@ def gather_results(local: np.ndarray, local_idx, n_total: int, group=None, devic
         out[np.asarray(local_idx, np.int64)] = local
         return out
     item = simsweep.RESULT_DTYPE.itemsize
-    counts = torch.tensor([len(local_idx)], dtype=torch.int64, device=device)
+    counts = torch.tensor([len(local_idx)], dtype=torch.int64, device=device if device is not None else "cpu")
     allc = [torch.zeros_like(counts) for _ in range(world)]
     dist.all_gather(allc, counts, group=group)
     cap = int(max(int(c.item()) for c in allc))
@@ -80,8 +80,9 @@ def gather_results(local: np.ndarray, local_idx, n_total: int, group=None, devic
     slab[: len(local_idx) * item] = np.frombuffer(local.tobytes(), np.uint8)
     slab[cap * item: cap * item + 8 * len(local_idx)] = np.frombuffer(
         np.asarray(local_idx, np.int64).tobytes(), np.uint8)
-    t = torch.from_numpy(slab).to(device)
-    big = torch.empty(world * t.numel(), dtype=torch.uint8, device=device)
+    dev = device if device is not None else torch.device("cpu")
+    t = torch.from_numpy(slab).to(dev)
+    big = torch.empty(world * t.numel(), dtype=torch.uint8, device=dev)
     dist.all_gather_into_tensor(big, t, group=group)
     if dist.get_rank(group) != 0:
         return None
