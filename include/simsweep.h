@@ -9,9 +9,10 @@
  * The semantics of every step are the readings Q1-Q38 of DESIGN.md.
  *
  * Conventions (all entry points):
- *  - plain pointers and sizes only; the CALLER owns every buffer.  The library
- *    keeps no global state, allocates only transient device scratch, and is
- *    reentrant.
+ *  - plain pointers and sizes only; the CALLER owns every buffer.  sim_sweep()
+ *    keeps one device arena, one pinned staging buffer and one stream per device
+ *    for reuse across calls (grow-only, mutex-guarded: calls are thread-safe and
+ *    serialized per device); sim_sweep_device() allocates nothing.
  *  - return value: 0 on success, < 0 on a call-level error (SIM_EINVAL ...;
  *    sim_strerror() names it).  Problems of one simulation are reported in its
  *    sim_result_t.status (SIM_S_*), never in the return value.
@@ -135,8 +136,9 @@ typedef struct {
 /* Simulate n_cfgs configurations.  HOST buffers: cfgs[n_cfgs], wls[n_wls]
  * (with host arrays), cms[n_cms], results[n_cfgs] and req (sized by the
  * offsets above; any member may be NULL to skip it).  Uses CUDA device
- * `device` (or the current device if < 0); all device memory is transient.
- * Returns 0 / SIM_E*.  Blocking. */
+ * `device` (or the current device if < 0).  Inputs are staged into a cached
+ * pinned buffer and copied with one H2D; outputs are copied straight into the
+ * caller's buffers (pinned buffers are fastest).  Returns 0 / SIM_E*.  Blocking. */
 int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
               const sim_cost_model_t* cms, int32_t n_cms, sim_result_t* results, sim_request_out_t req,
               int32_t device);

@@ -119,6 +119,9 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     S.status = 0;
     S.cur = 0;
     S.w_dirty = S.p_dirty = 1;
+    for (int z = 0; z < 18; z++) S.tot[z] = 0;
+    S.totmin = NOBRK;
+    S.wstale = 0;
   }
   if (tid < K) S.cm[tid] = p.cms[cfg.cost[tid]];
   for (int i = tid; i < 18 * 18; i += NT) S.hist[i] = 0;
@@ -588,7 +591,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     // failure; drop that failure} -- rejections change no state.  A cropped chunk (chunked prefill)
     // exhausts the token budget and ends the group.
     auto warp_np = [&](int src, int b0, int b1) {
+      // one call sees one kind: waiting (src 1: KV delta = s = c for a full admission) or running prefills
+      // (src 2 / 0: KV delta 0); counts come from ballots, so only the token prefix is scanned
       const bool overWin = src == 1;
+      const unsigned lt = (1u << lane) - 1u;
       for (int i0 = b0; i0 < b1; i0 += 32) {
         if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining one fails
         if (overWin && ((finiteM && (long long)U + minSW > M) || (!chunked && minSW > C - tok))) return;
@@ -609,30 +615,30 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         }
         const int4 rc = s_rec[sl < 0 ? 0 : sl];
         const uint8_t fl = s_fl[sl < 0 ? 0 : sl];
-        const bool isW = (fl & ST_MASK) == ST_WAIT;
         const int s = rc.x + rc.y, avail = s - rc.z;
-        const int dkv = isW ? s : 0;  // KV delta (Q13)
-        const int rem = (hist && isW) ? max(S.pred[bucket_of(rc.x)] - rc.y, 0) : 0;
+        const int dkv = overWin ? s : 0;  // KV delta (Q13)
+        const int rem = (hist && overWin) ? max(S.pred[bucket_of(rc.x)] - rc.y, 0) : 0;
         bool alive = sl >= 0;
         for (;;) {
           const int rt = C - tok;
           const bool anyRun0 = n_running > 0;
           bool fit = alive && rt >= 1 && (chunked || avail <= rt) && (!finiteM || U + dkv <= M);
-          if (hist && isW) fit = fit && !(anyRun0 && (long long)U + Rs + s + rem > M);
-          if (!__any_sync(FM, fit)) break;
-          const int cc = fit ? avail : 0, dd = fit ? dkv : 0, kk = fit, ww = fit && isW, rr = fit ? rem : 0;
-          int xc = cc, xd = dd, xk = kk, xw = ww, xr = rr;
+          if (hist && overWin) fit = fit && !(anyRun0 && (long long)U + Rs + s + rem > M);
+          const unsigned fm = __ballot_sync(FM, fit);
+          if (!fm) break;
+          const int cc = fit ? avail : 0, rr = fit ? rem : 0;
+          int xc = cc, xr = rr;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
-            const int yc = __shfl_up_sync(FM, xc, o), yd = __shfl_up_sync(FM, xd, o);
-            const int yk = __shfl_up_sync(FM, xk, o), yw = __shfl_up_sync(FM, xw, o);
-            if (lane >= o) xc += yc, xd += yd, xk += yk, xw += yw;
-            if (hist) {
+            const int yc = __shfl_up_sync(FM, xc, o);
+            if (lane >= o) xc += yc;
+            if (hist && overWin) {
               const int yr = __shfl_up_sync(FM, xr, o);
               if (lane >= o) xr += yr;
             }
           }
-          const int ec = xc - cc, ed = xd - dd, ek = xk - kk, ew = xw - ww, er = xr - rr;
+          const int ec = xc - cc, er = xr - rr, ek = __popc(fm & lt);
+          const int ed = overWin ? ec : 0;  // full admissions before this lane reserve exactly their c
           bool brk = false, crop = false;
           if (fit) {
             const int prt = rt - ec;
@@ -641,7 +647,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             else
               brk = avail > prt;
             if (finiteM) brk |= U + ed + dkv > M;
-            if (hist && isW) brk |= (anyRun0 || ek > 0) && (long long)U + ed + Rs + er + s + rem > M;
+            if (hist && overWin) brk |= (anyRun0 || ek > 0) && (long long)U + ed + Rs + er + s + rem > M;
             if (crop && prt <= 0) brk = true;
           }
           const unsigned bm = __ballot_sync(FM, brk), cm = __ballot_sync(FM, crop && !brk);
@@ -651,33 +657,36 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           if (adm || adc) {
             s_c[sl] = adm ? avail : rt - ec;
             s_bl[nB + ek] = (int16_t)sl;
-            if (isW) {
-              s_seq[sl] = seq + ew + 1;
+            if (overWin) {
+              s_seq[sl] = seq + ek + 1;
               s_rec[sl] = make_int4(rc.x, rc.y, 0, s);
               s_fl[sl] = ST_RUN | F_INB | (fl & F_FIRST);
-              s_new[n_new + ew] = (int16_t)sl;
+              s_new[n_new + ek] = (int16_t)sl;
             } else {
               s_fl[sl] = fl | F_INB;
             }
             alive = false;
           }
           const bool cropped = cl < b && cl < 32;
+          const int nadm = __popc(fm & (stop >= 32 ? FM : ((1u << stop) - 1u)));
           const int lastl = stop > 0 ? min(stop, 32) - 1 : 0;
           const int addc = stop > 0 ? __shfl_sync(FM, xc, lastl) : 0;
-          const int addd = stop > 0 ? __shfl_sync(FM, xd, lastl) : 0;
-          const int addk = stop > 0 ? __shfl_sync(FM, xk, lastl) : 0;
-          const int addw = stop > 0 ? __shfl_sync(FM, xw, lastl) : 0;
-          const int addr = stop > 0 ? __shfl_sync(FM, xr, lastl) : 0;
-          const int cropc = cropped ? __shfl_sync(FM, rt - ec, cl) : 0;
-          const int cropd = cropped ? __shfl_sync(FM, dkv, cl) : 0;
-          const int cropw = cropped ? __shfl_sync(FM, (int)isW, cl) : 0;
-          const int cropr = cropped ? __shfl_sync(FM, rem, cl) : 0;
+          const int addr = (hist && overWin && stop > 0) ? __shfl_sync(FM, xr, lastl) : 0;
+          int cropc = 0, crops = 0, cropr = 0;
+          if (cropped) {
+            cropc = __shfl_sync(FM, rt - ec, cl);
+            crops = __shfl_sync(FM, s, cl);
+            if (hist && overWin) cropr = __shfl_sync(FM, rem, cl);
+          }
+          const int nall = nadm + (cropped ? 1 : 0);
           tok += addc + cropc;
-          U += addd + cropd;
-          seq += addw + cropw, n_new += addw + cropw, n_running += addw + cropw;
-          nB += addk + (cropped ? 1 : 0);
-          Rs += addr + cropr;
-          if ((addk > 0 || cropped) && bph < 0) bph = PH_PRE;
+          if (overWin) {
+            U += addc + crops;
+            seq += nall, n_new += nall, n_running += nall;
+            Rs += addr + cropr;
+          }
+          nB += nall;
+          if (nall > 0 && bph < 0) bph = PH_PRE;
           if (cropped) return;  // the token budget is exhausted: every later candidate is rejected
           if (b < 32 && lane == b) alive = false;  // rejected (no state change)
           if (b >= 32) break;
@@ -1026,32 +1035,43 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           for (int k = 0; k < SIM_MAX_COST; k++) pce[k] = warp_sum(pce[k]);
         }
       }
-      if (lane == 0) {
-        long long* w = S.wred[wid];
-        w[0] = N, w[1] = np_, w[2] = cp, w[3] = mp, w[4] = nd, w[5] = md, w[6] = freed, w[7] = ndone;
-        w[8] = mdn, w[9] = nfill, w[10] = minrem, w[11] = c2, w[12] = mc, w[13] = pcm;
-        w[14] = pce[0], w[15] = pce[1], w[16] = pce[2], w[17] = pce[3];
+      if (lane == 0) {  // warp partials straight into the block totals (RED.shared)
+        atomicAdd(&S.tot[0], (unsigned long long)N), atomicAdd(&S.tot[1], (unsigned long long)np_);
+        atomicAdd(&S.tot[2], (unsigned long long)cp), atomicAdd(&S.tot[3], (unsigned long long)mp);
+        atomicAdd(&S.tot[4], (unsigned long long)nd), atomicAdd(&S.tot[5], (unsigned long long)md);
+        atomicAdd(&S.tot[6], (unsigned long long)freed), atomicAdd(&S.tot[7], (unsigned long long)ndone);
+        atomicAdd(&S.tot[8], (unsigned long long)mdn), atomicAdd(&S.tot[9], (unsigned long long)nfill);
+        atomicMin(&S.totmin, minrem);
+        if (np_ > 0) {
+          atomicAdd(&S.tot[11], (unsigned long long)c2), atomicAdd(&S.tot[12], (unsigned long long)mc);
+          if (anyTheo) {
+            atomicAdd(&S.tot[13], (unsigned long long)pcm);
+            for (int k = 0; k < SIM_MAX_COST; k++) atomicAdd(&S.tot[14 + k], (unsigned long long)pce[k]);
+          }
+        }
       }
-      // clear the preempted-this-step marks (Q9 applies within one step)
-      if (tid < 32) {
+      // clear the preempted-this-step marks (Q9 applies within one step); smallest s among the victims
+      // (they join R_w)
+      if (wid == 0) {
         const int nv = S.n_vic;
-        for (int v = lane; v < nv; v += 32) s_fl[s_vic[v]] &= ~F_PRE;
-      }
-      __syncthreads();
-      if (wid == 0) {  // warp 0 folds the per-warp partials (lane z owns column z)
-        int vmin = 0x7fffffff;  // smallest s among this step's victims (they join R_w)
-        for (int v = lane; v < S.n_vic; v += 32) {
-          const int4 rc = s_rec[s_vic[v]];
+        int vmin = 0x7fffffff;
+        for (int v = lane; v < nv; v += 32) {
+          const int sl = s_vic[v];
+          s_fl[sl] &= ~F_PRE;
+          const int4 rc = s_rec[sl];
           vmin = min(vmin, rc.x + rc.y);
         }
         vmin = (int)__reduce_min_sync(FM, (unsigned)vmin);
-        long long t = (lane == 10) ? NOBRK : 0;
-        if (lane < 18)
-          for (int w = 0; w < NW; w++) t = (lane == 10) ? min(t, S.wred[w][10]) : t + S.wred[w][lane];
+        if (lane == 0) S.vmin = vmin;
+      }
+      __syncthreads();
+      if (tid == 0) {
         long long tt[18];
-#pragma unroll
-        for (int z = 0; z < 18; z++) tt[z] = __shfl_sync(FM, t, z);
-        if (lane == 0) {
+        for (int z = 0; z < 18; z++) tt[z] = (long long)S.tot[z], S.tot[z] = 0;
+        tt[10] = S.totmin;
+        S.totmin = NOBRK;
+        const int vmin = S.vmin;
+        {
           Feat f;
           f.N = tt[0], f.np = tt[1], f.cp = tt[2], f.mp = tt[3], f.nd = tt[4], f.md = tt[5];
           f.c2 = tt[11], f.mc = tt[12], f.pcm = tt[13];
@@ -1091,9 +1111,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           S.r_dirty = changed;
           // removals only as the closed form's evicted suffix: the run list is cut, not compacted
           S.removals = S.h_pre || ndn > 0 ? 2 : (S.any_pre ? 1 : 0);
-          // R_w gains this step's victims (exact min update) and loses admissions (full recount)
-          S.w_dirty = n_new > 0 || arrived;
-          S.nW = nW + S.n_vic, S.minSW = min(minSW, vmin), S.wbuilt = wbuilt && S.n_vic == 0;
+          // R_w gains this step's victims and loses its admissions: |R_w| stays exact; the smallest s becomes a
+          // lower bound after admissions (the skip tests only get conservative) and is recounted every 32 of them
+          S.nW = nW - n_new + S.n_vic, S.minSW = min(minSW, vmin), S.wbuilt = wbuilt && S.n_vic == 0 && n_new == 0;
+          if (n_new > 0) S.wstale++;
+          S.w_dirty = arrived || S.wstale >= 32;
+          if (S.w_dirty) S.wstale = 0;
           S.rank_dirty = ndn > 0;
           // SRF order can change unless every running request was a decode in B (all +1)
           S.o_dirty = srf && (changed || f.np > 0 || f.nd != nrun);

@@ -5,6 +5,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstring>
+#include <mutex>
 #include <cmath>
 #include <numeric>
 #include <vector>
@@ -72,6 +74,7 @@ Variant make_variant() {
 static Variant g_variants[2] = {make_variant<SIM_NT_SMALL, 1024, 1024 / SIM_NT_SMALL>(), make_variant<512, 4096, 4>()};
 
 static int check_cuda(cudaError_t e) { return e == cudaSuccess ? 0 : SIM_ECUDA; }
+static unsigned g_attr_set[64];  // kernel attributes already set, per device and variant
 
 }  // namespace simsweep
 
@@ -141,11 +144,16 @@ int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* 
   for (int v = 1; v >= 0; v--) {
     if (!need[v]) continue;
     const Variant& V = g_variants[v];
-    if (cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V.smem) !=
-        cudaSuccess)
-      return SIM_ECUDA;
-    // state is shared-memory resident: take the largest carveout so that more CTAs fit per SM
-    cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !(g_attr_set[dev] >> v & 1)) {
+      if (cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V.smem) !=
+          cudaSuccess)
+        return SIM_ECUDA;
+      // state is shared-memory resident: take the largest carveout so that more CTAs fit per SM
+      cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      g_attr_set[dev] |= 1u << v;
+    }
     kp.variant = v;
     void* args[] = {&kp};
     if (cudaLaunchKernel((const void*)V.fn, dim3(n_cfgs), dim3(V.nt), args, V.smem, (cudaStream_t)stream) !=
@@ -192,16 +200,56 @@ static int validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload
   return 0;
 }
 
-// longest-processing-time-first estimate of one simulation's step count
-static double estimate_steps(const sim_config_t& c, const sim_workload_t& w) {
-  double sumIO = 0, sumI = 0, maxO = 0;
+// longest-processing-time-first estimate of one simulation's step count from per-workload statistics
+struct WlStats {
+  double sumIO, sumI, maxO;
+};
+
+static WlStats workload_stats(const sim_workload_t& w) {
+  WlStats st{0, 0, 0};
   for (int i = 0; i < w.n; i++) {
-    sumIO += ((double)w.I[i] + 0.5 * w.O[i]) * w.O[i];
-    sumI += w.I[i];
-    maxO = std::max(maxO, (double)w.O[i]);
+    st.sumIO += ((double)w.I[i] + 0.5 * w.O[i]) * w.O[i];
+    st.sumI += w.I[i];
+    st.maxO = std::max(st.maxO, (double)w.O[i]);
   }
+  return st;
+}
+
+static double estimate_steps(const sim_config_t& c, const WlStats& st) {
   const double Meff = c.M >= 0 ? (double)std::max<int64_t>(c.M, 1) : 1e18;
-  return maxO + sumIO / Meff + sumI / (double)c.C;
+  return st.maxO + st.sumIO / Meff + st.sumI / (double)c.C;
+}
+
+// Per-device cache of the host entry point: one device arena, one pinned staging buffer and one stream,
+// grown on demand and reused across calls (guarded by a mutex; released at process exit).
+struct DevCache {
+  std::mutex mu;
+  char* dbuf = nullptr;
+  size_t dcap = 0;
+  char* hbuf = nullptr;
+  size_t hcap = 0;
+  cudaStream_t stream = nullptr;
+  int checked = 0;  // 1 = sm_100 device, -1 = unsupported
+};
+static DevCache g_cache[64];
+
+static int cache_reserve(DevCache& c, size_t dbytes, size_t hbytes) {
+  if (!c.stream && cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess) return SIM_ECUDA;
+  if (dbytes > c.dcap) {
+    if (c.dbuf) cudaFree(c.dbuf);
+    c.dcap = 0;
+    const size_t want = dbytes + dbytes / 4;
+    if (cudaMalloc(&c.dbuf, want) != cudaSuccess) return SIM_ECUDA;
+    c.dcap = want;
+  }
+  if (hbytes > c.hcap) {
+    if (c.hbuf) cudaFreeHost(c.hbuf);
+    c.hcap = 0;
+    const size_t want = hbytes + hbytes / 4;
+    if (cudaMallocHost(&c.hbuf, want) != cudaSuccess) return SIM_ECUDA;
+    c.hcap = want;
+  }
+  return 0;
 }
 
 int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
@@ -214,10 +262,15 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return SIM_ENODEV;
   if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return SIM_ECUDA;
   int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return SIM_ECUDA;
-  if (prop.major != 10) return SIM_ENODEV;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return SIM_ECUDA;
+  DevCache& cache = g_cache[dev];
+  std::lock_guard<std::mutex> lock(cache.mu);
+  if (cache.checked == 0) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return SIM_ECUDA;
+    cache.checked = prop.major == 10 ? 1 : -1;
+  }
+  if (cache.checked < 0) return SIM_ENODEV;
 
   std::vector<int64_t> row_off(n_cfgs), tim_off(n_cfgs);
   int64_t rows = 0, trows = 0;
@@ -227,8 +280,10 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
     rows += wls[cfgs[i].workload].n;
     trows += (int64_t)cfgs[i].n_cost * wls[cfgs[i].workload].n;
   }
+  std::vector<WlStats> stats(n_wls);
+  for (int w = 0; w < n_wls; w++) stats[w] = workload_stats(wls[w]);
   std::vector<double> est(n_cfgs);
-  for (int i = 0; i < n_cfgs; i++) est[i] = estimate_steps(cfgs[i], wls[cfgs[i].workload]);
+  for (int i = 0; i < n_cfgs; i++) est[i] = estimate_steps(cfgs[i], stats[cfgs[i].workload]);
   std::vector<int32_t> order(n_cfgs);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return est[a] > est[b]; });
@@ -236,7 +291,7 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
   int64_t wtot = 0;
   for (int w = 0; w < n_wls; w++) wn[w] = wls[w].n, wtot += wls[w].n;
 
-  // one device arena: cfgs | wls | cms | order | row_off | tim_off | results | I O T | outputs
+  // arena layout: inputs (staged in pinned memory, one H2D) | outputs
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   size_t off = 0;
   const size_t o_cfg = off;
@@ -251,14 +306,15 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
   off = al(off + 8 * (size_t)n_cfgs);
   const size_t o_to = off;
   off = al(off + 8 * (size_t)n_cfgs);
-  const size_t o_res = off;
-  off = al(off + sizeof(sim_result_t) * n_cfgs);
   const size_t o_I = off;
   off = al(off + 4 * (size_t)wtot);
   const size_t o_O = off;
   off = al(off + 4 * (size_t)wtot);
   const size_t o_T = off;
   off = al(off + 8 * (size_t)wtot);
+  const size_t in_bytes = off;
+  const size_t o_res = off;
+  off = al(off + sizeof(sim_result_t) * n_cfgs);
   const size_t o_tf = off;
   off = al(off + 8 * (size_t)trows);
   const size_t o_td = off;
@@ -267,14 +323,13 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
   off = al(off + 8 * (size_t)rows);
   const size_t o_rf = off;
   off = al(off + 8 * (size_t)rows);
-  char* base = nullptr;
-  if (cudaMalloc(&base, off) != cudaSuccess) return SIM_ECUDA;
-  cudaStream_t s;
-  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
-    cudaFree(base);
-    return SIM_ECUDA;
-  }
-  std::vector<sim_workload_t> dw(n_wls);
+  if ((rc = cache_reserve(cache, off, in_bytes))) return rc;
+  char* base = cache.dbuf;
+  char* h = cache.hbuf;
+  cudaStream_t s = cache.stream;
+  // the previous call's stream work has completed (it synchronized before returning)
+  std::memcpy(h + o_cfg, cfgs, sizeof(sim_config_t) * n_cfgs);
+  sim_workload_t* dw = reinterpret_cast<sim_workload_t*>(h + o_wl);
   int64_t wo = 0;
   for (int w = 0; w < n_wls; w++) {
     dw[w].n = wls[w].n;
@@ -282,22 +337,16 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
     dw[w].I = reinterpret_cast<const int32_t*>(base + o_I) + wo;
     dw[w].O = reinterpret_cast<const int32_t*>(base + o_O) + wo;
     dw[w].T = reinterpret_cast<const double*>(base + o_T) + wo;
+    std::memcpy(h + o_I + 4 * wo, wls[w].I, 4 * (size_t)wls[w].n);
+    std::memcpy(h + o_O + 4 * wo, wls[w].O, 4 * (size_t)wls[w].n);
+    std::memcpy(h + o_T + 8 * wo, wls[w].T, 8 * (size_t)wls[w].n);
     wo += wls[w].n;
   }
-  rc = 0;
-  rc |= check_cuda(cudaMemcpyAsync(base + o_cfg, cfgs, sizeof(sim_config_t) * n_cfgs, cudaMemcpyHostToDevice, s));
-  rc |= check_cuda(cudaMemcpyAsync(base + o_wl, dw.data(), sizeof(sim_workload_t) * n_wls, cudaMemcpyHostToDevice, s));
-  rc |= check_cuda(cudaMemcpyAsync(base + o_cm, cms, sizeof(sim_cost_model_t) * n_cms, cudaMemcpyHostToDevice, s));
-  rc |= check_cuda(cudaMemcpyAsync(base + o_ord, order.data(), 4 * (size_t)n_cfgs, cudaMemcpyHostToDevice, s));
-  rc |= check_cuda(cudaMemcpyAsync(base + o_ro, row_off.data(), 8 * (size_t)n_cfgs, cudaMemcpyHostToDevice, s));
-  rc |= check_cuda(cudaMemcpyAsync(base + o_to, tim_off.data(), 8 * (size_t)n_cfgs, cudaMemcpyHostToDevice, s));
-  wo = 0;
-  for (int w = 0; w < n_wls && !rc; w++) {
-    rc |= check_cuda(cudaMemcpyAsync(base + o_I + 4 * wo, wls[w].I, 4 * (size_t)wls[w].n, cudaMemcpyHostToDevice, s));
-    rc |= check_cuda(cudaMemcpyAsync(base + o_O + 4 * wo, wls[w].O, 4 * (size_t)wls[w].n, cudaMemcpyHostToDevice, s));
-    rc |= check_cuda(cudaMemcpyAsync(base + o_T + 8 * wo, wls[w].T, 8 * (size_t)wls[w].n, cudaMemcpyHostToDevice, s));
-    wo += wls[w].n;
-  }
+  std::memcpy(h + o_cm, cms, sizeof(sim_cost_model_t) * n_cms);
+  std::memcpy(h + o_ord, order.data(), 4 * (size_t)n_cfgs);
+  std::memcpy(h + o_ro, row_off.data(), 8 * (size_t)n_cfgs);
+  std::memcpy(h + o_to, tim_off.data(), 8 * (size_t)n_cfgs);
+  rc = check_cuda(cudaMemcpyAsync(base, h, in_bytes, cudaMemcpyHostToDevice, s));
   sim_request_out_t dreq;
   dreq.t_first = reinterpret_cast<double*>(base + o_tf);
   dreq.t_done = reinterpret_cast<double*>(base + o_td);
@@ -320,11 +369,9 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
       rc |= check_cuda(cudaMemcpyAsync(req.n_preempt, dreq.n_preempt, 8 * rows, cudaMemcpyDeviceToHost, s));
     if (req.refill_tokens)
       rc |= check_cuda(cudaMemcpyAsync(req.refill_tokens, dreq.refill_tokens, 8 * rows, cudaMemcpyDeviceToHost, s));
-    rc |= check_cuda(cudaStreamSynchronize(s));
   }
-  cudaStreamDestroy(s);
-  cudaFree(base);
-  return rc ? SIM_ECUDA : 0;
+  rc |= check_cuda(cudaStreamSynchronize(s));
+  return rc ? (rc < 0 ? rc : SIM_ECUDA) : 0;
 }
 
 }  // extern "C"
