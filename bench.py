@@ -69,7 +69,7 @@ def _oracle_job(args):
     from paper_2411_07447_b200 import presets
 
     p = presets.preset(name)
-    cfg = o.make_config(p["order"], p["hybrid"], p["chunked"], p["replacement"], C=p["C"], M=M)
+    cfg = o.make_config(p["order"], p["hybrid"], p["chunked"], p["replacement"], C=p["C"], M=M, reserve=p["reserve"])
     cm = o.load_cost_models()["llama3-8b_a100_linear"]
     from paper_2411_07447_b200 import workloads
 

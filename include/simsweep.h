@@ -36,9 +36,17 @@ enum {
 };
 /* cache replacement policy on preemption */
 enum {
-  SIM_NRF = 0,     /* newest (most recently admitted) request first, Table 2 */
-  SIM_SRF = 1,     /* shortest (smallest m) request first */
-  SIM_SRF_HIST = 2 /* SRF + online output-length histogram deferral */
+  SIM_NRF = 0,      /* newest (most recently admitted) request first, Table 2 */
+  SIM_SRF = 1,      /* shortest (smallest m) request first */
+  SIM_SRF_HIST = 2, /* SRF + online output-length histogram deferral */
+  SIM_PF = 3        /* preemption-free (Table 2): never preempts; requires a
+                       PEAK or CONTEXT reserve; running order = admission order (reading Q39) */
+};
+/* initial KV reserve at (re)admission (Table 2 "Initial KV reserve") */
+enum {
+  SIM_RESERVE_SEQ = 0,    /* s = I + g: r.I for vLLM / Sarathi, generalised to refills (reading Q13) */
+  SIM_RESERVE_PEAK = 1,   /* I + O - 1: the *^pf schedulers */
+  SIM_RESERVE_CONTEXT = 2 /* S: Orca */
 };
 /* per-simulation status */
 enum {
@@ -47,11 +55,12 @@ enum {
   SIM_S_NEVER_FITS = 2, /* I+O-1 > M, or > C without chunked prefill (reading Q35) */
   SIM_S_MAX_STEPS = 3,  /* more than max_steps batches */
   SIM_S_DEADLOCK = 4,   /* B empty, nothing arriving, requests unfinished (defensive) */
-  SIM_S_CAPACITY = 5    /* more than SIM_MAX_WINDOW arrived-but-unfinished requests */
+  SIM_S_CAPACITY = 5    /* more than SIM_MAX_WINDOW arrived-but-unfinished requests (only if n > SIM_MAX_WINDOW) */
 };
 /* call-level errors */
 enum {
-  SIM_EINVAL = -1,    /* NULL pointer, n <= 0, bad enum, C not in [1, 2^30], M > 2^30, S not in [1, 2^18), n_cost not 1..4 */
+  SIM_EINVAL = -1,    /* NULL pointer, n <= 0, bad enum, C not in [1, 2^30], M > 2^30, S not in [1, 2^18), n_cost not 1..4,
+                         replacement == SIM_PF without a PEAK / CONTEXT reserve or vice versa */
   SIM_EWORKLOAD = -2, /* I < 1, O < 1, T not sorted, or T != 0 with n_cost > 1 */
   SIM_ECOST = -3,     /* cost-model index out of range or bad cost-model fields */
   SIM_ECUDA = -4,     /* a CUDA runtime error (device, allocation, launch) */
@@ -60,15 +69,17 @@ enum {
 
 #define SIM_MAX_COST 4
 /* largest simultaneously tracked request window (arrived and not finished,
- * counted from the oldest unfinished request); larger -> SIM_S_CAPACITY */
-#define SIM_MAX_WINDOW 4096
+ * counted from the oldest unfinished request); larger -> SIM_S_CAPACITY.
+ * Workloads of n <= 4096 requests never exceed it (state in shared memory);
+ * larger ones use a per-simulation arena of the caller's workspace. */
+#define SIM_MAX_WINDOW 32768
 
 /* One simulation.  72 bytes, naturally aligned. */
 typedef struct {
   int32_t order;       /* SIM_ORDER_* */
   int32_t hybrid;      /* 0/1: hybrid prefill+decode batches (step 2) */
   int32_t chunked;     /* 0/1: chunked prefill */
-  int32_t replacement; /* SIM_NRF / SIM_SRF / SIM_SRF_HIST */
+  int32_t replacement; /* SIM_NRF / SIM_SRF / SIM_SRF_HIST / SIM_PF */
   int32_t S;           /* model context size; requests need I+O-1 <= S */
   int32_t workload;    /* index into the workload table */
   int64_t C;           /* token limit per batch, 1 .. 2^30 */
@@ -76,7 +87,7 @@ typedef struct {
   int64_t max_steps;   /* livelock guard (>= 1) */
   int32_t n_cost;      /* 1..4 cost models charged on the same schedule; > 1 only for offline (all T = 0) */
   int32_t cost[SIM_MAX_COST]; /* indices into the cost-model table; the clock of cost[0] drives arrivals */
-  int32_t reserved0;
+  int32_t reserve;     /* SIM_RESERVE_*; != SEQ iff replacement == SIM_PF */
 } sim_config_t;
 
 /* One workload: n requests sorted by (T, id).  The pointers are HOST memory
@@ -152,12 +163,22 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
  * (device, may be NULL) is a permutation giving the launch order (e.g.
  * longest-first).  Launches asynchronously on `stream` (cudaStream_t, NULL =
  * legacy default stream) and does not synchronize; validation of workload
- * contents is the caller's responsibility (sim_sweep does it).  Returns the
- * number of kernel launches issued (>= 1) or SIM_E*. */
+ * contents is the caller's responsibility (sim_sweep does it).  d_workspace
+ * (device, caller-owned, may be NULL when sim_workspace_bytes() is 0) holds
+ * the state of simulations whose workload has n > 4096 requests; its first 4
+ * bytes are reset on `stream` before use, so one workspace serves successive
+ * calls on one stream.  Returns the number of kernel launches issued (>= 1) or
+ * SIM_E* (SIM_EINVAL if the workspace is missing or smaller than needed). */
 int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n,
                      const sim_config_t* d_cfgs, const sim_workload_t* d_wls, const sim_cost_model_t* d_cms,
                      int32_t n_cms, const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
-                     sim_result_t* d_results, sim_request_out_t d_req, void* stream);
+                     sim_result_t* d_results, sim_request_out_t d_req, void* d_workspace,
+                     int64_t workspace_bytes, void* stream);
+
+/* Device workspace bytes sim_sweep_device() needs for these configs (host
+ * arrays; wls_n = n of each workload): ~1.7 MB per simulation whose workload
+ * has n > 4096 requests, 0 if there is none.  Returns >= 0 or SIM_EINVAL. */
+int64_t sim_workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int32_t* wls_n);
 
 /* Scratch-free helper: total rows of the per-request outputs for n_cfgs configs
  * (rows = sum n_i, tim_rows = sum n_cost_i * n_i).  Returns 0 / SIM_EINVAL. */

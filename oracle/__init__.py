@@ -29,14 +29,16 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.cpp")
 
 ORDERS = {"prefill_first": 0, "decode_first": 1, "rank_org": 2, "rank_i": 3, "rank_o": 4}
-REPLACEMENTS = {"nrf": 0, "srf": 1, "srf_hist": 2}
+REPLACEMENTS = {"nrf": 0, "srf": 1, "srf_hist": 2, "pf": 3}
+RESERVES = {"seq": 0, "peak": 1, "context": 2}
 STATUS = {0: "ok", 1: "too_long", 2: "never_fits", 3: "max_steps", 4: "deadlock"}
 
 
 class OracleConfig(ctypes.Structure):
     _fields_ = [("order", ctypes.c_int32), ("hybrid", ctypes.c_int32), ("chunked", ctypes.c_int32),
                 ("replacement", ctypes.c_int32), ("S", ctypes.c_int32), ("n_cost", ctypes.c_int32),
-                ("C", ctypes.c_int64), ("M", ctypes.c_int64), ("max_steps", ctypes.c_int64)]
+                ("C", ctypes.c_int64), ("M", ctypes.c_int64), ("max_steps", ctypes.c_int64),
+                ("reserve", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class OracleCost(ctypes.Structure):
@@ -143,12 +145,14 @@ class OracleResult:
         raise AttributeError(k)
 
 
-def make_config(order, hybrid, chunked, replacement, C, M, S=4096, max_steps=10_000_000, n_cost=1) -> OracleConfig:
+def make_config(order, hybrid, chunked, replacement, C, M, S=4096, max_steps=10_000_000, n_cost=1,
+                reserve=0) -> OracleConfig:
     c = OracleConfig()
     c.order = ORDERS[order] if isinstance(order, str) else int(order)
     c.hybrid, c.chunked = int(bool(hybrid)), int(bool(chunked))
     c.replacement = REPLACEMENTS[replacement] if isinstance(replacement, str) else int(replacement)
     c.S, c.C, c.M, c.max_steps, c.n_cost = int(S), int(C), int(M), int(max_steps), int(n_cost)
+    c.reserve = RESERVES[reserve] if isinstance(reserve, str) else int(reserve)
     return c
 
 

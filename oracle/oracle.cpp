@@ -48,8 +48,9 @@ int64_t held(const Req& r) { return r.st == RUNNING ? std::max(r.reserved, r.m) 
 //      = most recently (re)admitted (Q6).
 // SRF: "prioritizes running long requests (having large m) and preempts short
 //      requests"; ties: later admission is preempted first (Q7).
+// PF: never preempts; its running order is admission order, as NRF (Q39).
 bool retained_longer(const Req& a, const Req& b, int repl) {
-  if (repl == OR_NRF) return a.seq < b.seq;
+  if (repl == OR_NRF || repl == OR_PF) return a.seq < b.seq;
   if (a.m != b.m) return a.m > b.m;
   return a.seq < b.seq;
 }
@@ -225,7 +226,9 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
   // ---- call-level validation ----
   if (!cfg || !out || n <= 0 || !I || !O || !T || !cms) return -1;
   if (cfg->order < OR_PREFILL_FIRST || cfg->order > OR_RANK_O) return -2;
-  if (cfg->replacement < OR_NRF || cfg->replacement > OR_SRF_HIST) return -2;
+  if (cfg->replacement < OR_NRF || cfg->replacement > OR_PF) return -2;
+  if (cfg->reserve < OR_RESERVE_SEQ || cfg->reserve > OR_RESERVE_CONTEXT) return -2;
+  if ((cfg->replacement == OR_PF) != (cfg->reserve != OR_RESERVE_SEQ)) return -2;  // Q39
   if (cfg->n_cost < 1 || cfg->n_cost > 4) return -3;
   if (cfg->C < 1 || cfg->S < 1 || cfg->max_steps < 1) return -4;
   for (int i = 0; i < n; i++) {
@@ -258,7 +261,9 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
     }
   for (int i = 0; i < n; i++) {
     int64_t peak = (int64_t)I[i] + O[i] - 1;  // peak KV usage I+O-1
-    if ((finiteM && peak > M) || (!cfg->chunked && peak > C)) {
+    // a CONTEXT reserve (Orca) of S > M can never be admitted either (Q35)
+    if ((finiteM && peak > M) || (!cfg->chunked && peak > C) ||
+        (finiteM && cfg->reserve == OR_RESERVE_CONTEXT && cfg->S > M)) {
       out->status = OR_NEVER_FITS;
       return 0;
     }
@@ -278,6 +283,14 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
   int next = 0;
   int64_t steps = 0, seq = 0, U = 0, n_done = 0;
   int status = OR_OK;
+
+  // Table 2 "Initial KV reserve": r.I for vLLM/Sarathi (generalised to s = I + g for
+  // refills), r.I + r.O - 1 for *^pf, S for Orca
+  auto initial_reserve = [&](const Req& r) -> int64_t {
+    if (cfg->reserve == OR_RESERVE_PEAK) return r.I + r.O - 1;
+    if (cfg->reserve == OR_RESERVE_CONTEXT) return cfg->S;
+    return seq_len(r);
+  };
 
   std::vector<int64_t> evs;  // preemption events of the current step: (id, m discarded)
   auto preempt = [&](Req& r) {  // PAPER.md:1644-1646; refill semantics PAPER.md:1570
@@ -370,11 +383,15 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
           if (any_running && U + sumrem + seq_len(r) + rem > M) continue;
         }
         // (3b) KV limit M: post-batch holdings sum max(reserved, m+c) <= M (Q13, Fig. 3)
-        int64_t newheld = std::max(r.st == WAITING ? seq_len(r) : r.reserved, r.m + c);
+        int64_t newheld = std::max(r.st == WAITING ? initial_reserve(r) : r.reserved, r.m + c);
         int64_t delta = newheld - held(r);
         bool fits = true;
         while (finiteM && U + delta > M) {
           if (r.st == WAITING) {  // holds no KVs: skipped, never preempts (Q5)
+            fits = false;
+            break;
+          }
+          if (repl == OR_PF) {  // preemption-free: skipped, never preempts (Table 2)
             fits = false;
             break;
           }
@@ -394,9 +411,9 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
           preempt(R[victim]);
         }
         if (!fits) continue;
-        if (r.st == WAITING) {  // (re)admission: reserve s = I + g (Table 2 "r.I", generalised to refills)
+        if (r.st == WAITING) {  // (re)admission: reserve the Table 2 "Initial KV reserve"
           r.st = RUNNING;
-          r.reserved = seq_len(r);
+          r.reserved = initial_reserve(r);
           r.filled = false;
           r.seq = ++seq;
         }

@@ -19,7 +19,10 @@ extern "C" {
 /* GroupRequests orders (Table 2; App. D) */
 enum { OR_PREFILL_FIRST = 0, OR_DECODE_FIRST = 1, OR_RANK_ORG = 2, OR_RANK_I = 3, OR_RANK_O = 4 };
 /* replacement policies (Table 2; Sec. SRF) */
-enum { OR_NRF = 0, OR_SRF = 1, OR_SRF_HIST = 2 };
+enum { OR_NRF = 0, OR_SRF = 1, OR_SRF_HIST = 2, OR_PF = 3 /* preemption-free, Table 2 PAPER.md:1603,1606 */ };
+/* initial KV reserve at (re)admission (Table 2 column "Initial KV reserve") */
+enum { OR_RESERVE_SEQ = 0 /* s = I + g (r.I) */, OR_RESERVE_PEAK = 1 /* I + O - 1 (*^pf) */,
+       OR_RESERVE_CONTEXT = 2 /* S (Orca) */ };
 /* per-simulation status */
 enum { OR_OK = 0, OR_TOO_LONG = 1, OR_NEVER_FITS = 2, OR_MAX_STEPS = 3, OR_DEADLOCK = 4 };
 
@@ -29,6 +32,8 @@ typedef struct {
   int64_t C;         /* token limit per batch */
   int64_t M;         /* KV capacity in tokens, < 0 = infinite (what-if) */
   int64_t max_steps;
+  int32_t reserve;   /* OR_RESERVE_*; != SEQ iff replacement == OR_PF (reading Q39) */
+  int32_t pad;
 } oracle_config_t;
 
 typedef struct {

@@ -33,6 +33,7 @@ constexpr int PH_DEC = 0, PH_PRE = 1;
 constexpr int NOBRK = 0x7fffffff;
 
 struct KParams {
+  unsigned char* ws;  // large-window variant: [WS_HEADER | arenas], the counter at ws[0]
   const sim_config_t* cfgs;
   const sim_workload_t* wls;
   const sim_cost_model_t* cms;
@@ -65,7 +66,7 @@ struct Scal {
   int cf_red[32][8];
   int pa, cut, h_pre, vmin, totmin, wstale;
   unsigned long long tot[18];  // block totals of the process pass (atomics)
-  int vt, status, any_pre, cur, wbuilt;
+  int vt, status, any_pre, cur, wbuilt, arena;
   int w_dirty, p_dirty, r_dirty, o_dirty, rank_dirty, removals;
   long long r_Rs;  // scalars handed back by thread 0 after a break
   int r_tok, r_U, r_seq, r_new, r_running, r_bph, r_nB, r_wdone;
@@ -312,16 +313,23 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// Per-slot arrays (51 B per slot), relative to the array base: shared memory right after Scal, or (GM
+// variant) a per-CTA arena in a caller-provided global workspace, served from L1/L2.
 template <int NT, int CAP>
 struct Smem {
   static constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-  static constexpr size_t off_rec = align16(sizeof(Scal));          // int4 {I, g, m, res} per slot
+  static constexpr size_t scal = align16(sizeof(Scal));
+  static constexpr size_t off_rec = 0;                              // int4 {I, g, m, res} per slot
   static constexpr size_t off_int = off_rec + 16 * CAP;             // O, seq, c (int32)
   static constexpr size_t off_rpos = off_int + 3 * 4 * CAP;         // position in the run list (int16)
   static constexpr size_t off_fl = off_rpos + 2 * CAP;              // flags (uint8)
   static constexpr size_t off_lists = align16(off_fl + CAP);        // runA runB rank wl pl blist (int16)
-  static constexpr size_t off_union = align16(off_lists + 6 * 2 * CAP);  // new ev vic | dbuf (upper half) | u64 keys
-  static constexpr size_t bytes = off_union + 8 * CAP;
+  // union, 8 B per slot: new (int16) | vic (int16) | ev (int32) -- the steady-run dbuf overlays ev (a steady
+  // run has no events) -- or the u64 sort keys
+  static constexpr size_t off_union = align16(off_lists + 6 * 2 * CAP);
+  static constexpr size_t arr_bytes = (off_union + 8 * CAP + 255) & ~size_t(255);
+  static constexpr size_t bytes = scal + arr_bytes;  // all in shared memory
 };
+constexpr size_t WS_HEADER = 256;  // workspace header: the arena counter
 
 }  // namespace simsweep

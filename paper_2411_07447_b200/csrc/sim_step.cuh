@@ -32,34 +32,43 @@ namespace simsweep {
 enum { K_NONE = 0, K_MARK = 1, K_EVENT = 2 };
 constexpr int WARP_MAX = 256;  // at most this many candidates left in a group: warp-level admission
 
-template <int NT, int CAP, int IPT_>
+template <int NT, int CAP, int IPT_, bool GM>
 __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) : 1)) sim_kernel(KParams p) {
   using L = Smem<NT, CAP>;
   constexpr int NW = NT / 32;
   constexpr int CH = NT * IPT_;  // candidates per round
+  constexpr int SLB = __builtin_ctz(CAP);  // bits of a slot index
+  static_assert((CAP & (CAP - 1)) == 0 && CAP <= 32768, "slots are int16 ring indices");
   constexpr unsigned FM = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem[];
   Scal& S = *reinterpret_cast<Scal*>(smem);
-  int4* s_rec = reinterpret_cast<int4*>(smem + L::off_rec);  // {I, g, m, res}
-  int32_t* s_O = reinterpret_cast<int32_t*>(smem + L::off_int);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int ci = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
+  if (variant_of(p.wls[p.cfgs[ci].workload].n) != p.variant) return;
+  unsigned char* arr = smem + L::scal;
+  if constexpr (GM) {  // claim a per-CTA arena of the workspace
+    if (tid == 0) S.arena = (int)atomicAdd(reinterpret_cast<unsigned*>(p.ws), 1u);
+    __syncthreads();
+    arr = p.ws + WS_HEADER + (size_t)S.arena * L::arr_bytes;
+  }
+  int4* s_rec = reinterpret_cast<int4*>(arr + L::off_rec);  // {I, g, m, res}
+  int32_t* s_O = reinterpret_cast<int32_t*>(arr + L::off_int);
   int32_t* s_seq = s_O + CAP;  // admission sequence number (Q6)
   int32_t* s_c = s_seq + CAP;  // c of the current batch
-  int16_t* s_rpos = reinterpret_cast<int16_t*>(smem + L::off_rpos);
-  uint8_t* s_fl = smem + L::off_fl;
-  int16_t* s_runA = reinterpret_cast<int16_t*>(smem + L::off_lists);
+  int16_t* s_rpos = reinterpret_cast<int16_t*>(arr + L::off_rpos);
+  uint8_t* s_fl = arr + L::off_fl;
+  int16_t* s_runA = reinterpret_cast<int16_t*>(arr + L::off_lists);
   int16_t* s_runB = s_runA + CAP;
   int16_t* s_rank = s_runB + CAP;
   int16_t* s_wl = s_rank + CAP;  // waiting list (index order)
   int16_t* s_pl = s_wl + CAP;    // Sarathi split of the run list (decodes, then prefills)
   int16_t* s_bl = s_pl + CAP;    // the batch B in admission order
-  int16_t* s_new = reinterpret_cast<int16_t*>(smem + L::off_union);  // admitted from waiting this step
-  int16_t* s_ev = s_new + CAP;                                          // first-token / completion events
-  int16_t* s_vic = s_ev + CAP;                                          // preempted this step
-  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem + L::off_union);
-  double* s_dbuf = reinterpret_cast<double*>(smem + L::off_union + 4 * CAP);  // CAP/2 doubles (vic | pad)
+  int16_t* s_new = reinterpret_cast<int16_t*>(arr + L::off_union);  // admitted from waiting this step
+  int16_t* s_vic = s_new + CAP;                                       // preempted this step
+  int32_t* s_ev = reinterpret_cast<int32_t*>(arr + L::off_union + 4 * CAP);  // first-token / completion events
+  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(arr + L::off_union);
+  double* s_dbuf = reinterpret_cast<double*>(arr + L::off_union + 4 * CAP);  // CAP/2 doubles (over ev)
 
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int ci = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
 #ifdef SIMSWEEP_PROFILE
   unsigned long long t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
@@ -67,13 +76,18 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   const sim_config_t cfg = p.cfgs[ci];
   const sim_workload_t wl = p.wls[cfg.workload];
   const int n = wl.n;
-  if (variant_of(n) != p.variant) return;
   const int K = cfg.n_cost;
   const int M = cfg.M >= 0 ? (int)cfg.M : 0, C = (int)cfg.C;  // host-validated < 2^30
   const bool finiteM = cfg.M >= 0, hybrid = cfg.hybrid != 0, chunked = cfg.chunked != 0;
   const int order = cfg.order;
-  const bool srf = cfg.replacement != SIM_NRF;
+  const bool srf = cfg.replacement == SIM_SRF || cfg.replacement == SIM_SRF_HIST;
   const bool hist = cfg.replacement == SIM_SRF_HIST && finiteM;
+  const bool pf = cfg.replacement == SIM_PF;  // preemption-free: a running KV failure is skipped (Table 2)
+  // Table 2 "Initial KV reserve": s = I + g (SEQ), I + O - 1 (PEAK, *^pf), S (CONTEXT, Orca).  Under
+  // PEAK / CONTEXT every running request already holds its peak usage, so its KV delta is 0 (kv1 = false:
+  // a decode needs no KV); under SEQ a filled request's decode needs exactly one.
+  const int rmode = cfg.reserve;
+  const bool kv1 = rmode == SIM_RESERVE_SEQ;
   const bool rank = order >= SIM_ORDER_RANK_ORG;
   const long long row0 = p.row_off[ci], tim0 = p.tim_off[ci];
   double* tf = p.req.t_first + tim0;
@@ -95,6 +109,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     long long pk = (long long)wl.I[i] + wl.O[i] - 1;  // peak KV usage
     bad_long |= pk > cfg.S;
     bad_fit |= (finiteM && pk > cfg.M) || (!chunked && pk > cfg.C);
+    bad_fit |= finiteM && cfg.reserve == SIM_RESERVE_CONTEXT && cfg.S > cfg.M;  // the reserve never fits (Q35)
   }
   bad_long = __syncthreads_or(bad_long);
   bad_fit = __syncthreads_or(bad_fit);
@@ -278,6 +293,9 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     int tok = 0, U = (int)S.U, n_new = 0, n_running = nrun, bph = -1, pos = 0, nB = 0;
     int seq = (int)S.seq;
 
+    auto rnew = [&](const int4& rc, int sl) -> int {  // reserve taken at (re)admission
+      return rmode == SIM_RESERVE_SEQ ? rc.x + rc.y : (rmode == SIM_RESERVE_PEAK ? rc.x + s_O[sl] - 1 : cfg.S);
+    };
     auto preempt = [&](int v) {  // thread 0 only (refill P:1570)
       const int4 rc = s_rec[v];
       U -= max(rc.w, rc.z);
@@ -308,9 +326,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         rem = max(S.pred[bucket_of(rc.x)] - rc.y, 0);
         if (n_running > 0 && (long long)U + Rs + s + rem > M) return;  // deferred (Q31)
       }
-      const int nh = max(isW ? s : rc.w, rc.z + c), held = isW ? 0 : max(rc.w, rc.z), delta = nh - held;
+      const int rw = isW ? rnew(rc, sl) : rc.w;
+      const int nh = max(rw, rc.z + c), held = isW ? 0 : max(rc.w, rc.z), delta = nh - held;
       while (finiteM && U + delta > M) {
-        if (isW) return;  // holds no KVs: skipped (Q5)
+        if (isW || pf) return;  // holds no KVs (Q5) / preemption-free: skipped
         const int pc = s_rpos[sl];
         int vt = S.vt;
         while (vt > pc) {  // lowest retention = tail of the retention-ordered run list
@@ -326,10 +345,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         preempt(run[vt]);
         S.vt = vt - 1;
       }
-      if (isW) {  // (re)admission reserves s = I + g (Table 2, Q13)
+      if (isW) {  // (re)admission takes the initial reserve (Table 2, Q13)
         seq++;
         s_seq[sl] = seq;
-        s_rec[sl] = make_int4(rc.x, rc.y, rc.z, s);
+        s_rec[sl] = make_int4(rc.x, rc.y, rc.z, rw);
         fl = ST_RUN | (fl & F_FIRST);
         s_new[n_new++] = (int16_t)sl;
         n_running++;
@@ -380,9 +399,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           rem = max(S.pred[bucket_of(rc.x)] - rc.y, 0);
           ok = ok && !(anyRun0 && (long long)U + Rs + s + rem > M);
         }
-        const int delta = max(isW ? s : rc.w, rc.z + c) - (isW ? 0 : max(rc.w, rc.z));
+        const int rw = isW ? rnew(rc, sl < 0 ? 0 : sl) : rc.w;
+        const int delta = max(rw, rc.z + c) - (isW ? 0 : max(rc.w, rc.z));
         const bool kvfail = finiteM && U + delta > M;
-        const int kind = !ok ? K_NONE : (kvfail ? (isW ? K_NONE : K_EVENT) : K_MARK);
+        const int kind = !ok ? K_NONE : (kvfail ? ((isW || pf) ? K_NONE : K_EVENT) : K_MARK);
         const bool mk = kind == K_MARK;
         const int cc = mk ? (ph == PH_DEC ? 1 : avail) : 0, dd = mk ? delta : 0, ww = mk && isW, kk = mk;
         const int rr = mk ? rem : 0;
@@ -418,7 +438,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           s_bl[nB + ek] = (int16_t)sl;
           if (isW) {
             s_seq[sl] = seq + ew + 1;
-            s_rec[sl] = make_int4(rc.x, rc.y, rc.z, s);
+            s_rec[sl] = make_int4(rc.x, rc.y, rc.z, rw);
             s_fl[sl] = ST_RUN | F_INB | (fl & F_FIRST);
             s_new[n_new + ew] = (int16_t)sl;
           } else {
@@ -456,7 +476,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     // pf: heads = run[0..k) (prefill-first, non-chunked: every running request decodes),
     // else heads = s_pl[0..k) (R_r^d).  Requires nrun <= CH.
     auto decode_group = [&](bool tail_sync) {  // heads = decodes (F_FILLED) of the run list, retention order
-      const int F = finiteM ? M - U : 0x3fffffff;
+      const bool fM = finiteM && kv1;  // heads need one KV each (else none: admitted up to the token budget)
+      const int F = fM ? M - U : 0x3fffffff;
       const int T = C - tok;
       // (i) reverse scan over run positions of (held, is-head): RS(q) = sum held at >= q, HS(q) = heads at >= q
       int hv[IPT_], rsv[IPT_], hsv[IPT_], ls = 0, lh = 0;
@@ -492,7 +513,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       for (int j = 0; j < IPT_; j++) os += hv[j], oh += hh[j], rsv[j] = os, hsv[j] = oh;
       // (ii) a_kv = #{heads i : F + RS(p_i + 1) >= i}, i = k - HS(p_i) + 1 (monotone in i)
       int cnt = 0;
-      if (finiteM) {
+      if (fM) {
 #pragma unroll
         for (int j = 0; j < IPT_; j++)
           if (hh[j]) cnt += F + (rsv[j] - hv[j]) >= k - hsv[j] + 1;
@@ -503,10 +524,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       int akv = 0;
 #pragma unroll
       for (int w = 0; w < NW; w++) akv += S.cf_red[w][2];
-      if (!finiteM) akv = k;
+      if (!fM) akv = k;
       const int a = min(min(akv, T), k);
       // (iii) q* = max{q : F + RS(q) >= a}; the position of head a+1
-      const bool needq = finiteM && F < a;
+      const bool needq = fM && F < a;
       int cq = 0;
 #pragma unroll
       for (int j = 0; j < IPT_; j++) {
@@ -528,7 +549,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       }
       // head a+1, when the KV (not the token budget) stopped the walk: a victim if it lies in the evicted
       // suffix, else it runs out of pool, evicts everything behind it and self-preempts (Q8)
-      if (finiteM && a == akv && a < min(k, T)) {
+      if (fM && a == akv && a < min(k, T)) {
         const int pa = S.pa;
         if (pa < qs) selfp = pa, qs = pa + 1;
       }
@@ -569,7 +590,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
 #pragma unroll
       for (int w = 0; w < NW; w++) tev += S.cf_red[w][4], teh += S.cf_red[w][5], ter += S.cf_red[w][6];
       tok += a;
-      U += a - teh;
+      U += (kv1 ? a : 0) - teh;
       nB += a;
       n_running -= tev;
       Rs -= ter;
@@ -586,7 +607,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
 
     // Candidates that never preempt, on warp 0: the waiting group (overWin: window offsets [0, L) = R_w
     // in index order; Q5) or running prefills (P positions [b0, b1) = R_r^p; their KV delta is 0 since
-    // reserved = s >= m + c).  All are in the prefill phase, so a chunk of 32 is resolved in registers:
+    // reserved >= s >= m + c).  All are in the prefill phase, so a chunk of 32 is resolved in registers:
     // repeat {ballot the lanes that fit alone; prefix-scan them; admit those before the first cumulative
     // failure; drop that failure} -- rejections change no state.  A cropped chunk (chunked prefill)
     // exhausts the token budget and ends the group.
@@ -616,7 +637,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         const int4 rc = s_rec[sl < 0 ? 0 : sl];
         const uint8_t fl = s_fl[sl < 0 ? 0 : sl];
         const int s = rc.x + rc.y, avail = s - rc.z;
-        const int dkv = overWin ? s : 0;  // KV delta (Q13)
+        const int dkv = overWin ? rnew(rc, sl < 0 ? 0 : sl) : 0;  // KV delta: the initial reserve >= s >= c (Q13)
         const int rem = (hist && overWin) ? max(S.pred[bucket_of(rc.x)] - rc.y, 0) : 0;
         bool alive = sl >= 0;
         for (;;) {
@@ -626,8 +647,9 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           if (hist && overWin) fit = fit && !(anyRun0 && (long long)U + Rs + s + rem > M);
           const unsigned fm = __ballot_sync(FM, fit);
           if (!fm) break;
-          const int cc = fit ? avail : 0, rr = fit ? rem : 0;
-          int xc = cc, xr = rr;
+          const int cc = fit ? avail : 0, rr = fit ? rem : 0, dk = fit ? dkv : 0;
+          const bool scand = overWin && !kv1;  // KV deltas differ from c only under a PEAK / CONTEXT reserve
+          int xc = cc, xr = rr, xd = dk;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const int yc = __shfl_up_sync(FM, xc, o);
@@ -636,9 +658,14 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
               const int yr = __shfl_up_sync(FM, xr, o);
               if (lane >= o) xr += yr;
             }
+            if (scand) {
+              const int yd = __shfl_up_sync(FM, xd, o);
+              if (lane >= o) xd += yd;
+            }
           }
           const int ec = xc - cc, er = xr - rr, ek = __popc(fm & lt);
-          const int ed = overWin ? ec : 0;  // full admissions before this lane reserve exactly their c
+          // full admissions before this lane reserve exactly their c under SEQ (waiting: m = 0, c = s)
+          const int ed = overWin ? (scand ? xd - dk : ec) : 0;
           bool brk = false, crop = false;
           if (fit) {
             const int prt = rt - ec;
@@ -659,7 +686,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             s_bl[nB + ek] = (int16_t)sl;
             if (overWin) {
               s_seq[sl] = seq + ek + 1;
-              s_rec[sl] = make_int4(rc.x, rc.y, 0, s);
+              s_rec[sl] = make_int4(rc.x, rc.y, 0, dkv);
               s_fl[sl] = ST_RUN | F_INB | (fl & F_FIRST);
               s_new[n_new + ek] = (int16_t)sl;
             } else {
@@ -672,16 +699,17 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           const int lastl = stop > 0 ? min(stop, 32) - 1 : 0;
           const int addc = stop > 0 ? __shfl_sync(FM, xc, lastl) : 0;
           const int addr = (hist && overWin && stop > 0) ? __shfl_sync(FM, xr, lastl) : 0;
+          const int addd = (scand && stop > 0) ? __shfl_sync(FM, xd, lastl) : addc;
           int cropc = 0, crops = 0, cropr = 0;
           if (cropped) {
             cropc = __shfl_sync(FM, rt - ec, cl);
-            crops = __shfl_sync(FM, s, cl);
+            crops = __shfl_sync(FM, dkv, cl);
             if (hist && overWin) cropr = __shfl_sync(FM, rem, cl);
           }
           const int nall = nadm + (cropped ? 1 : 0);
           tok += addc + cropc;
           if (overWin) {
-            U += addc + crops;
+            U += addd + crops;
             seq += nall, n_new += nall, n_running += nall;
             Rs += addr + cropr;
           }
@@ -824,9 +852,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           rem = max(S.pred[bucket_of(rc.x)] - rc.y, 0);
           ok = ok && !(anyRun0 && (long long)U + Rs + s + rem > M);
         }
-        const int delta = max(isW ? s : rc.w, rc.z + c) - (isW ? 0 : max(rc.w, rc.z));
+        const int rw = isW ? rnew(rc, slv[j] < 0 ? 0 : slv[j]) : rc.w;
+        const int delta = max(rw, rc.z + c) - (isW ? 0 : max(rc.w, rc.z));
         const bool kvfail = finiteM && U + delta > M;
-        kind[j] = !ok ? K_NONE : (kvfail ? (isW ? K_NONE : K_EVENT) : K_MARK);
+        kind[j] = !ok ? K_NONE : (kvfail ? ((isW || pf) ? K_NONE : K_EVENT) : K_MARK);
         const bool mk = kind[j] == K_MARK;
         cc[j] = mk ? (ph == PH_DEC ? 1 : avail) : 0;
         dd[j] = mk ? delta : 0;
@@ -907,7 +936,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
               if (ww[j]) {
                 s_seq[sl] = seq + pw + 1;
                 const int4 rc = rcv[j];
-                s_rec[sl] = make_int4(rc.x, rc.y, rc.z, ss[j]);
+                s_rec[sl] = make_int4(rc.x, rc.y, rc.z, kv1 ? ss[j] : rnew(rc, sl));
                 s_fl[sl] = ST_RUN | F_INB | (flv[j] & F_FIRST);
                 s_new[n_new + pw] = (int16_t)sl;
               } else {
@@ -1012,7 +1041,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             ndone++;
             if (hist) atomicAdd(&S.hist[bucket_of(rc.x) * 18 + bucket_of(O)], 1);
           }
-          if (evc) s_ev[atomicAdd(&S.n_ev, 1)] = (int16_t)(sl | (evc << 12));
+          if (evc) s_ev[atomicAdd(&S.n_ev, 1)] = sl | (evc << SLB);
         }
         if (!done) {
           minrem = min(minrem, O - g);
@@ -1098,7 +1127,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           long long Lr = 0;
           if (ndn == 0 && f.np == 0 && !S.any_pre && f.nd > 0) {
             Lr = tt[10];
-            if (finiteM) Lr = min(Lr, (long long)(M - Uafter) / f.nd);
+            if (finiteM && kv1) Lr = min(Lr, (long long)(M - Uafter) / f.nd);
             Lr = min(Lr, cfg.max_steps - S.steps);
           }
           S.runL = Lr;
@@ -1132,18 +1161,18 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     {
       const int nev = S.n_ev;
       for (int e = tid; e < nev; e += NT) {
-        const int code = s_ev[e], sl = code & 0xFFF;
+        const int code = s_ev[e], sl = code & (CAP - 1);
         const int idx = lo + ((sl - lo) & (CAP - 1));
-        if (code & (1 << 12))
+        if (code & (1 << SLB))
           for (int k = 0; k < K; k++) tf[(long long)k * n + idx] = S.clock[k];
-        if (code & (2 << 12))
+        if (code & (2 << SLB))
           for (int k = 0; k < K; k++) td[(long long)k * n + idx] = S.clock[k];
       }
       const long long Lr = S.runL;
       if (Lr > 0) {
         constexpr int DB = CAP / 2;
         const int cmax = min(NT, DB / K);
-        const long long ndd = S.last_nd, MD = S.runMD, U0 = S.U;
+        const long long ndd = S.last_nd, MD = S.runMD, U0 = S.U, du = kv1 ? ndd : 0;  // KV growth per run step
         long long E = 0;
         while (E < Lr) {
           const int chunk = (int)min((long long)cmax, Lr - E);
@@ -1207,16 +1236,16 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           if (ci == 0)
             for (long long k = 1; k <= E && S.steps + k - 1 < DBG_STEPS; k++) {
               int* d = g_dbg[S.steps + k - 1];
-              d[0] = (int)(S.steps + k - 1), d[1] = (int)ndd, d[2] = (int)(U0 + k * ndd), d[3] = (int)ndd;
+              d[0] = (int)(S.steps + k - 1), d[1] = (int)ndd, d[2] = (int)(U0 + k * du), d[3] = (int)ndd;
               d[4] = (int)S.preempt, d[5] = 0;
             }
 #endif
           S.steps += E;
-          S.sumU += E * U0 + ndd * (E * (E + 1) / 2);
+          S.sumU += E * U0 + du * (E * (E + 1) / 2);
           S.entries += E * ndd;
           S.processed += E * ndd;
           S.visits += E * nP;
-          S.U = U0 + E * ndd - fr2;
+          S.U = U0 + E * du - fr2;
           S.n_done += (int)nd2t;
           if (nd2t > 0) S.r_dirty = 1, S.removals = 2, S.rank_dirty = 1, S.p_dirty = 1;
           if (srf && E > 0 && ndd != nrun) S.o_dirty = 1;
@@ -1262,7 +1291,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       if (od) {  // SRF retention order: m descending, then admission order (Q3, Q7)
         auto key = [&](int sl) -> unsigned long long {
           return ((unsigned long long)(0x3FFFF - s_rec[sl].z) << 46) |
-                 ((unsigned long long)(unsigned)s_seq[sl] << 12) | (unsigned long long)sl;
+                 ((unsigned long long)(unsigned)s_seq[sl] << SLB) | (unsigned long long)sl;
         };
         int okk = 1;
         for (int q = tid; q + 1 < cnt; q += NT)
@@ -1272,7 +1301,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           PROF_CNT(8, 1);
           for (int q = tid; q < cnt; q += NT) s_keys[q] = key(rl[q]);
           block_bitonic<NT>(s_keys, cnt);
-          for (int q = tid; q < cnt; q += NT) rl[q] = (int16_t)(s_keys[q] & 0xFFF);
+          for (int q = tid; q < cnt; q += NT) rl[q] = (int16_t)(s_keys[q] & (CAP - 1));
           moved = true;
           if (tid == 0) S.p_dirty = 1;
           __syncthreads();

@@ -35,7 +35,10 @@ __device__ int g_dbg[DBG_STEPS][6];  // config 0 only: per full step (steps, tok
 #define PROF_CNT(i, v)
 #endif
 
-__host__ __device__ inline int variant_of(int n) { return n <= 1024 ? 0 : 1; }
+// 0: W <= 1024 and 1: W <= 4096, state in shared memory (the window never exceeds n <= CAP);
+// 2: larger workloads, a 32768-slot ring in a per-CTA global-memory arena (SIM_MAX_WINDOW)
+__host__ __device__ inline int variant_of(int n) { return n <= 1024 ? 0 : (n <= 4096 ? 1 : 2); }
+constexpr int N_VARIANTS = 3;
 
 #ifndef SIM_NT_SMALL
 #define SIM_NT_SMALL 256  // threads per CTA of the W <= 1024 variant
@@ -62,16 +65,25 @@ namespace simsweep {
 // ------------------------------------------------------------------ host side
 struct Variant {
   int nt, cap;
-  size_t smem;
+  size_t smem;   // dynamic shared memory per CTA
+  size_t arena;  // global workspace per CTA (GM variant), else 0
   void (*fn)(KParams);
 };
 
-template <int NT, int CAP, int IPT_>
+template <int NT, int CAP, int IPT_, bool GM>
 Variant make_variant() {
-  return Variant{NT, CAP, Smem<NT, CAP>::bytes, sim_kernel<NT, CAP, IPT_>};
+  using L = Smem<NT, CAP>;
+  return Variant{NT, CAP, GM ? L::scal : L::bytes, GM ? L::arr_bytes : 0, sim_kernel<NT, CAP, IPT_, GM>};
 }
 
-static Variant g_variants[2] = {make_variant<SIM_NT_SMALL, 1024, 1024 / SIM_NT_SMALL>(), make_variant<512, 4096, 4>()};
+static Variant g_variants[N_VARIANTS] = {make_variant<SIM_NT_SMALL, 1024, 1024 / SIM_NT_SMALL, false>(),
+                                         make_variant<512, 4096, 4, false>(), make_variant<512, SIM_MAX_WINDOW, 4, true>()};
+
+static int64_t workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int32_t* wls_n) {
+  int64_t big = 0;
+  for (int i = 0; i < n_cfgs; i++) big += variant_of(wls_n[cfgs[i].workload]) == 2;
+  return big ? (int64_t)WS_HEADER + big * (int64_t)g_variants[2].arena : 0;
+}
 
 static int check_cuda(cudaError_t e) { return e == cudaSuccess ? 0 : SIM_ECUDA; }
 static unsigned g_attr_set[64];  // kernel attributes already set, per device and variant
@@ -120,16 +132,25 @@ int sim_request_rows(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workloa
   return 0;
 }
 
+int64_t sim_workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int32_t* wls_n) {
+  if (!cfgs || !wls_n || n_cfgs <= 0) return SIM_EINVAL;
+  return workspace_bytes(cfgs, n_cfgs, wls_n);
+}
+
 int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, const sim_config_t* d_cfgs,
                      const sim_workload_t* d_wls, const sim_cost_model_t* d_cms, int32_t n_cms,
                      const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
-                     sim_result_t* d_results, sim_request_out_t d_req, void* stream) {
+                     sim_result_t* d_results, sim_request_out_t d_req, void* d_workspace, int64_t workspace_bytes_,
+                     void* stream) {
   if (!h_cfgs || !h_wls_n || !d_cfgs || !d_wls || !d_cms || n_cfgs <= 0 || n_cms <= 0 || !d_row_off ||
       !d_tim_off || !d_results || !d_req.t_first || !d_req.t_done || !d_req.n_preempt || !d_req.refill_tokens)
     return SIM_EINVAL;
-  bool need[2] = {false, false};
+  bool need[N_VARIANTS] = {false, false, false};
   for (int i = 0; i < n_cfgs; i++) need[variant_of(h_wls_n[h_cfgs[i].workload])] = true;
+  const int64_t wsb = workspace_bytes(h_cfgs, n_cfgs, h_wls_n);
+  if (wsb > 0 && (!d_workspace || workspace_bytes_ < wsb)) return SIM_EINVAL;
   KParams kp;
+  kp.ws = reinterpret_cast<unsigned char*>(d_workspace);
   kp.cfgs = d_cfgs;
   kp.wls = d_wls;
   kp.cms = d_cms;
@@ -140,8 +161,8 @@ int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* 
   kp.req = d_req;
   kp.n_cfgs = n_cfgs;
   int launches = 0;
-  // the large-window variant first: its simulations are the longest
-  for (int v = 1; v >= 0; v--) {
+  // the large-window variants first: their simulations are the longest
+  for (int v = N_VARIANTS - 1; v >= 0; v--) {
     if (!need[v]) continue;
     const Variant& V = g_variants[v];
     int dev = 0;
@@ -150,10 +171,12 @@ int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* 
       if (cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V.smem) !=
           cudaSuccess)
         return SIM_ECUDA;
-      // state is shared-memory resident: take the largest carveout so that more CTAs fit per SM
-      cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      // shared-memory resident state: the largest carveout, so that more CTAs fit per SM; the global-arena
+      // variant keeps the carveout small and leaves the rest of the 256 KB to L1
+      cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout, V.arena ? 10 : 100);
       g_attr_set[dev] |= 1u << v;
     }
+    if (V.arena && cudaMemsetAsync(d_workspace, 0, 4, (cudaStream_t)stream) != cudaSuccess) return SIM_ECUDA;
     kp.variant = v;
     void* args[] = {&kp};
     if (cudaLaunchKernel((const void*)V.fn, dim3(n_cfgs), dim3(V.nt), args, V.smem, (cudaStream_t)stream) !=
@@ -171,7 +194,9 @@ static int validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload
   for (int i = 0; i < n_cfgs; i++) {
     const sim_config_t& c = cfgs[i];
     if (c.order < SIM_ORDER_PREFILL_FIRST || c.order > SIM_ORDER_RANK_O) return SIM_EINVAL;
-    if (c.replacement < SIM_NRF || c.replacement > SIM_SRF_HIST) return SIM_EINVAL;
+    if (c.replacement < SIM_NRF || c.replacement > SIM_PF) return SIM_EINVAL;
+    if (c.reserve < SIM_RESERVE_SEQ || c.reserve > SIM_RESERVE_CONTEXT) return SIM_EINVAL;
+    if ((c.replacement == SIM_PF) != (c.reserve != SIM_RESERVE_SEQ)) return SIM_EINVAL;  // Q39
     if ((c.hybrid != 0 && c.hybrid != 1) || (c.chunked != 0 && c.chunked != 1)) return SIM_EINVAL;
     if (c.C < 1 || c.C > (1 << 30) || c.M > (1 << 30) || c.S < 1 || c.S > 262143 || c.max_steps < 1) return SIM_EINVAL;
     if (c.n_cost < 1 || c.n_cost > SIM_MAX_COST) return SIM_EINVAL;
@@ -202,22 +227,29 @@ static int validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload
 
 // longest-processing-time-first estimate of one simulation's step count from per-workload statistics
 struct WlStats {
-  double sumIO, sumI, maxO;
+  double sumIO, sumPO, sumO, sumI, maxO;
 };
 
 static WlStats workload_stats(const sim_workload_t& w) {
-  WlStats st{0, 0, 0};
+  WlStats st{0, 0, 0, 0, 0};
   for (int i = 0; i < w.n; i++) {
     st.sumIO += ((double)w.I[i] + 0.5 * w.O[i]) * w.O[i];
+    st.sumPO += ((double)w.I[i] + w.O[i] - 1) * w.O[i];
+    st.sumO += w.O[i];
     st.sumI += w.I[i];
     st.maxO = std::max(st.maxO, (double)w.O[i]);
   }
   return st;
 }
 
+// KV-time area / M: the average usage is ~(I + O/2) per running request under SEQ, the whole reserve
+// (I + O - 1 or S) under the preemption-free reserves
 static double estimate_steps(const sim_config_t& c, const WlStats& st) {
   const double Meff = c.M >= 0 ? (double)std::max<int64_t>(c.M, 1) : 1e18;
-  return st.maxO + st.sumIO / Meff + st.sumI / (double)c.C;
+  const double area = c.reserve == SIM_RESERVE_PEAK      ? st.sumPO
+                      : c.reserve == SIM_RESERVE_CONTEXT ? (double)c.S * st.sumO
+                                                         : st.sumIO;
+  return st.maxO + area / Meff + st.sumI / (double)c.C;
 }
 
 // Per-device cache of the host entry point: one device arena, one pinned staging buffer and one stream,
@@ -323,6 +355,9 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
   off = al(off + 8 * (size_t)rows);
   const size_t o_rf = off;
   off = al(off + 8 * (size_t)rows);
+  const int64_t wsb = workspace_bytes(cfgs, n_cfgs, wn.data());
+  const size_t o_ws = off;
+  off = al(off + (size_t)wsb);
   if ((rc = cache_reserve(cache, off, in_bytes))) return rc;
   char* base = cache.dbuf;
   char* h = cache.hbuf;
@@ -358,7 +393,8 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
                              reinterpret_cast<const sim_cost_model_t*>(base + o_cm), n_cms,
                              reinterpret_cast<const int32_t*>(base + o_ord),
                              reinterpret_cast<const int64_t*>(base + o_ro), reinterpret_cast<const int64_t*>(base + o_to),
-                             reinterpret_cast<sim_result_t*>(base + o_res), dreq, s);
+                             reinterpret_cast<sim_result_t*>(base + o_res), dreq, wsb ? base + o_ws : nullptr, wsb,
+                             s);
     if (l < 0) rc = l;
   }
   if (!rc) {

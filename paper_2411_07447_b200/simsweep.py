@@ -29,7 +29,7 @@ class SimConfig(ctypes.Structure):
     _fields_ = [("order", ctypes.c_int32), ("hybrid", ctypes.c_int32), ("chunked", ctypes.c_int32),
                 ("replacement", ctypes.c_int32), ("S", ctypes.c_int32), ("workload", ctypes.c_int32),
                 ("C", ctypes.c_int64), ("M", ctypes.c_int64), ("max_steps", ctypes.c_int64),
-                ("n_cost", ctypes.c_int32), ("cost", ctypes.c_int32 * SIM_MAX_COST), ("reserved0", ctypes.c_int32)]
+                ("n_cost", ctypes.c_int32), ("cost", ctypes.c_int32 * SIM_MAX_COST), ("reserve", ctypes.c_int32)]
 
 
 class SimWorkload(ctypes.Structure):
@@ -84,7 +84,9 @@ def lib() -> ctypes.CDLL:
         L.sim_sweep_device.argtypes = [P(SimConfig), ctypes.c_int32, P(ctypes.c_int32), ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, SimRequestOut,
-                                       ctypes.c_void_p]
+                                       ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.sim_workspace_bytes.restype = ctypes.c_int64
+        L.sim_workspace_bytes.argtypes = [P(SimConfig), ctypes.c_int32, P(ctypes.c_int32)]
         L.sim_request_rows.restype = ctypes.c_int
         L.sim_request_rows.argtypes = [P(SimConfig), ctypes.c_int32, P(SimWorkload), ctypes.c_int32,
                                        P(ctypes.c_int64), P(ctypes.c_int64)]
@@ -96,7 +98,8 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-EXPORTED_SYMBOLS = ["sim_sweep", "sim_sweep_device", "sim_request_rows", "sim_strerror", "sim_version"]
+EXPORTED_SYMBOLS = ["sim_sweep", "sim_sweep_device", "sim_workspace_bytes", "sim_request_rows", "sim_strerror",
+                    "sim_version"]
 
 
 def strerror(code: int) -> str:
@@ -143,9 +146,10 @@ def unit_cost(d: float = 1.0) -> SimCostModel:
 
 # ------------------------------------------------------------ configs
 def make_config(order, hybrid, chunked, replacement, C, M, S=4096, workload=0, cost=(0,),
-                max_steps=10_000_000) -> SimConfig:
+                max_steps=10_000_000, reserve=0) -> SimConfig:
     c = SimConfig()
     c.order, c.hybrid, c.chunked, c.replacement = int(order), int(bool(hybrid)), int(bool(chunked)), int(replacement)
+    c.reserve = int(reserve)
     c.S, c.workload, c.C, c.M, c.max_steps = int(S), int(workload), int(C), int(M), int(max_steps)
     cost = list(cost)
     assert 1 <= len(cost) <= SIM_MAX_COST
@@ -158,7 +162,7 @@ def make_config(order, hybrid, chunked, replacement, C, M, S=4096, workload=0, c
 def preset_config(name: str, M: int, S: int = 4096, workload: int = 0, cost=(0,), **kw) -> SimConfig:
     p = _presets.preset(name, S=S)
     return make_config(p["order"], p["hybrid"], p["chunked"], p["replacement"], C=kw.pop("C", p["C"]), M=M, S=S,
-                       workload=workload, cost=cost, **kw)
+                       workload=workload, cost=cost, reserve=p["reserve"], **kw)
 
 
 @dataclass
@@ -282,6 +286,9 @@ class DeviceSweep:
         self.t_done = torch.zeros(trows, dtype=torch.float64, device=self.dev)
         self.n_preempt = torch.zeros(rows, dtype=torch.int64, device=self.dev)
         self.refill = torch.zeros(rows, dtype=torch.int64, device=self.dev)
+        # state of simulations with n > 4096 requests (a per-CTA arena each); none for the grid sweep
+        self.ws_bytes = int(_check(lib().sim_workspace_bytes(self.h_cfgs, len(self.cfgs), self.h_wls_n)))
+        self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=self.dev)
 
     def launch(self, stream=None) -> int:
         """Enqueue the sweep on `stream` (torch.cuda.Stream or None = current); returns #kernel launches."""
@@ -291,7 +298,8 @@ class DeviceSweep:
         rc = lib().sim_sweep_device(self.h_cfgs, len(self.cfgs), self.h_wls_n, self.d_cfgs.data_ptr(),
                                     self.d_wls.data_ptr(), self.d_cms.data_ptr(), self.n_cms,
                                     self.d_order.data_ptr(), self.d_row_off.data_ptr(), self.d_tim_off.data_ptr(),
-                                    self.d_results.data_ptr(), req, ctypes.c_void_p(s.cuda_stream))
+                                    self.d_results.data_ptr(), req, ctypes.c_void_p(self.ws.data_ptr()),
+                                    self.ws_bytes, ctypes.c_void_p(s.cuda_stream))
         return _check(rc)
 
     def fetch(self) -> SweepResult:

@@ -35,15 +35,42 @@ def grid_sweep(M: int = 100_000, W: int = 1024, policies=("", "-srf"), preset_na
     return cfgs, wls, cms, labels
 
 
+def varying_m_sweep(Ms=(100, 1_000, 10_000, 100_000, 1_000_000), O: int = 32, W: int = 1024,
+                    preset_names=("vllm", "sarathi", "sarathi-cs"), policies=("", "-pf"), S: int = 4096,
+                    cost_names=(GRID_COST,), values=None):
+    """E5 (Fig. varying_M): O = 32, W = 1024, I over the grid values, M from 100 to 1M, each
+    scheduler and its preemption-free version.  Configs whose requests exceed M report never_fits.
+    Returns (cfgs, wls, cost_model_list, labels (name, I, M))."""
+    values = values or workloads.grid_values()
+    pcms = simsweep.load_cost_models()
+    cms = [pcms[c] for c in cost_names]
+    wls = [workloads.fixed(I, O, W) for I in values]
+    cfgs, labels = [], []
+    for name in preset_names:
+        for pol in policies:
+            for M in Ms:
+                for wi, I in enumerate(values):
+                    cfgs.append(simsweep.preset_config(name + pol, M, S=S, workload=wi, cost=tuple(range(len(cms)))))
+                    labels.append((name + pol, I, M))
+    return cfgs, wls, cms, labels
+
+
 def estimate(cfgs, wls) -> np.ndarray:
-    """Step-count estimate per simulation (LPT key): max O + sum (I + O/2) O / M + sum I / C."""
+    """Step-count estimate per simulation (LPT key): max O + KV-time area / M + sum I / C (area = sum (I + O/2) O,
+    or the reserve times O under the preemption-free reserves)."""
     est = np.empty(len(cfgs))
     for i, c in enumerate(cfgs):
         w = wls[c.workload]
         I = np.asarray(w.I, np.float64)
         O = np.asarray(w.O, np.float64)
         Meff = float(max(c.M, 1)) if c.M >= 0 else 1e18
-        est[i] = O.max() + float(((I + 0.5 * O) * O).sum()) / Meff + float(I.sum()) / float(c.C)
+        if c.reserve == 1:  # PEAK: the whole reserve I + O - 1 is held while running
+            area = float(((I + O - 1) * O).sum())
+        elif c.reserve == 2:  # CONTEXT: S per running request
+            area = float(c.S) * float(O.sum())
+        else:
+            area = float(((I + 0.5 * O) * O).sum())
+        est[i] = O.max() + area / Meff + float(I.sum()) / float(c.C)
     return est
 
 

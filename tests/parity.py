@@ -30,12 +30,18 @@ def cost_models():
 
 def oracle_config(c: simsweep.SimConfig) -> o.OracleConfig:
     return o.make_config(c.order, c.hybrid, c.chunked, c.replacement, C=c.C, M=c.M, S=c.S, max_steps=c.max_steps,
-                         n_cost=c.n_cost)
+                         n_cost=c.n_cost, reserve=c.reserve)
 
 
-def run_case_list(cases, device=-1):
+def _oracle_job(args):
+    c, wl, ocost = args
+    return o.run(c, wl.I, wl.O, wl.T, ocost)
+
+
+def run_case_list(cases, device=-1, processes=0):
     """cases: list of (SimConfig, Workload, [cost names or ('unit', d)]).  Runs all cases in ONE sim_sweep
-    call (one kernel launch per variant) and the oracle per case.  Returns (gpu SweepResult, [oracle results])."""
+    call (one kernel launch per variant) and the oracle per case (in `processes` forked workers if > 0).
+    Returns (gpu SweepResult, [oracle results])."""
     ocms, pcms = cost_models()
     wls, cms_p, cfgs, ors = [], [], [], []
     cm_index = {}
@@ -59,7 +65,13 @@ def run_case_list(cases, device=-1):
             c.cost[k] = v
         cfgs.append(c)
         ocost = [o.unit_cost(nm[1]) if isinstance(nm, tuple) else ocms[nm] for nm in names]
-        ors.append(o.run(oracle_config(c), wl.I, wl.O, wl.T, ocost))
+        ors.append((oracle_config(c), wl, ocost))
+    if processes > 0:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(processes) as pool:
+            ors = pool.map(_oracle_job, ors, chunksize=1)
+    else:
+        ors = [_oracle_job(a) for a in ors]
     g = simsweep.sim_sweep(cfgs, wls, cms_p, device=device)
     return g, ors
 

@@ -23,7 +23,7 @@ def L():
 
 def declared_functions():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(sim_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(sim_\w+)\s*\(", txt, re.M)))
 
 
 def test_exports_every_declared_symbol(L):
@@ -42,6 +42,7 @@ def test_struct_layout_matches_header(tmp_path):
                    'int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(sim_config_t), '
                    'sizeof(sim_workload_t), sizeof(sim_cost_model_t), sizeof(sim_result_t), '
                    'sizeof(sim_request_out_t), offsetof(sim_config_t, n_cost), offsetof(sim_result_t, makespan));'
+                   'printf("%zu\\n", offsetof(sim_config_t, reserve));'
                    'return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
@@ -49,7 +50,7 @@ def test_struct_layout_matches_header(tmp_path):
     want = [ctypes.sizeof(simsweep.SimConfig), ctypes.sizeof(simsweep.SimWorkload),
             ctypes.sizeof(simsweep.SimCostModel), ctypes.sizeof(simsweep.SimResult),
             ctypes.sizeof(simsweep.SimRequestOut), simsweep.SimConfig.n_cost.offset,
-            simsweep.SimResult.makespan.offset]
+            simsweep.SimResult.makespan.offset, simsweep.SimConfig.reserve.offset]
     assert got == want
     assert got[0] == 72
 
@@ -97,3 +98,20 @@ def test_invalid_calls_rejected_before_device(L):
         simsweep.sim_sweep([simsweep.preset_config("vllm", 100)], [wl2], [simsweep.unit_cost()])
     with pytest.raises(simsweep.SimError, match="cost"):
         simsweep.sim_sweep([simsweep.preset_config("vllm", 100, cost=(3,))], [wl], [simsweep.unit_cost()])
+
+
+def test_workspace_bytes_host_query(L):
+    """sim_workspace_bytes is host-only: 0 for workloads of <= 4096 requests, a header plus one arena per
+    simulation of a larger workload; sim_sweep_device rejects a missing workspace before touching the GPU."""
+    from paper_2411_07447_b200 import workloads
+    small = [simsweep.preset_config("vllm", 100_000, workload=0)]
+    n = (ctypes.c_int32 * 2)(1024, 19_700)
+    assert L.sim_workspace_bytes(simsweep._cfg_array(small), 1, n) == 0
+    big = [simsweep.preset_config(nm, 100_000, workload=1) for nm in ("vllm", "sarathi", "vllm-pf")]
+    b1 = L.sim_workspace_bytes(simsweep._cfg_array(big[:1]), 1, n)
+    b3 = L.sim_workspace_bytes(simsweep._cfg_array(big), 3, n)
+    assert b1 > 32768 * 51 and b3 - 256 == 3 * (b1 - 256)
+    assert L.sim_workspace_bytes(None, 1, n) == -1
+    req = simsweep.SimRequestOut(1, 1, 1, 1)
+    rc = L.sim_sweep_device(simsweep._cfg_array(big), 3, n, 1, 1, 1, 1, None, 1, 1, 1, req, None, 0, None)
+    assert rc == -1

@@ -17,8 +17,8 @@ def cfg(order, hybrid, chunked, repl, C, M, S=4096, **kw):
     return simsweep.make_config(order, hybrid, chunked, repl, C=C, M=M, S=S, **kw)
 
 
-def assert_parity(cases):
-    g, ors = run_case_list(cases)
+def assert_parity(cases, processes=0):
+    g, ors = run_case_list(cases, processes=processes)
     bad = []
     for i in range(len(cases)):
         bad += compare(g, ors, i, label=f"case{i}:{cases[i][1].name}")
@@ -126,6 +126,15 @@ def test_online_longform_and_hist():
     assert_parity(cases)
 
 
+def test_online_azureconv():
+    """BASELINE configs[3] at full size: the AzureConv-like trace (19.7K requests) through
+    the 4096-slot ring-buffer variant; every per-request output compared with the oracle."""
+    wl = workloads.azureconv(0)
+    cases = [(simsweep.preset_config(nm, 100_000, S=131072), wl, A100)
+             for nm in ("vllm", "vllm-srf", "sarathi", "sarathi-srf-hist")]
+    assert_parity(cases, processes=len(cases))
+
+
 def test_online_70b_what_ifs():
     wl = workloads.longform(3)
     cases = []
@@ -153,8 +162,8 @@ def _oracle_grid_job(args):
     from paper_2411_07447_b200 import workloads as wk
     p = pr.preset(name)
     wl = wk.fixed(I, O, 1024)
-    r = o2.run(o2.make_config(p["order"], p["hybrid"], p["chunked"], p["replacement"], C=p["C"], M=M), wl.I, wl.O,
-               wl.T, o2.load_cost_models()["llama3-8b_a100_linear"])
+    r = o2.run(o2.make_config(p["order"], p["hybrid"], p["chunked"], p["replacement"], C=p["C"], M=M,
+                              reserve=p["reserve"]), wl.I, wl.O, wl.T, o2.load_cost_models()["llama3-8b_a100_linear"])
     return (r.status, [getattr(r, f) for f in ("steps", "preemptions", "batch_entries", "processed_tokens", "sum_U",
                                                "prefill_entries", "idle_jumps", "visits")],
             r.t_first[0].copy(), r.t_done[0].copy(), r.n_preempt.copy(), r.refill.copy(), r.makespan[0])
@@ -220,3 +229,82 @@ def test_random_medium_contention(block):
         M = int(rng.integers(peak, 6 * peak + 1))
         cases.append((cfg(o_, hybrid, chunked, r, C, M, S=512), wl, A100))
     assert_parity(cases)
+
+
+def test_pf_orca_hand_traces():
+    """Example A under vLLM^pf (8 sequential steps) and the Orca S-reserve trace (tests/test_oracle_pf.py)."""
+    cases = [
+        (cfg(0, 0, 0, P.REPL_PF, 4096, 6, reserve=P.RESERVE_PEAK), W([2, 2], [4, 4]), UNIT),
+        (cfg(1, 1, 0, P.REPL_PF, 10, 20, S=10, reserve=P.RESERVE_CONTEXT), W([2, 2, 2], [3, 3, 3]), UNIT),
+        (simsweep.preset_config("orca", 1000, S=128), workloads.fixed(8, 16, 64), UNIT),
+        (simsweep.preset_config("orca", 100, S=128), workloads.fixed(2, 2, 4), UNIT),  # S > M: never fits
+    ]
+    g, _ = assert_parity(cases)
+    assert g.status(3) == "never_fits"
+    assert int(g.results["steps"][0]) == 8 and int(g.results["steps"][1]) == 6
+    assert int(g.results["preemptions"][:3].sum()) == 0
+
+
+@pytest.mark.parametrize("name", ["vllm-pf", "sarathi-pf", "sarathi-cs-pf", "sarathi-nocp-pf", "vllm-hy-pf",
+                                  "sarathi-nohy-pf", "orca"])
+def test_pf_grid_sample(name):
+    """E4 (Fig. exp_bin_packing): preemption-free presets on O = W = 1024 plus a spread of
+    (I, O), M = 100K -- the PEAK / CONTEXT reserve through the closed-form decode group and the lean loops."""
+    cases = [(simsweep.preset_config(name, 100_000), workloads.fixed(I, O, 1024), A100)
+             for (I, O) in [(1, 1024), (1024, 1024), (64, 1024), (16, 16), (512, 2), (2, 512), (1, 1), (256, 64)]]
+    assert_parity(cases)
+
+
+def test_varying_M_sweep():
+    """E5 (Fig. varying_M): O = 32, W = 1024, M from 100 to 1M, vLLM / Sarathi and their PF
+    versions -- the small-M regime where preemption helps and the large-M regime where nothing binds."""
+    cases = []
+    for nm in ("vllm", "vllm-pf", "sarathi", "sarathi-pf"):
+        for M in (100, 1000, 10_000, 1_000_000):
+            for I in (8, 64):
+                cases.append((simsweep.preset_config(nm, M), workloads.fixed(I, 32, 1024), A100))
+    assert_parity(cases)
+
+
+@pytest.mark.parametrize("block", range(2))
+def test_random_pf_contention(block):
+    """Random workloads under the PEAK / CONTEXT reserves across all orders, chunking and hybrid settings,
+    online and offline, with M tight enough that reserves bind."""
+    cases = []
+    for seed in range(9000 + block * 60, 9000 + block * 60 + 60):
+        rng = np.random.default_rng(seed)
+        Wn = int(rng.integers(1, 400))
+        S = 512
+        wl = workloads.random_small(seed, Wn, max_len=int(rng.integers(4, 200)), online=bool(rng.integers(0, 2)), S=S)
+        o_ = int(rng.integers(0, 5))
+        res = int(rng.integers(1, 3))
+        chunked = int(rng.integers(0, 2))
+        hybrid = int(rng.integers(0, 2)) if o_ < 2 else 1
+        peak = int((wl.I.astype(int) + wl.O - 1).max())
+        C = int(rng.integers(max(1, peak // 4), 2 * peak + 1)) if chunked else int(rng.integers(peak, 3 * peak + 1))
+        lo = peak if res == 1 else S
+        M = -1 if rng.random() < 0.1 else int(rng.integers(lo, 6 * lo + 1))
+        cases.append((cfg(o_, hybrid, chunked, P.REPL_PF, C, M, S=S, reserve=res), wl, A100))
+    assert_parity(cases)
+
+
+def test_large_window_variant():
+    """Workloads of n > 4096 requests run the 32768-slot global-arena variant: every order / policy / reserve,
+    online and offline, with windows far beyond the 4096-slot shared-memory ring (offline: the whole
+    workload is waiting at step 1)."""
+    cases = []
+    for k, seed in enumerate(range(31_000, 31_012)):
+        rng = np.random.default_rng(seed)
+        Wn = int(rng.integers(4097, 9000))
+        wl = workloads.random_small(seed, Wn, max_len=int(rng.integers(4, 64)), online=bool(k % 2), S=256)
+        o_ = k % 5
+        r = [0, 1, 1, P.REPL_PF][k % 4] if k != 6 else 2  # SRF+Hist: the oracle's deferral check is O(n) per
+        res = (1 + k % 2) if r == P.REPL_PF else 0             # candidate -- one case keeps it affordable
+        chunked = int(rng.integers(0, 2))
+        hybrid = int(rng.integers(0, 2)) if o_ < 2 else 1
+        peak = int((wl.I.astype(int) + wl.O - 1).max())
+        C = int(rng.integers(max(1, peak // 2), 4 * peak + 1)) if chunked else int(rng.integers(peak, 4 * peak + 1))
+        lo = 256 if res == 2 else peak
+        M = int(rng.integers(lo, 20 * lo + 1))
+        cases.append((cfg(o_, hybrid, chunked, r, C, M, S=256, reserve=res), wl, A100))
+    assert_parity(cases, processes=len(cases))

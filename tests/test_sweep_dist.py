@@ -33,6 +33,23 @@ def test_grid_sweep_shape():
                                                           "sarathi-nohy") for s in ("", "-srf")}
 
 
+def test_varying_m_sweep_shape():
+    cfgs, wls, cms, labels = sweep.varying_m_sweep()
+    assert len(cfgs) == 3 * 2 * 5 * 11 and len(wls) == 11 and all(w.n == 1024 and int(w.O[0]) == 32 for w in wls)
+    pf = [c for c, lab in zip(cfgs, labels) if lab[0].endswith("-pf")]
+    assert len(pf) == len(cfgs) // 2 and all(c.replacement == 3 and c.reserve == 1 for c in pf)
+    assert sorted({lab[2] for lab in labels}) == [100, 1_000, 10_000, 100_000, 1_000_000]
+
+
+def test_pf_grid_sweep_and_estimate():
+    """E4 grid: the PF versions are just another policy suffix; the LPT estimate charges their full reserve."""
+    cfgs, wls, cms, labels = sweep.grid_sweep(policies=("", "-pf"), preset_names=["vllm"])
+    est = sweep.estimate(cfgs, wls)
+    i = labels.index(("vllm", 1, 1024))
+    j = labels.index(("vllm-pf", 1, 1024))
+    assert est[j] > est[i]
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

@@ -16,8 +16,12 @@ trace: list of dict(step, U, tok, start, d, entries=[(id, phase, c, m_before)],
 from __future__ import annotations
 
 
-def verify(steps, I, O, T, C, M, K_out=None, hybrid=True):
+def verify(steps, I, O, T, C, M, K_out=None, hybrid=True, reserve="seq", S=None):
     """Returns a list of violation strings (empty = valid).
+
+    reserve: the Table 2 "Initial KV reserve" taken at (re)admission:
+    "seq" = s = I + g, "peak" = I + O - 1, "context" = S.  With "peak"/"context" the
+    scheduler is preemption-free: any preemption event is a violation.
 
     K_out: optional dict(t_first=[...], t_done=[...], n_preempt=[...], refill=[...])
     to cross-check the reported per-request outputs against the trace.
@@ -50,6 +54,8 @@ def verify(steps, I, O, T, C, M, K_out=None, hybrid=True):
         prev_end = start + d
         # preemption events (Eq. 4: m := 0 when e = 1); refill keeps g
         for (i, md) in evs:
+            if reserve != "seq":
+                v.append(f"step {j}: preemption of {i} under a preemption-free reserve")
             if not running[i]:
                 v.append(f"step {j}: preempted request {i} was not running")
             if md != m[i]:
@@ -80,9 +86,9 @@ def verify(steps, I, O, T, C, M, K_out=None, hybrid=True):
             if ph == 0 and not (c == 1 and m[i] == s - 1):
                 v.append(f"step {j}: decode entry {i} with c={c}, m={m[i]}, s={s}")
             phases.add(ph)
-            if not running[i]:  # (re)admission reserves s
+            if not running[i]:  # (re)admission reserves the initial reserve
                 running[i] = True
-                res[i] = s
+                res[i] = s if reserve == "seq" else (I[i] + O[i] - 1 if reserve == "peak" else S)
             sum_c += c
         if not hybrid and len(phases) > 1:
             v.append(f"step {j}: hybrid batch while hybrid batching is off")

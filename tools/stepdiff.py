@@ -22,7 +22,7 @@ steps = int(g.results["steps"][0])
 dbg = np.zeros((65536, 6), np.int32)
 L.sim_debug_steps(dbg.ctypes.data, 65536)
 p = presets.preset(name)
-r = o.run(o.make_config(p["order"], p["hybrid"], p["chunked"], p["replacement"], C=p["C"], M=M), wl.I, wl.O, wl.T,
+r = o.run(o.make_config(p["order"], p["hybrid"], p["chunked"], p["replacement"], C=p["C"], M=M, reserve=p["reserve"]), wl.I, wl.O, wl.T,
           o.load_cost_models()["llama3-8b_a100_linear"], trace=True, trace_cap=1 << 28)
 print("gpu steps", steps, "oracle steps", r.steps)
 pre = 0
