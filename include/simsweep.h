@@ -6,7 +6,7 @@
  * scheduler preset (Table 2; Table "Schedulers used",
  * PAPER.md:39-57), one replacement policy (NRF, Table 2; SRF / SRF+Hist,
  * PAPER.md:647-653) and 1..4 batch-latency models.
- * The semantics of every step are the readings Q1-Q38 of DESIGN.md.
+ * The semantics of every step are the readings Q1-Q40 of DESIGN.md.
  *
  * Conventions (all entry points):
  *  - plain pointers and sizes only; the CALLER owns every buffer.  sim_sweep()

@@ -6,7 +6,7 @@
  * cpu_baseline / --impl reference legs may load it.  It shares no code,
  * header, table or constant with paper_2411_07447_b200/ (the product).
  *
- * Semantics: DESIGN.md "Readings" Q1-Q38 (frozen from SURVEY.md 8(c)).
+ * Semantics: DESIGN.md "Readings" Q1-Q40 (frozen from SURVEY.md 8(c), plus Q39-Q40 for the preemption-free reserves).
  */
 #ifndef INFERMAX_ORACLE_H
 #define INFERMAX_ORACLE_H

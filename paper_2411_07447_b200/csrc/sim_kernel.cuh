@@ -18,7 +18,7 @@
 //   a10 Process             parallel m += c, Eq. (6) token generation, completions
 //   run-list maintenance    stable compaction (NRF = admission order); SRF order is
 //                           re-sorted (bitonic) only when the compacted list is unsorted
-// Semantics: DESIGN.md readings Q1-Q38, identical to oracle/oracle.cpp.
+// Semantics: DESIGN.md readings Q1-Q40, identical to oracle/oracle.cpp.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
