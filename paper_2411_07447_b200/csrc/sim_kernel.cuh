@@ -64,8 +64,7 @@ struct Scal {
   long long wred[16][18];  // per-warp partials of the process pass
   int next, new_next, lo, n_done, n_run, nW, nrank, minSW, n_ev, n_vic, nB, nRd;
   int cf_red[32][8];
-  int pa, cut, h_pre, vmin, totmin, wstale;
-  unsigned long long tot[18];  // block totals of the process pass (atomics)
+  int pa, cut, h_pre, vmin, wstale, wfirst;
   int vt, status, any_pre, cur, wbuilt, arena;
   int w_dirty, p_dirty, r_dirty, o_dirty, rank_dirty, removals;
   long long r_Rs;  // scalars handed back by thread 0 after a break

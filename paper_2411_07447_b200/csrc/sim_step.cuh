@@ -134,9 +134,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     S.status = 0;
     S.cur = 0;
     S.w_dirty = S.p_dirty = 1;
-    for (int z = 0; z < 18; z++) S.tot[z] = 0;
-    S.totmin = NOBRK;
     S.wstale = 0;
+    S.wfirst = 0;
   }
   if (tid < K) S.cm[tid] = p.cms[cfg.cost[tid]];
   for (int i = tid; i < 18 * 18; i += NT) S.hist[i] = 0;
@@ -165,6 +164,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           else
             b = mid;
         }
+        if (a > S.next) S.wfirst = min(S.wfirst, S.next);  // new arrivals wait
         S.new_next = a;
         int st = 0;
         if (S.n_done == n)
@@ -220,9 +220,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       __syncthreads();
     }
     int nW = S.nW, minSW = S.minSW, wbuilt = S.wbuilt;
+    const int w0 = max(S.wfirst - lo, 0);  // window offsets below w0 hold no waiting request
     if (!rank && (S.w_dirty || arrived)) {  // |R_w| and its smallest s (the skip test); list built lazily
       int cnt = 0, mn = 0x7fffffff;
-      for (int q = tid; q < nx1 - lo; q += NT) {
+      for (int q = w0 + tid; q < nx1 - lo; q += NT) {
         const int sl = (lo + q) & (CAP - 1);
         if ((s_fl[sl] & ST_MASK) == ST_WAIT) {
           const int4 r = s_rec[sl];
@@ -475,6 +476,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     // exactly the sequential head/tail walk of steps (3)-(4), done in O(1) passes.
     // pf: heads = run[0..k) (prefill-first, non-chunked: every running request decodes),
     // else heads = s_pl[0..k) (R_r^d).  Requires nrun <= CH.
+    int rp_first = 0;  // after decode_group: first run position of a surviving running prefill (nrun if none)
     auto decode_group = [&](bool tail_sync) {  // heads = decodes (F_FILLED) of the run list, retention order
       const bool fM = finiteM && kv1;  // heads need one KV each (else none: admitted up to the token budget)
       const int F = fM ? M - U : 0x3fffffff;
@@ -555,11 +557,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       }
       // (iv) apply: evict [qs, nrun) (+ the self-preempted head), admit heads 1..a
       const int nvic0 = S.n_vic;
-      int ev = 0, eh = 0, er = 0;
+      int ev = 0, eh = 0, er = 0, pm = nrun;
 #pragma unroll
       for (int j = 0; j < IPT_; j++) {
         const int q = nrun - 1 - (tid * IPT_ + j);
         if (q < 0) continue;
+        if (q < qs && !hh[j]) pm = min(pm, q);
         const int sl = run[q];
         if (q >= qs || q == selfp) {
           const int4 rc = s_rec[sl];
@@ -584,11 +587,14 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       ev = (int)__reduce_add_sync(FM, (unsigned)ev);
       eh = (int)__reduce_add_sync(FM, (unsigned)eh);
       if (hist) er = (int)__reduce_add_sync(FM, (unsigned)er);
-      if (lane == 0) S.cf_red[wid][4] = ev, S.cf_red[wid][5] = eh, S.cf_red[wid][6] = er;
+      pm = (int)__reduce_min_sync(FM, (unsigned)pm);
+      if (lane == 0) S.cf_red[wid][4] = ev, S.cf_red[wid][5] = eh, S.cf_red[wid][6] = er, S.cf_red[wid][7] = pm;
       __syncthreads();
       int tev = 0, teh = 0, ter = 0;
+      rp_first = nrun;
 #pragma unroll
-      for (int w = 0; w < NW; w++) tev += S.cf_red[w][4], teh += S.cf_red[w][5], ter += S.cf_red[w][6];
+      for (int w = 0; w < NW; w++)
+        tev += S.cf_red[w][4], teh += S.cf_red[w][5], ter += S.cf_red[w][6], rp_first = min(rp_first, S.cf_red[w][7]);
       tok += a;
       U += (kv1 ? a : 0) - teh;
       nB += a;
@@ -611,11 +617,14 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     // repeat {ballot the lanes that fit alone; prefix-scan them; admit those before the first cumulative
     // failure; drop that failure} -- rejections change no state.  A cropped chunk (chunked prefill)
     // exhausts the token budget and ends the group.
+    int wnext = -1;  // after warp_np(1): no window offset below it holds a waiting request (except victims)
     auto warp_np = [&](int src, int b0, int b1) {
       // one call sees one kind: waiting (src 1: KV delta = s = c for a full admission) or running prefills
       // (src 2 / 0: KV delta 0); counts come from ballots, so only the token prefix is scanned
       const bool overWin = src == 1;
       const unsigned lt = (1u << lane) - 1u;
+      bool wcont = overWin;  // every waiting request at offsets [b0, i0) was admitted
+      if (overWin) wnext = b0;
       for (int i0 = b0; i0 < b1; i0 += 32) {
         if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining one fails
         if (overWin && ((finiteM && (long long)U + minSW > M) || (!chunked && minSW > C - tok))) return;
@@ -639,7 +648,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         const int s = rc.x + rc.y, avail = s - rc.z;
         const int dkv = overWin ? rnew(rc, sl < 0 ? 0 : sl) : 0;  // KV delta: the initial reserve >= s >= c (Q13)
         const int rem = (hist && overWin) ? max(S.pred[bucket_of(rc.x)] - rc.y, 0) : 0;
-        bool alive = sl >= 0;
+        bool alive = sl >= 0, admitted = false;
         for (;;) {
           const int rt = C - tok;
           const bool anyRun0 = n_running > 0;
@@ -693,6 +702,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
               s_fl[sl] = fl | F_INB;
             }
             alive = false;
+            admitted = true;
           }
           const bool cropped = cl < b && cl < 32;
           const int nadm = __popc(fm & (stop >= 32 ? FM : ((1u << stop) - 1u)));
@@ -715,10 +725,20 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           }
           nB += nall;
           if (nall > 0 && bph < 0) bph = PH_PRE;
-          if (cropped) return;  // the token budget is exhausted: every later candidate is rejected
+          if (cropped) break;  // the token budget is exhausted: every later candidate is rejected
           if (b < 32 && lane == b) alive = false;  // rejected (no state change)
           if (b >= 32) break;
         }
+        if (wcont) {  // advance the waiting bound past this chunk unless a waiting request is left in it
+          const unsigned lf = __ballot_sync(FM, sl >= 0 && !admitted);
+          if (lf) {
+            wnext = i0 + __ffs(lf) - 1;
+            wcont = false;
+          } else {
+            wnext = min(i0 + 32, b1);
+          }
+        }
+        if (chunked && tok >= C) return;  // cropped: the token budget is exhausted
       }
     };
 
@@ -738,7 +758,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         if (nrun > 0) decode_group(true);
         PROF_CNT(12, 1);
         if (wid == 0) {
-          if (nrun > 0) warp_np(2, 0, nrun);
+          if (rp_first < nrun) warp_np(2, rp_first, nrun);
           int wdone = nW == 0;
           if (!wdone) {
             const bool wrej = (!hybrid && bph == PH_DEC) || (finiteM && (long long)U + minSW > M) ||
@@ -748,11 +768,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             if (wrej) {
               wdone = 1;
             } else if (amax <= 128 || nx1 - lo <= WARP_MAX) {
-              warp_np(1, 0, nx1 - lo);
+              warp_np(1, w0, nx1 - lo);
               wdone = 1;
             }
           }
           if (lane == 0) {
+            if (wnext >= 0) S.wfirst = lo + wnext;
             S.r_tok = tok, S.r_U = U, S.r_seq = seq, S.r_Rs = Rs, S.r_nB = nB;
             S.r_new = n_new, S.r_running = n_running, S.r_bph = bph, S.r_wdone = wdone;
           }
@@ -789,7 +810,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           PROF_CNT(11, 1);
           if (wid == 0) {
             if (mode == 2)
-              warp_np(1, 0, nx1 - lo);
+              warp_np(1, w0, nx1 - lo);
             else if (mode == 3)
               warp_np(0, pos, lim);
             else
@@ -797,6 +818,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             if (lane == 0) {
               S.r_tok = tok, S.r_U = U, S.r_seq = seq, S.r_Rs = Rs, S.r_nB = nB;
               S.r_new = n_new, S.r_running = n_running, S.r_bph = bph;
+              if (wnext >= 0) S.wfirst = lo + wnext;
             }
           }
           __syncthreads();
@@ -1064,41 +1086,47 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           for (int k = 0; k < SIM_MAX_COST; k++) pce[k] = warp_sum(pce[k]);
         }
       }
-      if (lane == 0) {  // warp partials straight into the block totals (RED.shared)
-        atomicAdd(&S.tot[0], (unsigned long long)N), atomicAdd(&S.tot[1], (unsigned long long)np_);
-        atomicAdd(&S.tot[2], (unsigned long long)cp), atomicAdd(&S.tot[3], (unsigned long long)mp);
-        atomicAdd(&S.tot[4], (unsigned long long)nd), atomicAdd(&S.tot[5], (unsigned long long)md);
-        atomicAdd(&S.tot[6], (unsigned long long)freed), atomicAdd(&S.tot[7], (unsigned long long)ndone);
-        atomicAdd(&S.tot[8], (unsigned long long)mdn), atomicAdd(&S.tot[9], (unsigned long long)nfill);
-        atomicMin(&S.totmin, minrem);
-        if (np_ > 0) {
-          atomicAdd(&S.tot[11], (unsigned long long)c2), atomicAdd(&S.tot[12], (unsigned long long)mc);
-          if (anyTheo) {
-            atomicAdd(&S.tot[13], (unsigned long long)pcm);
-            for (int k = 0; k < SIM_MAX_COST; k++) atomicAdd(&S.tot[14 + k], (unsigned long long)pce[k]);
-          }
-        }
+      if (lane == 0) {  // per-warp partials (plain stores; folded by warp 0 after the barrier)
+        long long* w = S.wred[wid];
+        w[0] = N, w[1] = np_, w[2] = cp, w[3] = mp, w[4] = nd, w[5] = md, w[6] = freed, w[7] = ndone;
+        w[8] = mdn, w[9] = nfill, w[10] = minrem, w[11] = c2, w[12] = mc, w[13] = pcm;
+#pragma unroll
+        for (int k = 0; k < SIM_MAX_COST; k++) w[14 + k] = pce[k];
       }
       // clear the preempted-this-step marks (Q9 applies within one step); smallest s among the victims
       // (they join R_w)
       if (wid == 0) {
         const int nv = S.n_vic;
-        int vmin = 0x7fffffff;
+        int vmin = 0x7fffffff, vidx = 0x7fffffff;
         for (int v = lane; v < nv; v += 32) {
           const int sl = s_vic[v];
           s_fl[sl] &= ~F_PRE;
           const int4 rc = s_rec[sl];
           vmin = min(vmin, rc.x + rc.y);
+          vidx = min(vidx, lo + ((sl - lo) & (CAP - 1)));
         }
         vmin = (int)__reduce_min_sync(FM, (unsigned)vmin);
-        if (lane == 0) S.vmin = vmin;
+        vidx = (int)__reduce_min_sync(FM, (unsigned)vidx);
+        if (lane == 0) {
+          S.vmin = vmin;
+          S.wfirst = min(S.wfirst, vidx);  // this step's victims wait from the next step on
+        }
       }
       __syncthreads();
+      long long tt[18];
+      if (wid == 0) {  // lane z folds column z of the per-warp partials; thread 0 gathers them
+        long long v = lane == 10 ? (long long)NOBRK : 0;
+        if (lane < 18) {
+#pragma unroll
+          for (int w = 0; w < NW; w++) {
+            const long long x = S.wred[w][lane];
+            v = lane == 10 ? min(v, x) : v + x;
+          }
+        }
+#pragma unroll
+        for (int z = 0; z < 18; z++) tt[z] = __shfl_sync(FM, v, z);
+      }
       if (tid == 0) {
-        long long tt[18];
-        for (int z = 0; z < 18; z++) tt[z] = (long long)S.tot[z], S.tot[z] = 0;
-        tt[10] = S.totmin;
-        S.totmin = NOBRK;
         const int vmin = S.vmin;
         {
           Feat f;
