@@ -141,13 +141,17 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   for (int i = tid; i < 18 * 18; i += NT) S.hist[i] = 0;
   __syncthreads();
 #ifdef SIMSWEEP_PROFILE
-  long long prof[16] = {0};
+  long long prof[24] = {0};
   long long prof_last = clock64();
 #endif
 
   int exit_status = 0;
+#ifdef SIMSWEEP_TRACE
+  int trn = 0;
+#endif
   for (;;) {
     PROF_MARK(10);
+    TMARK(1);
     // ---- (1) a2: GetNewRequests (Alg. 1 line 3): all T <= clock, inclusive (Q21) ----
     int nx1;
     if (S.next >= n) {  // everything has arrived (offline after step 1): uniform checks, no barrier
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     }
     if (arrived) __syncthreads();
     PROF_MARK(0);
+    TMARK(2);
     // ---- (2) a3: GroupRequests (step 1) ----
     if (rank && arrived) {  // one group sorted by (key, T, id) (App. D, Q20, Q37)
       for (int idx = nx0 + tid; idx < nx1; idx += NT) s_rank[nrank + idx - nx0] = (int16_t)(idx & (CAP - 1));
@@ -289,6 +294,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       S.visits += nP;
     }
     PROF_MARK(1);
+    TMARK(3);
 
     // ---- (3) a4-a8: GetNextBatch (steps 2-4) ----
     int tok = 0, U = (int)S.U, n_new = 0, n_running = nrun, bph = -1, pos = 0, nB = 0;
@@ -481,15 +487,21 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       const bool fM = finiteM && kv1;  // heads need one KV each (else none: admitted up to the token budget)
       const int F = fM ? M - U : 0x3fffffff;
       const int T = C - tok;
+      // warps whose items all lie beyond the run list only meet the barriers and fold the active warps' partials
+      const int nact = min(NW, (nrun + 32 * IPT_ - 1) / (32 * IPT_));
+      TMARK(10);
+      const bool act = wid < nact;
       // (i) reverse scan over run positions of (held, is-head): RS(q) = sum held at >= q, HS(q) = heads at >= q
       int hv[IPT_], rsv[IPT_], hsv[IPT_], ls = 0, lh = 0;
       bool hh[IPT_];
+      int16_t sls[IPT_];
 #pragma unroll
       for (int j = 0; j < IPT_; j++) {
         const int q = nrun - 1 - (tid * IPT_ + j);
-        hv[j] = 0, hh[j] = false;
+        hv[j] = 0, hh[j] = false, sls[j] = 0;
         if (q >= 0) {
           const int sl = run[q];
+          sls[j] = (int16_t)sl;
           const int4 rc = s_rec[sl];
           hv[j] = max(rc.w, rc.z);
           hh[j] = (s_fl[sl] & F_FILLED) != 0;
@@ -497,104 +509,120 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         ls += hv[j], lh += hh[j];
       }
       int xs = ls, xh = lh;
+      if (act) {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int ys = __shfl_up_sync(FM, xs, o), yh = __shfl_up_sync(FM, xh, o);
-        if (lane >= o) xs += ys, xh += yh;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int ys = __shfl_up_sync(FM, xs, o), yh = __shfl_up_sync(FM, xh, o);
+          if (lane >= o) xs += ys, xh += yh;
+        }
+        if (lane == 31) S.cf_red[wid][0] = xs, S.cf_red[wid][1] = xh;
       }
-      if (lane == 31) S.cf_red[wid][0] = xs, S.cf_red[wid][1] = xh;
       __syncthreads();
       int os = xs - ls, oh = xh - lh, k = 0;
-#pragma unroll
-      for (int w = 0; w < NW; w++) {
+      for (int w = 0; w < nact; w++) {
         const int a0 = S.cf_red[w][0], a1 = S.cf_red[w][1];
         if (w < wid) os += a0, oh += a1;
         k += a1;
       }
 #pragma unroll
       for (int j = 0; j < IPT_; j++) os += hv[j], oh += hh[j], rsv[j] = os, hsv[j] = oh;
+      TMARK(11);
       // (ii) a_kv = #{heads i : F + RS(p_i + 1) >= i}, i = k - HS(p_i) + 1 (monotone in i)
-      int cnt = 0;
+      int akv = k;
       if (fM) {
+        if (act) {
+          int cnt = 0;
 #pragma unroll
-        for (int j = 0; j < IPT_; j++)
-          if (hh[j]) cnt += F + (rsv[j] - hv[j]) >= k - hsv[j] + 1;
+          for (int j = 0; j < IPT_; j++)
+            if (hh[j]) cnt += F + (rsv[j] - hv[j]) >= k - hsv[j] + 1;
+          cnt = (int)__reduce_add_sync(FM, (unsigned)cnt);
+          if (lane == 0) S.cf_red[wid][2] = cnt;
+        }
+        __syncthreads();
+        akv = 0;
+        for (int w = 0; w < nact; w++) akv += S.cf_red[w][2];
       }
-      cnt = (int)__reduce_add_sync(FM, (unsigned)cnt);
-      if (lane == 0) S.cf_red[wid][2] = cnt;
-      __syncthreads();
-      int akv = 0;
-#pragma unroll
-      for (int w = 0; w < NW; w++) akv += S.cf_red[w][2];
-      if (!fM) akv = k;
+      TMARK(12);
       const int a = min(min(akv, T), k);
       // (iii) q* = max{q : F + RS(q) >= a}; the position of head a+1
       const bool needq = fM && F < a;
-      int cq = 0;
+      const bool needp = fM && a == akv && a < min(k, T);
+      int qs = nrun, selfp = -1;
+      if (needq || needp) {
+        if (act) {
+          int cq = 0;
 #pragma unroll
-      for (int j = 0; j < IPT_; j++) {
-        const int q = nrun - 1 - (tid * IPT_ + j);
-        if (q >= 0) {
-          if (needq) cq += F + rsv[j] >= a;
-          if (hh[j] && k - hsv[j] + 1 == a + 1) S.pa = q;
+          for (int j = 0; j < IPT_; j++) {
+            const int q = nrun - 1 - (tid * IPT_ + j);
+            if (q >= 0) {
+              if (needq) cq += F + rsv[j] >= a;
+              if (hh[j] && k - hsv[j] + 1 == a + 1) S.pa = q;
+            }
+          }
+          cq = (int)__reduce_add_sync(FM, (unsigned)cq);
+          if (lane == 0) S.cf_red[wid][3] = cq;
+        }
+        __syncthreads();
+        if (needq) {
+          int tot = 0;
+          for (int w = 0; w < nact; w++) tot += S.cf_red[w][3];
+          qs = tot - 1;
+        }
+        // head a+1, when the KV (not the token budget) stopped the walk: a victim if it lies in the evicted
+        // suffix, else it runs out of pool, evicts everything behind it and self-preempts (Q8)
+        if (needp) {
+          const int pa = S.pa;
+          if (pa < qs) selfp = pa, qs = pa + 1;
         }
       }
-      cq = (int)__reduce_add_sync(FM, (unsigned)cq);
-      if (lane == 0) S.cf_red[wid][3] = cq;
-      __syncthreads();
-      int qs = nrun, selfp = -1;
-      if (needq) {
-        int tot = 0;
-#pragma unroll
-        for (int w = 0; w < NW; w++) tot += S.cf_red[w][3];
-        qs = tot - 1;
-      }
-      // head a+1, when the KV (not the token budget) stopped the walk: a victim if it lies in the evicted
-      // suffix, else it runs out of pool, evicts everything behind it and self-preempts (Q8)
-      if (fM && a == akv && a < min(k, T)) {
-        const int pa = S.pa;
-        if (pa < qs) selfp = pa, qs = pa + 1;
-      }
+      TMARK(13);
       // (iv) apply: evict [qs, nrun) (+ the self-preempted head), admit heads 1..a
       const int nvic0 = S.n_vic;
-      int ev = 0, eh = 0, er = 0, pm = nrun;
+      const bool evict = qs < nrun || selfp >= 0;
+      int tev = 0, teh = 0, ter = 0;
+      if (act) {
+        int ev = 0, eh = 0, er = 0, pm = nrun;
 #pragma unroll
-      for (int j = 0; j < IPT_; j++) {
-        const int q = nrun - 1 - (tid * IPT_ + j);
-        if (q < 0) continue;
-        if (q < qs && !hh[j]) pm = min(pm, q);
-        const int sl = run[q];
-        if (q >= qs || q == selfp) {
-          const int4 rc = s_rec[sl];
-          ev++;
-          eh += hv[j];
-          if (hist) er += max(S.pred[bucket_of(rc.x)] - rc.y, 0);
-          const int idx = lo + ((sl - lo) & (CAP - 1));
-          atomicAdd(&npre[idx], 1ull);
-          atomicAdd(&refill[idx], (unsigned long long)rc.z);
-          s_rec[sl] = make_int4(rc.x, rc.y, 0, 0);
-          s_fl[sl] = ST_WAIT | F_PRE | (s_fl[sl] & F_FIRST);
-          s_vic[nvic0 + (q == selfp ? nrun - qs : q - qs)] = (int16_t)sl;
-        } else if (hh[j]) {
-          const int i = k - hsv[j] + 1;
-          if (i <= a) {
-            s_c[sl] = 1;
-            s_fl[sl] |= F_INB;
-            s_bl[nB + i - 1] = (int16_t)sl;
+        for (int j = 0; j < IPT_; j++) {
+          const int q = nrun - 1 - (tid * IPT_ + j);
+          if (q < 0) continue;
+          if (q < qs && !hh[j]) pm = min(pm, q);
+          const int sl = sls[j];
+          if (q >= qs || q == selfp) {
+            const int4 rc = s_rec[sl];
+            ev++;
+            eh += hv[j];
+            if (hist) er += max(S.pred[bucket_of(rc.x)] - rc.y, 0);
+            const int idx = lo + ((sl - lo) & (CAP - 1));
+            atomicAdd(&npre[idx], 1ull);
+            atomicAdd(&refill[idx], (unsigned long long)rc.z);
+            s_rec[sl] = make_int4(rc.x, rc.y, 0, 0);
+            s_fl[sl] = ST_WAIT | F_PRE | (s_fl[sl] & F_FIRST);
+            s_vic[nvic0 + (q == selfp ? nrun - qs : q - qs)] = (int16_t)sl;
+          } else if (hh[j]) {
+            const int i = k - hsv[j] + 1;
+            if (i <= a) {
+              s_c[sl] = 1;
+              s_fl[sl] |= F_INB;
+              s_bl[nB + i - 1] = (int16_t)sl;
+            }
           }
         }
+        if (evict) {  // evictions happened: count them (the common step has none)
+          ev = (int)__reduce_add_sync(FM, (unsigned)ev);
+          eh = (int)__reduce_add_sync(FM, (unsigned)eh);
+          if (hist) er = (int)__reduce_add_sync(FM, (unsigned)er);
+        }
+        pm = (int)__reduce_min_sync(FM, (unsigned)pm);
+        if (lane == 0) S.cf_red[wid][4] = ev, S.cf_red[wid][5] = eh, S.cf_red[wid][6] = er, S.cf_red[wid][7] = pm;
       }
-      ev = (int)__reduce_add_sync(FM, (unsigned)ev);
-      eh = (int)__reduce_add_sync(FM, (unsigned)eh);
-      if (hist) er = (int)__reduce_add_sync(FM, (unsigned)er);
-      pm = (int)__reduce_min_sync(FM, (unsigned)pm);
-      if (lane == 0) S.cf_red[wid][4] = ev, S.cf_red[wid][5] = eh, S.cf_red[wid][6] = er, S.cf_red[wid][7] = pm;
       __syncthreads();
-      int tev = 0, teh = 0, ter = 0;
+      TMARK(14);
       rp_first = nrun;
-#pragma unroll
-      for (int w = 0; w < NW; w++)
-        tev += S.cf_red[w][4], teh += S.cf_red[w][5], ter += S.cf_red[w][6], rp_first = min(rp_first, S.cf_red[w][7]);
+      for (int w = 0; w < nact; w++) {
+        if (evict) tev += S.cf_red[w][4], teh += S.cf_red[w][5], ter += S.cf_red[w][6];
+        rp_first = min(rp_first, S.cf_red[w][7]);
+      }
       tok += a;
       U += (kv1 ? a : 0) - teh;
       nB += a;
@@ -608,6 +636,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         S.vt = min(S.vt, (selfp >= 0 ? selfp : qs) - 1);
         S.cut = selfp >= 0 ? selfp : qs;  // run positions >= cut were evicted (a suffix)
       }
+      TMARK(15);
       if (tail_sync) __syncthreads();  // evictions and admissions are visible; cf_red may be reused
     };
 
@@ -744,6 +773,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
 
     bool rfast = false;  // the decode-first running groups were resolved (once per step)
     while (pos < nP) {
+      TMARK(20);
       // running decodes in closed form
       if (order == SIM_ORDER_PREFILL_FIRST && pos == nW && nW < nP && !chunked && nrun <= CH) {
         if (hybrid || bph != PH_PRE) decode_group(false);  // else every decode fails step 2 (no running prefills)
@@ -989,6 +1019,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       pos = b + 1;
     }
     __syncthreads();  // admissions of the last round are visible
+    TMARK(21);
     if (tok == 0) {   // B = {}: idle jump to the next arrival, not a step (Q21)
       if (tid == 0) {
         if (S.any_pre)
@@ -1016,6 +1047,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       unsigned N = 0, np_ = 0, cp = 0, mp = 0, nd = 0, md = 0, freed = 0, ndone = 0, mdn = 0, nfill = 0;
       int minrem = NOBRK;
       long long c2 = 0, mc = 0, pcm = 0, pce[SIM_MAX_COST] = {0, 0, 0, 0};
+      const int nwa = min(NW, (nB + 31) >> 5);  // warps holding batch entries; the others only meet the barrier
+      if (wid < nwa) {
       for (int e = tid; e < nB; e += NT) {
         const int sl = s_bl[e];
         uint8_t fl = s_fl[sl];
@@ -1072,6 +1105,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         s_rec[sl] = make_int4(rc.x, g, m, rc.w);
         s_fl[sl] = fl;
       }
+      TMARK(30);
       N = __reduce_add_sync(FM, N), np_ = __reduce_add_sync(FM, np_), cp = __reduce_add_sync(FM, cp);
       mp = __reduce_add_sync(FM, mp), nd = __reduce_add_sync(FM, nd), md = __reduce_add_sync(FM, md);
       freed = __reduce_add_sync(FM, freed), ndone = __reduce_add_sync(FM, ndone);
@@ -1093,6 +1127,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
 #pragma unroll
         for (int k = 0; k < SIM_MAX_COST; k++) w[14 + k] = pce[k];
       }
+      }  // wid < nwa
+      TMARK(31);
       // clear the preempted-this-step marks (Q9 applies within one step); smallest s among the victims
       // (they join R_w)
       if (wid == 0) {
@@ -1114,11 +1150,11 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       }
       __syncthreads();
       long long tt[18];
+      TMARK(33);
       if (wid == 0) {  // lane z folds column z of the per-warp partials; thread 0 gathers them
         long long v = lane == 10 ? (long long)NOBRK : 0;
         if (lane < 18) {
-#pragma unroll
-          for (int w = 0; w < NW; w++) {
+          for (int w = 0; w < nwa; w++) {
             const long long x = S.wred[w][lane];
             v = lane == 10 ? min(v, x) : v + x;
           }
@@ -1126,6 +1162,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
 #pragma unroll
         for (int z = 0; z < 18; z++) tt[z] = __shfl_sync(FM, v, z);
       }
+      TMARK(34);
       if (tid == 0) {
         const int vmin = S.vmin;
         {
@@ -1134,6 +1171,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           f.c2 = tt[11], f.mc = tt[12], f.pcm = tt[13];
           f.pceil[0] = tt[14], f.pceil[1] = tt[15], f.pceil[2] = tt[16], f.pceil[3] = tt[17];
           for (int k = 0; k < K; k++) S.clock[k] = dadd(S.clock[k], batch_time(S.cm[k], f, k));  // Q36
+          TMARK(35);
 #ifdef SIMSWEEP_PROFILE
           if (ci == 0 && S.steps < DBG_STEPS) {
             int* d = g_dbg[S.steps];
@@ -1141,6 +1179,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           }
 #endif
           S.steps++;
+          PROF_CNT(16, 1);
           S.sumU += U;
           S.entries += f.np + f.nd;
           S.processed += f.N;
@@ -1183,6 +1222,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       }
       __syncthreads();
     }
+    TMARK(36);
     PROF_MARK(3);
 
     // ---- (5) event times; steady decode run ----
@@ -1196,6 +1236,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         if (code & (2 << SLB))
           for (int k = 0; k < K; k++) td[(long long)k * n + idx] = S.clock[k];
       }
+      TMARK(40);
       const long long Lr = S.runL;
       if (Lr > 0) {
         constexpr int DB = CAP / 2;
@@ -1228,7 +1269,16 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             } else {
               for (int k = 0; k < K; k++) {
                 double clk = S.clock[k];
-                for (int t = 0; t < chunk; t++) clk = dadd(clk, s_dbuf[k * cmax + t]);
+                const double* db = s_dbuf + k * cmax;
+                int t = 0;
+                for (; t + 8 <= chunk; t += 8) {  // loads first: the chain is one DADD latency per step
+                  double v[8];
+#pragma unroll
+                  for (int u = 0; u < 8; u++) v[u] = db[t + u];
+#pragma unroll
+                  for (int u = 0; u < 8; u++) clk = dadd(clk, v[u]);
+                }
+                for (; t < chunk; t++) clk = dadd(clk, db[t]);
                 S.clock[k] = clk;
               }
             }
@@ -1269,6 +1319,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             }
 #endif
           S.steps += E;
+          PROF_CNT(17, E);
           S.sumU += E * U0 + du * (E * (E + 1) / 2);
           S.entries += E * ndd;
           S.processed += E * ndd;
@@ -1281,6 +1332,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         __syncthreads();
       }
     }
+    TMARK(41);
     PROF_MARK(4);
 
     // ---- (6) run list (retention order) for the next step ----
@@ -1316,6 +1368,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           __syncthreads();
         }
       }
+      TMARK(50);
       if (od) {  // SRF retention order: m descending, then admission order (Q3, Q7)
         auto key = [&](int sl) -> unsigned long long {
           return ((unsigned long long)(0x3FFFF - s_rec[sl].z) << 46) |
@@ -1335,6 +1388,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           __syncthreads();
         }
       }
+      TMARK(51);
       if (moved)
         for (int q = tid; q < cnt; q += NT) s_rpos[rl[q]] = (int16_t)q;
       if (tid == 0) {
@@ -1346,6 +1400,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         S.lo = l;
       }
       __syncthreads();
+      TMARK(52);
       PROF_MARK(5);
     }
   }
@@ -1356,10 +1411,13 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     prof[14] = (long long)t_start, prof[15] = (long long)t_end, prof[9] = smid;
-    for (int i = 0; i < 16; i++) g_prof[ci][i] = prof[i];
+    for (int i = 0; i < 24; i++) g_prof[ci][i] = prof[i];
   }
 #endif
 
+#ifdef SIMSWEEP_TRACE
+  if (tid == 0 && ci == 0) g_trn = trn;
+#endif
   // ---- a11: metrics ----
   const int st = exit_status == -1 ? SIM_S_OK : exit_status;
   __threadfence();

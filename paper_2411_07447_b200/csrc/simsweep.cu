@@ -19,7 +19,7 @@ namespace simsweep {
 
 #ifdef SIMSWEEP_PROFILE  // phase cycle counters of thread 0 (tools/probe.py); not in the product build
 constexpr int PROF_MAX_CFG = 8192;
-__device__ long long g_prof[PROF_MAX_CFG][16];
+__device__ long long g_prof[PROF_MAX_CFG][24];
 constexpr int DBG_STEPS = 1 << 16;
 __device__ int g_dbg[DBG_STEPS][6];  // config 0 only: per full step (steps, tok, U, nB, preemptions, n_vic)
 #define PROF_MARK(i)                  \
@@ -35,6 +35,21 @@ __device__ int g_dbg[DBG_STEPS][6];  // config 0 only: per full step (steps, tok
 #define PROF_CNT(i, v)
 #endif
 
+#ifdef SIMSWEEP_TRACE  // clock marks of thread 0 of config 0 (tools/tmarks.py); not in the product build
+constexpr int TR_MAX = 1 << 22;
+__device__ unsigned g_tr[TR_MAX];
+__device__ int g_trn;
+#define TMARK(i)                                               \
+  if (tid == 0 && ci == 0) {                                   \
+    unsigned _c;                                               \
+    asm volatile("mov.u32 %0, %%clock;" : "=r"(_c)::"memory"); \
+    if (trn < TR_MAX / 2) g_tr[2 * trn] = (i), g_tr[2 * trn + 1] = _c; \
+    trn++;                                                     \
+  }
+#else
+#define TMARK(i)
+#endif
+
 // 0: W <= 1024 and 1: W <= 4096, state in shared memory (the window never exceeds n <= CAP);
 // 2: larger workloads, a 32768-slot ring in a per-CTA global-memory arena (SIM_MAX_WINDOW)
 __host__ __device__ inline int variant_of(int n) { return n <= 1024 ? 0 : (n <= 4096 ? 1 : 2); }
@@ -42,6 +57,9 @@ constexpr int N_VARIANTS = 3;
 
 #ifndef SIM_NT_SMALL
 #define SIM_NT_SMALL 256  // threads per CTA of the W <= 1024 variant
+#endif
+#ifndef SIM_IPT_SMALL
+#define SIM_IPT_SMALL (1024 / SIM_NT_SMALL)  // candidates per thread and round of the W <= 1024 variant
 #endif
 
 template <int NT>
@@ -76,7 +94,7 @@ Variant make_variant() {
   return Variant{NT, CAP, GM ? L::scal : L::bytes, GM ? L::arr_bytes : 0, sim_kernel<NT, CAP, IPT_, GM>};
 }
 
-static Variant g_variants[N_VARIANTS] = {make_variant<SIM_NT_SMALL, 1024, 1024 / SIM_NT_SMALL, false>(),
+static Variant g_variants[N_VARIANTS] = {make_variant<SIM_NT_SMALL, 1024, SIM_IPT_SMALL, false>(),
                                          make_variant<512, 4096, 4, false>(), make_variant<512, SIM_MAX_WINDOW, 4, true>()};
 
 static int64_t workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int32_t* wls_n) {
@@ -94,9 +112,15 @@ using namespace simsweep;
 
 extern "C" {
 
+#ifdef SIMSWEEP_TRACE
+int sim_trace_read(uint32_t* out, int32_t n, int32_t* count) {
+  if (cudaMemcpyFromSymbol(count, g_trn, sizeof(int)) != cudaSuccess) return SIM_ECUDA;
+  return cudaMemcpyFromSymbol(out, g_tr, sizeof(unsigned) * 2 * (size_t)n) == cudaSuccess ? 0 : SIM_ECUDA;
+}
+#endif
 #ifdef SIMSWEEP_PROFILE
 int sim_debug_read(int64_t* out, int32_t n_cfgs) {
-  return cudaMemcpyFromSymbol(out, g_prof, sizeof(long long) * 16 * (size_t)n_cfgs) == cudaSuccess ? 0 : SIM_ECUDA;
+  return cudaMemcpyFromSymbol(out, g_prof, sizeof(long long) * 24 * (size_t)n_cfgs) == cudaSuccess ? 0 : SIM_ECUDA;
 }
 int sim_debug_steps(int32_t* out, int32_t n) {
   return cudaMemcpyFromSymbol(out, g_dbg, sizeof(int) * 6 * (size_t)n) == cudaSuccess ? 0 : SIM_ECUDA;

@@ -4,6 +4,7 @@ import csv
 import subprocess
 import sys
 
+COL = int(sys.argv[2]) if len(sys.argv) > 2 else 4  # 4 = stall samples, 7 = instructions executed
 RANGES = [("setup", 1, 149), ("arrivals+groups", 150, 291), ("handle/preempt", 292, 364), ("warp_run", 365, 469),
           ("decode_group", 470, 607), ("warp_np", 608, 724), ("round driver", 725, 968), ("idle", 969, 991),
           ("process+cost", 992, 1158), ("events+steady", 1159, 1257), ("run list", 1258, 1323), ("metrics", 1324, 2000)]
@@ -17,7 +18,7 @@ for r in csv.reader(out.splitlines()):
         fname = r[1].rsplit("/", 1)[-1]
         continue
     try:
-        ln, s = int(r[0]), float(r[4])
+        ln, s = int(r[0]), float(r[COL])
     except (ValueError, IndexError):
         continue
     tot += s

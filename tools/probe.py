@@ -38,7 +38,7 @@ if "--one" in sys.argv:  # a single simulation (for ncu: -k regex:sim_kernel -s 
     j = sys.argv.index("--one")
     cases = [(sys.argv[j + 1], int(sys.argv[j + 2]), int(sys.argv[j + 3]))]
 else:
-  cases = [("vllm", 1024, 1024), ("vllm-srf", 1024, 1024), ("sarathi", 1024, 1024), ("sarathi-srf", 1024, 1024),
+  cases = [("vllm", 128, 1024), ("vllm", 256, 1024), ("vllm", 1024, 1024), ("vllm-srf", 1024, 1024), ("sarathi", 1024, 1024), ("sarathi-srf", 1024, 1024),
          ("vllm", 1, 1024), ("sarathi", 1, 1024), ("sarathi-nohy", 1024, 1024), ("vllm-hy-srf", 64, 1024),
          ("sarathi-cs", 256, 256), ("vllm", 16, 16), ("sarathi-nocp-srf", 4, 512)]
 print(f"{'case':28s} {'steps':>7s} {'ms':>8s} {'us/step':>8s} {'rnd/st':>6s} {'brk/st':>6s} {'sorts':>6s} " +
@@ -56,7 +56,7 @@ for (nm, I, O) in cases:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     r = ds.fetch().results[0]
-    prof = np.zeros(16, np.int64)
+    prof = np.zeros(24, np.int64)
     if not PRODUCT:
         L.sim_debug_read(prof.ctypes.data, 1)
     steps = int(r["steps"])
@@ -64,5 +64,7 @@ for (nm, I, O) in cases:
     tot = prof[[0, 1, 2, 3, 4, 5, 10]].sum()
     share = " ".join(f"{100.0 * prof[i] / max(tot, 1):8.1f}%" for i in range(6))
     share += " | warp-mode/st %.2f closedR/st %.2f chunks/st %.1f wbrk/st %.2f" % tuple(prof[i] / steps for i in (11, 12, 13, 14))
+    full = max(int(prof[16]), 1)
+    share += f" | full steps {full} ({1000 * ms / full:.2f} us/full step), run steps {int(prof[17])}"
     print(f"{nm + f' {I}/{O}':28s} {steps:7d} {ms:8.2f} {1000 * ms / steps:8.2f} {prof[6] / steps:6.2f} "
           f"{prof[7] / steps:6.2f} {prof[8]:6d} {share}  cyc/step={tot / steps:.0f}")

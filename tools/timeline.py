@@ -13,7 +13,7 @@ cfgs, wls, cms, labels = sweep.grid_sweep()
 order = sweep.partition_lpt(sweep.estimate(cfgs, wls), 1)[0]
 ds = simsweep.DeviceSweep(cfgs, wls, cms, order=np.asarray(order, np.int32))
 ds.launch(); torch.cuda.synchronize(); ds.launch(); torch.cuda.synchronize()
-prof = np.zeros((len(cfgs), 16), np.int64)
+prof = np.zeros((len(cfgs), 24), np.int64)
 L.sim_debug_read(prof.ctypes.data, len(cfgs))
 res = ds.fetch().results
 t0 = prof[:, 14].min()
@@ -30,3 +30,5 @@ for i in idx:
     print(f"  {labels[i]!s:32s} {st[i]:7.2f} {du[i]:7.2f} {en[i]:7.2f} {int(res['steps'][i]):7d} {rank[i]:5d} {est[i]:9.0f}")
 hist = np.histogram(st, bins=[0, 1, 5, 10, 20, 40, 80])[0]
 print("start-time histogram [0,1,5,10,20,40,80] ms:", hist)
+if len(sys.argv) > 1:  # save per-simulation start/duration/steps for offline comparison
+    np.savez(sys.argv[1], st=st, du=du, steps=np.asarray(res["steps"]), labels=np.asarray([str(l) for l in labels]))
