@@ -8,7 +8,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "simsweep.cu")]
-HDRS = [os.path.join(PKG, "csrc", h) for h in ("sim_kernel.cuh", "sim_step.cuh")]
+HDRS = [os.path.join(PKG, "csrc", h) for h in ("sim_kernel.cuh", "sim_step.cuh", "sim_warp.cuh")]
 DEPS = SRC + HDRS + [os.path.join(ROOT, "include", "simsweep.h")]
 LIB = os.path.join(PKG, "libsimsweep.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -28,10 +28,14 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False, defines=()) -> str:
-    """profile=True builds libsimsweep_prof.so with per-phase cycle counters (tools/probe.py)."""
-    lib = LIB.replace(".so", "_prof.so") if profile else LIB
-    if force or profile or needs_build():
+WARP_LIB = LIB.replace(".so", "_warp.so")
+
+
+def build(force: bool = False, verbose: bool = False, profile: bool = False, defines=(), lib=None) -> str:
+    """profile=True builds libsimsweep_prof.so with per-phase cycle counters (tools/probe.py); lib=WARP_LIB with
+    defines=("SIM_WARP_SMALL",) builds the opt-in warp-per-simulation variant for W <= 1024."""
+    lib = lib or (LIB.replace(".so", "_prof.so") if profile else LIB)
+    if force or profile or lib != LIB or needs_build():
         cmd = ([NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + (["-DSIMSWEEP_PROFILE"] if profile else []) + ["-D" + d for d in defines]
                + ["-o", lib] + SRC)
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -20,6 +20,14 @@ t0 = prof[:, 14].min()
 st = (prof[:, 14] - t0) / 1e6
 en = (prof[:, 15] - t0) / 1e6
 du = en - st
+sm = prof[:, 9]
+print("max simulations per SM over the sweep:", np.bincount(sm).max(), "SMs used:", len(np.unique(sm)))
+ev = sorted([(s, 1) for s in st] + [(e, -1) for e in en])
+cur = mx = 0
+for _, d in ev:
+    cur += d
+    mx = max(mx, cur)
+print("max concurrently running simulations:", mx)
 print(f"sweep makespan {en.max():.2f} ms; sum of sim durations {du.sum():.1f} ms; "
       f"mean concurrency {du.sum() / en.max():.0f}; longest sim {du.max():.2f} ms")
 idx = np.argsort(-en)[:25]
