@@ -197,7 +197,7 @@ def bench_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfgs, wls, cms, _ = sweep.grid_sweep(M=rank_M(rank))
+    cfgs, wls, cms, labels = sweep.grid_sweep(M=rank_M(rank))
     order = sweep.partition_lpt(sweep.estimate(cfgs, wls), 1)[0]  # longest first within the rank
     ds = simsweep.DeviceSweep(cfgs, wls, cms, device=dev, order=np.asarray(order, np.int32))
     stream = torch.cuda.Stream(device=dev)
@@ -261,6 +261,26 @@ def bench_ours(args, rank, world, local_rank):
     value = steps_all / (ms / 1000.0)
     n_sims = len(cfgs) * world
 
+    # critical path (outside the timed region): the longest-estimated simulations, each launched alone.  The
+    # sweep can never be shorter than its longest simulation (each simulation is one dependent chain of steps).
+    critical = None
+    if rank == 0 and not args.no_critical:
+        top = order[:16]  # LPT order: the largest step-count estimates first
+        alone = []
+        for i in top:
+            one = simsweep.DeviceSweep([simsweep.SimConfig.from_buffer_copy(cfgs[int(i)])], wls, cms, device=dev)
+            one.launch(stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            one.launch(stream)
+            e1.record(stream)
+            stream.synchronize()
+            alone.append((e0.elapsed_time(e1), int(i)))
+        lm, li = max(alone)
+        critical = {"longest_simulation_alone_ms": lm, "longest_simulation": "%s I=%d O=%d" % labels[li],
+                    "its_steps": int(res["steps"][li]), "sweep_kernel_over_longest": kms / lm,
+                    "probed": "the 16 simulations with the largest LPT estimates, each launched alone"}
+
     # e2e: the public host API (sim_sweep: pinned H2D + kernel + D2H, blocking), every step
     e2e = None
     if not args.no_e2e:
@@ -315,7 +335,8 @@ def bench_ours(args, rank, world, local_rank):
         "data": "synthetic",
         "config": workload_desc(world) | {"configs_per_s": n_sims / (ms / 1000.0), "kernel_ms": kms,
                                           "steps_per_sweep": steps_all, "batch_entries_per_sweep": entries_all,
-                                          "candidate_visits_per_sweep": visits_all, "failed_simulations": bad},
+                                          "candidate_visits_per_sweep": visits_all, "failed_simulations": bad,
+                                          "critical_path": critical},
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tintop/s",
                      "frac": achieved / peak_ops, "traffic": traffic,
                      "kernel": "simsweep::sim_kernel<256,1024>",
@@ -346,6 +367,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-critical", action="store_true")
     args = ap.parse_args()
     rank, world, local_rank = _env_dist()
     if args.impl == "reference":
