@@ -185,6 +185,48 @@ int64_t sim_workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int3
 int sim_request_rows(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
                      int64_t* rows, int64_t* tim_rows);
 
+/* ---- Cost-model analytics: the batch-latency model of
+ * row a9 evaluated on batch shapes instead of simulated batches.  All three
+ * calls take HOST buffers, evaluate on CUDA device `device` (current if < 0),
+ * are blocking, return 0 / SIM_E*, and use the expression order of DESIGN.md 2
+ * (fp64, no contraction), so a shape gets the exact d_j a simulated batch with
+ * the same entries gets. */
+
+/* One batch shape: n_p prefill entries, each processing c tokens on top of m_p
+ * cached KVs, plus n_d decode entries, each on top of m_d cached KVs
+ * (Eq. (1)-(2) per request).  n_p, n_d >= 0, n_p + n_d >= 1,
+ * c >= 1 when n_p > 0; every feature sum must stay below 2^62. */
+typedef struct {
+  int64_t n_p, c, m_p, n_d, m_d;
+} sim_batch_shape_t;
+
+/* Batch time (seconds) of every shape under every cost model:
+ * out[k * n + i] = d(shapes[i]) under cms[k] (k-major).  SIM_EINVAL on a bad
+ * shape or n <= 0, SIM_ECOST on a bad model. */
+int sim_batch_times(const sim_cost_model_t* cms, int32_t n_cms, const sim_batch_shape_t* shapes, int32_t n,
+                    double* out, int32_t device);
+
+/* SLO frontier (Fig. SLO, "TPOT threshold of 1s" :574): a hybrid batch of n_p prefills
+ * (c, m) and n_d decodes (m) sharing one m.  For every query and model, the
+ * largest m in [0, m_max] whose batch time is <= tau (binary search; the time
+ * is non-decreasing in m for non-negative linear coefficients and for Eq. (3)),
+ * or -1 when even m = 0 exceeds tau.  out[k * n + i]. */
+typedef struct {
+  int64_t n_p, c, n_d, m_max;
+  double tau; /* seconds (the paper's TPOT threshold: 1 s) */
+} sim_slo_query_t;
+int sim_slo_frontier(const sim_cost_model_t* cms, int32_t n_cms, const sim_slo_query_t* q, int32_t n, int64_t* out,
+                     int32_t device);
+
+/* Recompute vs swap and the 5-minute rule for KVs (Eq. (8)-(9),
+ * PAPER.md:257-274).  For N[i] >= 1 KVs of one request and every model k:
+ *   recompute[k*n+i] = d(one prefill entry, c = N, m = 0)          (refill cost)
+ *   swap[k*n+i]      = N * 2 * layers * NKV * H * e / xfer_bw       (K and V over the host link)
+ *   interval[k*n+i]  = recompute / N * M    (break-even interval t^N_recom M / N)
+ * xfer_bw in bytes/s (> 0), M > 0.  Any output pointer may be NULL. */
+int sim_kv_break_even(const sim_cost_model_t* cms, int32_t n_cms, const int64_t* N, int32_t n, double xfer_bw, int64_t M,
+                      double* recompute, double* swap, double* interval, int32_t device);
+
 const char* sim_strerror(int code);
 const char* sim_version(void);
 

@@ -78,6 +78,7 @@ __device__ __forceinline__ long long block_sum_ll(long long v, Scal& S) {
 
 #include "sim_step.cuh"
 #include "sim_warp.cuh"
+#include "sim_analytics.cuh"
 
 namespace simsweep {
 
@@ -221,6 +222,19 @@ int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* 
   return launches;
 }
 
+static int validate_cms(const sim_cost_model_t* cms, int32_t n_cms) {
+  if (!cms || n_cms <= 0) return SIM_EINVAL;
+  for (int k = 0; k < n_cms; k++) {
+    const sim_cost_model_t& m = cms[k];
+    if (m.mode != 0 && m.mode != 1) return SIM_ECOST;
+    if (m.layers < 1 || m.e < 1 || m.tp < 1 || m.H < 1) return SIM_ECOST;
+    if (m.mode == 1 && (m.h < 1 || m.f < 1 || m.NQ < 1 || m.NKV < 1 || !(m.flops > 0) || !(m.bw > 0) ||
+                        (m.tp > 1 && !(m.link_bw > 0))))
+      return SIM_ECOST;
+  }
+  return 0;
+}
+
 static int validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
                     const sim_cost_model_t* cms, int32_t n_cms) {
   if (!cfgs || !wls || !cms || n_cfgs <= 0 || n_wls <= 0 || n_cms <= 0) return SIM_EINVAL;
@@ -248,15 +262,7 @@ static int validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload
       if (multi[w] && W.T[i] != 0.0) return SIM_EWORKLOAD;
     }
   }
-  for (int k = 0; k < n_cms; k++) {
-    const sim_cost_model_t& m = cms[k];
-    if (m.mode != 0 && m.mode != 1) return SIM_ECOST;
-    if (m.layers < 1 || m.e < 1 || m.tp < 1) return SIM_ECOST;
-    if (m.mode == 1 && (m.h < 1 || m.f < 1 || m.H < 1 || m.NQ < 1 || m.NKV < 1 || !(m.flops > 0) || !(m.bw > 0) ||
-                        (m.tp > 1 && !(m.link_bw > 0))))
-      return SIM_ECOST;
-  }
-  return 0;
+  return validate_cms(cms, n_cms);
 }
 
 // longest-processing-time-first estimate of one simulation's step count from per-workload statistics
@@ -442,6 +448,88 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
   }
   rc |= check_cuda(cudaStreamSynchronize(s));
   return rc ? (rc < 0 ? rc : SIM_ECUDA) : 0;
+}
+
+}  // extern "C"
+
+// ---- cost-model analytics: host buffers in and out, one kernel each ----
+static bool shape_ok(int64_t n_p, int64_t c, int64_t m_p, int64_t n_d, int64_t m_d) {
+  if (n_p < 0 || n_d < 0 || n_p + n_d < 1 || m_p < 0 || m_d < 0 || (n_p > 0 && c < 1)) return false;
+  const double lim = 4.0e18;  // every feature sum below 2^62 (checked in floating point, no overflow)
+  const double P = (double)n_p, Cc = (double)c, Mp = (double)m_p;
+  return P * Cc * (Cc + Mp) < lim && P * Cc + (double)n_d < lim && (double)n_d * (double)m_d < lim && P * Mp < lim;
+}
+
+template <typename In, typename Out, typename Launch>
+static int run_analytics(const sim_cost_model_t* cms, int32_t n_cms, const In* in, int32_t n, Out** outs, int n_outs,
+                         int32_t device, Launch launch) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return SIM_ENODEV;
+  if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return SIM_ECUDA;
+  const size_t total = (size_t)n * n_cms;
+  sim_cost_model_t* d_cms = nullptr;
+  In* d_in = nullptr;
+  Out* d_out = nullptr;
+  int rc = 0;
+  rc |= check_cuda(cudaMalloc(&d_cms, sizeof(sim_cost_model_t) * n_cms));
+  rc |= check_cuda(cudaMalloc(&d_in, sizeof(In) * n));
+  rc |= check_cuda(cudaMalloc(&d_out, sizeof(Out) * total * n_outs));
+  if (!rc) rc |= check_cuda(cudaMemcpy(d_cms, cms, sizeof(sim_cost_model_t) * n_cms, cudaMemcpyHostToDevice));
+  if (!rc) rc |= check_cuda(cudaMemcpy(d_in, in, sizeof(In) * n, cudaMemcpyHostToDevice));
+  if (!rc) {
+    const int threads = 128, blocks = (int)std::min<size_t>((total + threads - 1) / threads, 148 * 16);
+    launch(blocks, threads, d_cms, d_in, d_out, total);
+    rc |= check_cuda(cudaGetLastError());
+  }
+  for (int o = 0; o < n_outs && !rc; o++)
+    if (outs[o]) rc |= check_cuda(cudaMemcpy(outs[o], d_out + o * total, sizeof(Out) * total, cudaMemcpyDeviceToHost));
+  cudaFree(d_cms);
+  cudaFree(d_in);
+  cudaFree(d_out);
+  return rc ? SIM_ECUDA : 0;
+}
+
+extern "C" {
+
+int sim_batch_times(const sim_cost_model_t* cms, int32_t n_cms, const sim_batch_shape_t* shapes, int32_t n,
+                    double* out, int32_t device) {
+  if (!shapes || !out || n <= 0) return SIM_EINVAL;
+  if (int rc = validate_cms(cms, n_cms)) return rc;
+  for (int i = 0; i < n; i++)
+    if (!shape_ok(shapes[i].n_p, shapes[i].c, shapes[i].m_p, shapes[i].n_d, shapes[i].m_d)) return SIM_EINVAL;
+  double* outs[1] = {out};
+  return run_analytics(cms, n_cms, shapes, n, outs, 1, device,
+                       [&](int b, int t, const sim_cost_model_t* dc, const sim_batch_shape_t* di, double* dout, size_t) {
+                         batch_times_kernel<<<b, t>>>(dc, n_cms, di, n, dout);
+                       });
+}
+
+int sim_slo_frontier(const sim_cost_model_t* cms, int32_t n_cms, const sim_slo_query_t* q, int32_t n, int64_t* out,
+                     int32_t device) {
+  if (!q || !out || n <= 0) return SIM_EINVAL;
+  if (int rc = validate_cms(cms, n_cms)) return rc;
+  for (int i = 0; i < n; i++)
+    if (q[i].m_max < 0 || !(q[i].tau > 0) || !shape_ok(q[i].n_p, q[i].c, q[i].m_max, q[i].n_d, q[i].m_max))
+      return SIM_EINVAL;
+  int64_t* outs[1] = {out};
+  return run_analytics(cms, n_cms, q, n, outs, 1, device,
+                       [&](int b, int t, const sim_cost_model_t* dc, const sim_slo_query_t* di, int64_t* dout, size_t) {
+                         slo_frontier_kernel<<<b, t>>>(dc, n_cms, di, n, reinterpret_cast<long long*>(dout));
+                       });
+}
+
+int sim_kv_break_even(const sim_cost_model_t* cms, int32_t n_cms, const int64_t* N, int32_t n, double xfer_bw, int64_t M,
+                      double* recompute, double* swap, double* interval, int32_t device) {
+  if (!N || n <= 0 || !(xfer_bw > 0) || M <= 0) return SIM_EINVAL;
+  if (int rc = validate_cms(cms, n_cms)) return rc;
+  for (int i = 0; i < n; i++)
+    if (N[i] < 1 || !shape_ok(1, N[i], 0, 0, 0)) return SIM_EINVAL;
+  double* outs[3] = {recompute, swap, interval};
+  return run_analytics(cms, n_cms, N, n, outs, 3, device,
+                       [&](int b, int t, const sim_cost_model_t* dc, const int64_t* di, double* dout, size_t total) {
+                         kv_break_even_kernel<<<b, t>>>(dc, n_cms, reinterpret_cast<const long long*>(di), n, xfer_bw,
+                                                        (long long)M, dout, dout + total, dout + 2 * total);
+                       });
 }
 
 }  // extern "C"

@@ -54,6 +54,16 @@ class SimResult(ctypes.Structure):
                 ("mean_tpot", ctypes.c_double * SIM_MAX_COST)]
 
 
+class SimBatchShape(ctypes.Structure):
+    _fields_ = [("n_p", ctypes.c_int64), ("c", ctypes.c_int64), ("m_p", ctypes.c_int64), ("n_d", ctypes.c_int64),
+                ("m_d", ctypes.c_int64)]
+
+
+class SimSloQuery(ctypes.Structure):
+    _fields_ = [("n_p", ctypes.c_int64), ("c", ctypes.c_int64), ("n_d", ctypes.c_int64), ("m_max", ctypes.c_int64),
+                ("tau", ctypes.c_double)]
+
+
 class SimRequestOut(ctypes.Structure):
     _fields_ = [("t_first", ctypes.c_void_p), ("t_done", ctypes.c_void_p), ("n_preempt", ctypes.c_void_p),
                 ("refill_tokens", ctypes.c_void_p)]
@@ -90,6 +100,16 @@ def lib() -> ctypes.CDLL:
         L.sim_request_rows.restype = ctypes.c_int
         L.sim_request_rows.argtypes = [P(SimConfig), ctypes.c_int32, P(SimWorkload), ctypes.c_int32,
                                        P(ctypes.c_int64), P(ctypes.c_int64)]
+        L.sim_batch_times.restype = ctypes.c_int
+        L.sim_batch_times.argtypes = [P(SimCostModel), ctypes.c_int32, P(SimBatchShape), ctypes.c_int32,
+                                      P(ctypes.c_double), ctypes.c_int32]
+        L.sim_slo_frontier.restype = ctypes.c_int
+        L.sim_slo_frontier.argtypes = [P(SimCostModel), ctypes.c_int32, P(SimSloQuery), ctypes.c_int32,
+                                       P(ctypes.c_int64), ctypes.c_int32]
+        L.sim_kv_break_even.restype = ctypes.c_int
+        L.sim_kv_break_even.argtypes = [P(SimCostModel), ctypes.c_int32, P(ctypes.c_int64), ctypes.c_int32,
+                                        ctypes.c_double, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_int32]
         L.sim_strerror.restype = ctypes.c_char_p
         L.sim_strerror.argtypes = [ctypes.c_int]
         L.sim_version.restype = ctypes.c_char_p
@@ -99,7 +119,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED_SYMBOLS = ["sim_sweep", "sim_sweep_device", "sim_workspace_bytes", "sim_request_rows", "sim_strerror",
-                    "sim_version"]
+                    "sim_version", "sim_batch_times", "sim_slo_frontier", "sim_kv_break_even"]
 
 
 def strerror(code: int) -> str:
@@ -318,3 +338,40 @@ def lpt_order(cfgs, wls) -> np.ndarray:
         Meff = float(max(c.M, 1)) if c.M >= 0 else 1e18
         est.append(O.max() + float(((I + 0.5 * O) * O).sum()) / Meff + float(I.sum()) / float(c.C))
     return np.argsort(-np.asarray(est), kind="stable").astype(np.int32)
+
+
+# ------------------------------------------------------------ cost-model analytics
+def sim_batch_times(cms, shapes, device: int = -1) -> np.ndarray:
+    """Batch time of every shape (n_p, c, m_p, n_d, m_d) under every model: float64 [len(cms), len(shapes)].
+    `shapes` is any [n, 5] integer array-like (an int64 [n, 5] array is passed without copying)."""
+    cms = list(cms)
+    arr = np.ascontiguousarray(np.asarray(shapes, np.int64).reshape(-1, 5))  # == sim_batch_shape_t[n]
+    n = arr.shape[0]
+    out = np.zeros(len(cms) * n, np.float64)
+    _check(lib().sim_batch_times(_cm_array(cms), len(cms), arr.ctypes.data_as(ctypes.POINTER(SimBatchShape)), n,
+                                 out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(device)))
+    return out.reshape(len(cms), n)
+
+
+def sim_slo_frontier(cms, queries, device: int = -1) -> np.ndarray:
+    """Largest m with batch time <= tau for every query (n_p, c, n_d, m_max, tau) and model (-1: none):
+    int64 [len(cms), len(queries)]."""
+    cms = list(cms)
+    arr = (SimSloQuery * len(queries))()
+    for i, (n_p, c, n_d, m_max, tau) in enumerate(queries):
+        arr[i].n_p, arr[i].c, arr[i].n_d, arr[i].m_max, arr[i].tau = int(n_p), int(c), int(n_d), int(m_max), float(tau)
+    out = np.zeros(len(cms) * len(queries), np.int64)
+    _check(lib().sim_slo_frontier(_cm_array(cms), len(cms), arr, len(queries),
+                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(device)))
+    return out.reshape(len(cms), len(queries))
+
+
+def sim_kv_break_even(cms, N, xfer_bw: float, M: int, device: int = -1):
+    """-> (recompute, swap, interval), each float64 [len(cms), len(N)] (seconds)."""
+    cms = list(cms)
+    Nn = np.ascontiguousarray(N, np.int64)
+    outs = [np.zeros(len(cms) * len(Nn), np.float64) for _ in range(3)]
+    _check(lib().sim_kv_break_even(_cm_array(cms), len(cms), Nn.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                   len(Nn), float(xfer_bw), int(M), outs[0].ctypes.data, outs[1].ctypes.data,
+                                   outs[2].ctypes.data, int(device)))
+    return tuple(o.reshape(len(cms), len(Nn)) for o in outs)

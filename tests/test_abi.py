@@ -43,6 +43,7 @@ def test_struct_layout_matches_header(tmp_path):
                    'sizeof(sim_workload_t), sizeof(sim_cost_model_t), sizeof(sim_result_t), '
                    'sizeof(sim_request_out_t), offsetof(sim_config_t, n_cost), offsetof(sim_result_t, makespan));'
                    'printf("%zu\\n", offsetof(sim_config_t, reserve));'
+                   'printf("%zu %zu %zu\\n", sizeof(sim_batch_shape_t), sizeof(sim_slo_query_t), offsetof(sim_slo_query_t, tau));'
                    'return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
@@ -50,7 +51,8 @@ def test_struct_layout_matches_header(tmp_path):
     want = [ctypes.sizeof(simsweep.SimConfig), ctypes.sizeof(simsweep.SimWorkload),
             ctypes.sizeof(simsweep.SimCostModel), ctypes.sizeof(simsweep.SimResult),
             ctypes.sizeof(simsweep.SimRequestOut), simsweep.SimConfig.n_cost.offset,
-            simsweep.SimResult.makespan.offset, simsweep.SimConfig.reserve.offset]
+            simsweep.SimResult.makespan.offset, simsweep.SimConfig.reserve.offset,
+            ctypes.sizeof(simsweep.SimBatchShape), ctypes.sizeof(simsweep.SimSloQuery), simsweep.SimSloQuery.tau.offset]
     assert got == want
     assert got[0] == 72
 
@@ -84,6 +86,12 @@ def test_no_gpu_fails_loudly(L):
     wl = workloads.fixed(2, 2, 4)
     with pytest.raises(simsweep.SimError, match="no sm_100"):
         simsweep.sim_sweep([simsweep.preset_config("vllm", 100)], [wl], [simsweep.unit_cost()])
+    with pytest.raises(simsweep.SimError, match="no sm_100"):
+        simsweep.sim_batch_times([simsweep.unit_cost()], [(1, 1, 0, 0, 0)])
+    with pytest.raises(simsweep.SimError, match="no sm_100"):
+        simsweep.sim_slo_frontier([simsweep.unit_cost()], [(1, 1, 1, 10, 1.0)])
+    with pytest.raises(simsweep.SimError, match="no sm_100"):
+        simsweep.sim_kv_break_even([simsweep.unit_cost()], [4], 64e9, 100)
 
 
 def test_invalid_calls_rejected_before_device(L):
@@ -98,6 +106,12 @@ def test_invalid_calls_rejected_before_device(L):
         simsweep.sim_sweep([simsweep.preset_config("vllm", 100)], [wl2], [simsweep.unit_cost()])
     with pytest.raises(simsweep.SimError, match="cost"):
         simsweep.sim_sweep([simsweep.preset_config("vllm", 100, cost=(3,))], [wl], [simsweep.unit_cost()])
+    with pytest.raises(simsweep.SimError, match="invalid argument"):  # analytics: shapes checked on the host
+        simsweep.sim_batch_times([simsweep.unit_cost()], [(0, 1, 0, 0, 0)])
+    bad_cm = simsweep.unit_cost()
+    bad_cm.mode = 7
+    with pytest.raises(simsweep.SimError, match="cost"):
+        simsweep.sim_slo_frontier([bad_cm], [(1, 1, 1, 10, 1.0)])
 
 
 def test_workspace_bytes_host_query(L):
