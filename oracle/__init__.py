@@ -13,6 +13,9 @@ Parity status per function:
   oracle_batch_time     pinned: Eq. (1) SPEC example, matmul example,
                         intensity limits 128 / ~2, hand sums
   oracle_hist_predict   pinned: hand-computed histogram examples (Q31)
+  oracle_optimum        pinned: single-request and no-contention closed forms, the full reachable-state
+                        count, Example A by hand (6 batches vs 8 preemption-free), and the lower bound
+                        it must be for every simulated preset (tests/test_oracle_optimum.py)
 """
 from __future__ import annotations
 
@@ -236,6 +239,28 @@ def matmul_cost(c, n_in, n_out):
     f, r = ctypes.c_int64(), ctypes.c_int64()
     lib().oracle_matmul_cost(c, n_in, n_out, ctypes.byref(f), ctypes.byref(r))
     return f.value, r.value
+
+
+class OracleOpt(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("pad", ctypes.c_int32), ("states", ctypes.c_int64),
+                ("optimum", ctypes.c_double)]
+
+
+def optimum(I, O, C: int, M: int, cost: OracleCost):
+    """Exact CSP optimum (Dijkstra): -> (status 'ok' | 'unreachable', reachable states, min sum_j d_j)."""
+    Ia = np.ascontiguousarray(I, np.int32)
+    Oa = np.ascontiguousarray(O, np.int32)
+    out = OracleOpt()
+    L = lib()
+    L.oracle_optimum.restype = ctypes.c_int
+    L.oracle_optimum.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                 ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(OracleCost), ctypes.POINTER(OracleOpt)]
+    rc = L.oracle_optimum(len(Ia), Ia.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                          Oa.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), int(C), int(M), ctypes.byref(cost),
+                          ctypes.byref(out))
+    if rc < 0:
+        raise ValueError(f"oracle_optimum call error {rc}")
+    return ("ok" if out.status == 0 else "unreachable"), int(out.states), float(out.optimum)
 
 
 def hist_predict(hist: np.ndarray, I: int) -> int:

@@ -10,6 +10,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
+#include <map>
+#include <queue>
 #include <vector>
 
 namespace {
@@ -537,6 +540,111 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
     n_preempt[i] = R[i].n_preempt;
     refill_tokens[i] = R[i].refill;
   }
+  return 0;
+}
+
+// ---- exact optimum of the CSP (Sec. "Optimal Scheduling as Constraint Satisfaction Problem") ----
+// One request's state after batch j: done, or (g = tokens generated, m = KVs cached, filled).  Batch j chooses for
+// every unfinished request either e = 1 (preempt: m := 0, Eq. (4)) or c in [0, s - m] with s = I + g (Eq. (5)); it
+// generates a token iff c = s - m (Eq. (6)), s grows by that token, and the batch respects sum c <= C and
+// sum m <= M after processing (Eq. (7)).  A request that generated its O-th token is done and holds nothing from
+// the next batch on (Q14, Q44).  The objective is sum_j d_j with the batch cost model; an entry is
+// a prefill unless the request is filled (its last (re)fill completed, Q17, Q45).  Batches with sum c = 0 are
+// excluded (they cost time and change nothing but could be merged, Q43).  Dijkstra from the all-empty state.
+struct OptReq {
+  int64_t g, m;
+  bool filled, done;
+};
+
+int oracle_optimum(int32_t n, const int32_t* I, const int32_t* O, int64_t C, int64_t M, const oracle_cost_t* cm,
+                   oracle_opt_t* out) {
+  if (n < 1 || !I || !O || !cm || !out || C < 1 || M < 0) return -1;
+  for (int i = 0; i < n; i++)
+    if (I[i] < 1 || O[i] < 1) return -5;
+  using State = std::vector<OptReq>;
+  auto key = [&](const State& st) {
+    std::vector<int64_t> k;
+    for (const OptReq& r : st) {
+      k.push_back(r.done ? -1 : 2 * r.g + (r.filled ? 1 : 0));
+      k.push_back(r.done ? 0 : r.m);
+    }
+    return k;
+  };
+  std::map<std::vector<int64_t>, double> dist;
+  std::map<std::vector<int64_t>, bool> settled;
+  using Item = std::pair<double, std::vector<int64_t>>;
+  std::priority_queue<Item, std::vector<Item>, std::greater<Item>> pq;
+  std::map<std::vector<int64_t>, State> states;
+  State start(n);
+  for (int i = 0; i < n; i++) start[i] = OptReq{0, 0, false, false};
+  dist[key(start)] = 0.0;
+  states[key(start)] = start;
+  pq.push(Item(0.0, key(start)));
+  int64_t n_settled = 0;
+  double best = -1.0;
+  while (!pq.empty()) {
+    const Item top = pq.top();
+    pq.pop();
+    if (settled[top.second]) continue;
+    settled[top.second] = true;
+    n_settled++;
+    const State u = states[top.second];
+    const double du = top.first;
+    bool all_done = true;
+    for (const OptReq& r : u) all_done = all_done && r.done;
+    if (all_done) {
+      best = du;
+      continue;
+    }
+    // every batch: each unfinished request picks idle, preempt (m > 0) or a c >= 1; recursion over requests
+    State v(n);
+    std::vector<Entry> B;
+    std::function<void(int, int64_t, int64_t)> rec = [&](int i, int64_t sum_c, int64_t sum_m) {
+      if (sum_c > C || sum_m > M) return;  // Eq. (7); both sums only grow with i
+      if (i == n) {
+        if (sum_c == 0) return;
+        const double w = batch_time(*cm, B);
+        const double cand = du + w;
+        const std::vector<int64_t> kv = key(v);
+        auto it = dist.find(kv);
+        if (it == dist.end() || cand < it->second) {
+          dist[kv] = cand;
+          states[kv] = v;
+          pq.push(Item(cand, kv));
+        }
+        return;
+      }
+      const OptReq& r = u[i];
+      if (r.done) {
+        v[i] = r;
+        rec(i + 1, sum_c, sum_m);
+        return;
+      }
+      const int64_t s = I[i] + r.g;
+      v[i] = r;  // idle: c = 0, e = 0
+      rec(i + 1, sum_c, sum_m + r.m);
+      if (r.m > 0) {  // preempt: e = 1, m := 0, c = 0 (Eq. (4)-(5))
+        v[i] = OptReq{r.g, 0, false, false};
+        rec(i + 1, sum_c, sum_m);
+      }
+      for (int64_t c = 1; c <= s - r.m; c++) {
+        const bool token = c == s - r.m;  // Eq. (6)
+        const int64_t m2 = r.m + c;
+        if (token)
+          v[i] = (r.g + 1 == O[i]) ? OptReq{r.g + 1, 0, true, true} : OptReq{r.g + 1, m2, true, false};
+        else
+          v[i] = OptReq{r.g, m2, false, false};
+        B.push_back(Entry{i, c, r.m, r.filled ? PH_DECODE : PH_PREFILL});
+        rec(i + 1, sum_c + c, sum_m + m2);  // a request finishing in this batch still holds m2 now (Q44)
+        B.pop_back();
+      }
+    };
+    rec(0, 0, 0);
+  }
+  out->status = best < 0.0 ? 1 : 0;
+  out->pad = 0;
+  out->states = n_settled;
+  out->optimum = best < 0.0 ? 0.0 : best;
   return 0;
 }
 

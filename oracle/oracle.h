@@ -71,6 +71,18 @@ void oracle_matmul_cost(int64_t c, int64_t in, int64_t out, int64_t* flops, int6
 /* SRF+Hist output-length prediction from an 18x18 histogram (reading Q31). */
 int64_t oracle_hist_predict(const int32_t* hist, int64_t I);
 
+/* Exact optimum of the paper's CSP for a tiny offline workload, by Dijkstra over every
+ * reachable schedule state (readings Q43-Q45).  status 0 = optimum found, 1 = the
+ * all-done state is unreachable (some I+O-1 > M).  states = number of reachable states (all are settled). */
+typedef struct {
+  int32_t status;
+  int32_t pad;
+  int64_t states;
+  double optimum; /* min over schedules of sum_j d_j (seconds) */
+} oracle_opt_t;
+int oracle_optimum(int32_t n, const int32_t* I, const int32_t* O, int64_t C, int64_t M, const oracle_cost_t* cm,
+                   oracle_opt_t* out);
+
 #ifdef __cplusplus
 }
 #endif
