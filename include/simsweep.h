@@ -227,6 +227,35 @@ int sim_slo_frontier(const sim_cost_model_t* cms, int32_t n_cms, const sim_slo_q
 int sim_kv_break_even(const sim_cost_model_t* cms, int32_t n_cms, const int64_t* N, int32_t n, double xfer_bw, int64_t M,
                       double* recompute, double* swap, double* interval, int32_t device);
 
+/* ---- Exact optimum of the paper's CSP ----
+ * A tiny offline workload of n <= SIM_OPT_MAX_N requests.  Every batch j chooses for each unfinished request
+ * either preemption (e = 1: m := 0, Eq. (4)) or c in [0, s - m] (Eq. (5)); a token is generated iff
+ * c = s - m (Eq. (6)); sum c <= C and sum m <= M after processing (Eq. (7)); a finished request holds its KVs
+ * until the end of the batch that finished it.  The objective is sum_j d_j under the cost model (entries are
+ * prefills unless the request's last (re)fill completed).  Batches with sum c = 0 are not considered (a
+ * preemption can always ride with the next batch; readings Q43-Q45).  Solved exactly on the GPU by parallel
+ * relaxation rounds over the dense state space (every reachable state, fp64 path sums), so the result is the
+ * minimum over ALL schedules: a lower bound for every simulated preset. */
+#define SIM_OPT_MAX_N 4
+typedef struct {
+  int32_t n;                   /* requests, 1..SIM_OPT_MAX_N */
+  int32_t I[SIM_OPT_MAX_N];    /* >= 1 */
+  int32_t O[SIM_OPT_MAX_N];    /* >= 1 */
+  int32_t pad;
+  int64_t C;                   /* token limit per batch, >= 1 */
+  int64_t M;                   /* KV limit per batch, >= 0 (finite) */
+} sim_opt_problem_t;
+typedef struct {
+  int32_t status;  /* 0 ok, 1 unreachable (some I + O - 1 > M), 2 state space too large (> 2^25 states) */
+  int32_t rounds;  /* relaxation rounds until no state improved */
+  int64_t states;  /* reachable states */
+  double optimum;  /* min over schedules of sum_j d_j (seconds); 0 unless status 0 */
+} sim_opt_result_t;
+/* Solves n_probs problems in turn under cost model cm on CUDA device `device` (current if < 0).  HOST buffers;
+ * blocking; returns 0 / SIM_E* (SIM_EINVAL on a bad problem, SIM_ECOST on a bad model). */
+int sim_optimum(const sim_opt_problem_t* probs, int32_t n_probs, const sim_cost_model_t* cm, sim_opt_result_t* out,
+                int32_t device);
+
 const char* sim_strerror(int code);
 const char* sim_version(void);
 

@@ -79,6 +79,7 @@ __device__ __forceinline__ long long block_sum_ll(long long v, Scal& S) {
 #include "sim_step.cuh"
 #include "sim_warp.cuh"
 #include "sim_analytics.cuh"
+#include "sim_optimum.cuh"
 
 namespace simsweep {
 
@@ -530,6 +531,123 @@ int sim_kv_break_even(const sim_cost_model_t* cms, int32_t n_cms, const int64_t*
                          kv_break_even_kernel<<<b, t>>>(dc, n_cms, reinterpret_cast<const long long*>(di), n, xfer_bw,
                                                         (long long)M, dout, dout + total, dout + 2 * total);
                        });
+}
+
+}  // extern "C"
+
+namespace simsweep {
+__global__ void opt_fill_kernel(unsigned long long* dist, unsigned char* cur, unsigned char* nxt, long long n) {
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n; x += (long long)gridDim.x * blockDim.x)
+    dist[x] = OPT_INF, cur[x] = 0, nxt[x] = 0;
+}
+}  // namespace simsweep
+
+extern "C" {
+
+int sim_optimum(const sim_opt_problem_t* probs, int32_t n_probs, const sim_cost_model_t* cm, sim_opt_result_t* out,
+                int32_t device) {
+  if (!probs || !out || n_probs <= 0) return SIM_EINVAL;
+  if (int rc = validate_cms(cm, 1)) return rc;
+  constexpr long long MAX_STATES = 1ll << 25;
+  std::vector<OptDev> P(n_probs);
+  std::vector<long long> nst(n_probs);
+  long long cap = 0;
+  for (int q = 0; q < n_probs; q++) {
+    const sim_opt_problem_t& pr = probs[q];
+    if (pr.n < 1 || pr.n > OPT_MAXN || pr.C < 1 || pr.M < 0) return SIM_EINVAL;
+    OptDev& d = P[q];
+    memset(&d, 0, sizeof(d));
+    d.n = pr.n, d.C = pr.C, d.M = pr.M;
+    long long total = 1;
+    for (int i = 0; i < pr.n; i++) {
+      if (pr.I[i] < 1 || pr.O[i] < 1 || pr.O[i] > OPT_MAXO || pr.I[i] > (1 << 20)) return SIM_EINVAL;
+      d.I[i] = pr.I[i], d.O[i] = pr.O[i];
+      long long b = 1;  // local id 0 = done; block g holds the I+g unfilled states (+ the filled one for g >= 1)
+      for (int g = 0; g < pr.O[i]; g++) {
+        d.base[i][g] = (int)b;
+        b += pr.I[i] + g + (g >= 1 ? 1 : 0);
+        if (b > MAX_STATES) break;
+      }
+      d.base[i][pr.O[i]] = (int)std::min<long long>(b, MAX_STATES + 1);
+      d.ns[i] = b;
+      d.stride[i] = total;
+      total = (total > MAX_STATES || b > MAX_STATES) ? MAX_STATES + 1 : total * b;
+    }
+    nst[q] = total;
+    if (total <= MAX_STATES) cap = std::max(cap, total);
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return SIM_ENODEV;
+  if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return SIM_ECUDA;
+  unsigned long long* dist = nullptr;
+  unsigned char *cur = nullptr, *nxt = nullptr;
+  int* changed = nullptr;
+  long long* reached = nullptr;
+  int rc = 0;
+  if (cap > 0) {
+    rc |= check_cuda(cudaMalloc(&dist, 8 * (size_t)cap));
+    rc |= check_cuda(cudaMalloc(&cur, (size_t)cap));
+    rc |= check_cuda(cudaMalloc(&nxt, (size_t)cap));
+  }
+  rc |= check_cuda(cudaMalloc(&changed, sizeof(int)));
+  rc |= check_cuda(cudaMalloc(&reached, sizeof(long long)));
+  for (int q = 0; q < n_probs && !rc; q++) {
+    sim_opt_result_t& r = out[q];
+    memset(&r, 0, sizeof(r));
+    const OptDev& d = P[q];
+    long long peak = 0;
+    for (int i = 0; i < d.n; i++) peak = std::max<long long>(peak, (long long)d.I[i] + d.O[i] - 1);
+    if (nst[q] > MAX_STATES) {
+      r.status = 2;
+      continue;
+    }
+    if (peak > d.M) {  // that request can never hold its last KVs (Eq. (7))
+      r.status = 1;
+      continue;
+    }
+    const long long ns = nst[q];
+    const int threads = 256, blocks = (int)std::min<long long>((ns + threads - 1) / threads, 148 * 16);
+    opt_fill_kernel<<<blocks, threads>>>(dist, cur, nxt, ns);
+    long long start = 0;
+    for (int i = 0; i < d.n; i++) start += d.stride[i];  // every request at (g = 0, m = 0): local id 1
+    const unsigned long long zero = 0ull;
+    const unsigned char one = 1;
+    const long long one_ll = 1;
+    rc |= check_cuda(cudaMemcpy(dist + start, &zero, 8, cudaMemcpyHostToDevice));
+    rc |= check_cuda(cudaMemcpy(cur + start, &one, 1, cudaMemcpyHostToDevice));
+    rc |= check_cuda(cudaMemcpy(reached, &one_ll, 8, cudaMemcpyHostToDevice));
+    int rounds = 0;
+    unsigned char *a = cur, *b = nxt;
+    while (!rc) {
+      rc |= check_cuda(cudaMemset(changed, 0, sizeof(int)));
+      opt_round_kernel<<<blocks, threads>>>(d, *cm, dist, a, b, ns, changed, reached);
+      rc |= check_cuda(cudaGetLastError());
+      int h = 0;
+      rc |= check_cuda(cudaMemcpy(&h, changed, sizeof(int), cudaMemcpyDeviceToHost));
+      rounds++;
+      if (!h) break;
+      std::swap(a, b);  // the processed flags were all cleared: the old frontier array is the next one
+    }
+    unsigned long long goal = OPT_INF;
+    long long nreach = 0;
+    rc |= check_cuda(cudaMemcpy(&goal, dist, 8, cudaMemcpyDeviceToHost));  // state 0 = every request done
+    rc |= check_cuda(cudaMemcpy(&nreach, reached, 8, cudaMemcpyDeviceToHost));
+    r.rounds = rounds;
+    r.states = nreach;
+    if (goal == OPT_INF) {
+      r.status = 1;
+    } else {
+      double v;
+      memcpy(&v, &goal, 8);
+      r.optimum = v;
+    }
+  }
+  cudaFree(dist);
+  cudaFree(cur);
+  cudaFree(nxt);
+  cudaFree(changed);
+  cudaFree(reached);
+  return rc ? SIM_ECUDA : 0;
 }
 
 }  // extern "C"

@@ -64,6 +64,19 @@ class SimSloQuery(ctypes.Structure):
                 ("tau", ctypes.c_double)]
 
 
+SIM_OPT_MAX_N = 4
+
+
+class SimOptProblem(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("I", ctypes.c_int32 * SIM_OPT_MAX_N), ("O", ctypes.c_int32 * SIM_OPT_MAX_N),
+                ("pad", ctypes.c_int32), ("C", ctypes.c_int64), ("M", ctypes.c_int64)]
+
+
+class SimOptResult(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("rounds", ctypes.c_int32), ("states", ctypes.c_int64),
+                ("optimum", ctypes.c_double)]
+
+
 class SimRequestOut(ctypes.Structure):
     _fields_ = [("t_first", ctypes.c_void_p), ("t_done", ctypes.c_void_p), ("n_preempt", ctypes.c_void_p),
                 ("refill_tokens", ctypes.c_void_p)]
@@ -110,6 +123,8 @@ def lib() -> ctypes.CDLL:
         L.sim_kv_break_even.argtypes = [P(SimCostModel), ctypes.c_int32, P(ctypes.c_int64), ctypes.c_int32,
                                         ctypes.c_double, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_int32]
+        L.sim_optimum.restype = ctypes.c_int
+        L.sim_optimum.argtypes = [P(SimOptProblem), ctypes.c_int32, P(SimCostModel), P(SimOptResult), ctypes.c_int32]
         L.sim_strerror.restype = ctypes.c_char_p
         L.sim_strerror.argtypes = [ctypes.c_int]
         L.sim_version.restype = ctypes.c_char_p
@@ -119,7 +134,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED_SYMBOLS = ["sim_sweep", "sim_sweep_device", "sim_workspace_bytes", "sim_request_rows", "sim_strerror",
-                    "sim_version", "sim_batch_times", "sim_slo_frontier", "sim_kv_break_even"]
+                    "sim_version", "sim_batch_times", "sim_slo_frontier", "sim_kv_break_even", "sim_optimum"]
 
 
 def strerror(code: int) -> str:
@@ -375,3 +390,21 @@ def sim_kv_break_even(cms, N, xfer_bw: float, M: int, device: int = -1):
                                    len(Nn), float(xfer_bw), int(M), outs[0].ctypes.data, outs[1].ctypes.data,
                                    outs[2].ctypes.data, int(device)))
     return tuple(o.reshape(len(cms), len(Nn)) for o in outs)
+
+
+# ------------------------------------------------------------ exact CSP optimum
+OPT_STATUS = {0: "ok", 1: "unreachable", 2: "too_large"}
+
+
+def sim_optimum(problems, cm: SimCostModel, device: int = -1):
+    """problems: [(I list, O list, C, M)] -> [(status, rounds, reachable states, optimum seconds)]."""
+    arr = (SimOptProblem * len(problems))()
+    for q, (I, O, C, M) in enumerate(problems):
+        assert 1 <= len(I) == len(O) <= SIM_OPT_MAX_N
+        arr[q].n = len(I)
+        for i, (a, b) in enumerate(zip(I, O)):
+            arr[q].I[i], arr[q].O[i] = int(a), int(b)
+        arr[q].C, arr[q].M = int(C), int(M)
+    out = (SimOptResult * len(problems))()
+    _check(lib().sim_optimum(arr, len(problems), ctypes.byref(cm), out, int(device)))
+    return [(OPT_STATUS[r.status], int(r.rounds), int(r.states), float(r.optimum)) for r in out]

@@ -44,6 +44,7 @@ def test_struct_layout_matches_header(tmp_path):
                    'sizeof(sim_request_out_t), offsetof(sim_config_t, n_cost), offsetof(sim_result_t, makespan));'
                    'printf("%zu\\n", offsetof(sim_config_t, reserve));'
                    'printf("%zu %zu %zu\\n", sizeof(sim_batch_shape_t), sizeof(sim_slo_query_t), offsetof(sim_slo_query_t, tau));'
+                   'printf("%zu %zu %zu\\n", sizeof(sim_opt_problem_t), offsetof(sim_opt_problem_t, C), sizeof(sim_opt_result_t));'
                    'return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
@@ -52,7 +53,8 @@ def test_struct_layout_matches_header(tmp_path):
             ctypes.sizeof(simsweep.SimCostModel), ctypes.sizeof(simsweep.SimResult),
             ctypes.sizeof(simsweep.SimRequestOut), simsweep.SimConfig.n_cost.offset,
             simsweep.SimResult.makespan.offset, simsweep.SimConfig.reserve.offset,
-            ctypes.sizeof(simsweep.SimBatchShape), ctypes.sizeof(simsweep.SimSloQuery), simsweep.SimSloQuery.tau.offset]
+            ctypes.sizeof(simsweep.SimBatchShape), ctypes.sizeof(simsweep.SimSloQuery), simsweep.SimSloQuery.tau.offset,
+            ctypes.sizeof(simsweep.SimOptProblem), simsweep.SimOptProblem.C.offset, ctypes.sizeof(simsweep.SimOptResult)]
     assert got == want
     assert got[0] == 72
 
@@ -92,6 +94,8 @@ def test_no_gpu_fails_loudly(L):
         simsweep.sim_slo_frontier([simsweep.unit_cost()], [(1, 1, 1, 10, 1.0)])
     with pytest.raises(simsweep.SimError, match="no sm_100"):
         simsweep.sim_kv_break_even([simsweep.unit_cost()], [4], 64e9, 100)
+    with pytest.raises(simsweep.SimError, match="no sm_100"):
+        simsweep.sim_optimum([([2, 2], [4, 4], 4096, 6)], simsweep.unit_cost())
 
 
 def test_invalid_calls_rejected_before_device(L):
@@ -112,6 +116,8 @@ def test_invalid_calls_rejected_before_device(L):
     bad_cm.mode = 7
     with pytest.raises(simsweep.SimError, match="cost"):
         simsweep.sim_slo_frontier([bad_cm], [(1, 1, 1, 10, 1.0)])
+    with pytest.raises(simsweep.SimError, match="invalid argument"):  # the optimum: C >= 1
+        simsweep.sim_optimum([([2], [2], 0, 6)], simsweep.unit_cost())
 
 
 def test_workspace_bytes_host_query(L):
