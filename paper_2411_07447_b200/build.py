@@ -8,7 +8,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "simsweep.cu")]
-HDRS = [os.path.join(PKG, "csrc", h) for h in ("sim_kernel.cuh", "sim_step.cuh", "sim_warp.cuh", "sim_analytics.cuh", "sim_optimum.cuh")]
+HDRS = [os.path.join(PKG, "csrc", h) for h in ("sim_kernel.cuh", "sim_step.cuh", "sim_analytics.cuh", "sim_optimum.cuh")]
 DEPS = SRC + HDRS + [os.path.join(ROOT, "include", "simsweep.h")]
 LIB = os.path.join(PKG, "libsimsweep.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -28,12 +28,9 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-WARP_LIB = LIB.replace(".so", "_warp.so")
-
-
 def build(force: bool = False, verbose: bool = False, profile: bool = False, defines=(), lib=None) -> str:
-    """profile=True builds libsimsweep_prof.so with per-phase cycle counters (tools/probe.py); lib=WARP_LIB with
-    defines=("SIM_WARP_SMALL",) builds the opt-in warp-per-simulation variant for W <= 1024."""
+    """profile=True builds libsimsweep_prof.so with per-phase cycle counters (tools/probe.py); `lib` and
+    `defines` build comparison variants (e.g. -DSIM_NT_SMALL=128) under another name."""
     lib = lib or (LIB.replace(".so", "_prof.so") if profile else LIB)
     if force or profile or lib != LIB or needs_build():
         cmd = ([NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + (["-DSIMSWEEP_PROFILE"] if profile else []) + ["-D" + d for d in defines]

@@ -77,7 +77,6 @@ __device__ __forceinline__ long long block_sum_ll(long long v, Scal& S) {
 }  // namespace simsweep
 
 #include "sim_step.cuh"
-#include "sim_warp.cuh"
 #include "sim_analytics.cuh"
 #include "sim_optimum.cuh"
 
@@ -91,22 +90,13 @@ struct Variant {
   void (*fn)(KParams);
 };
 
-template <int CAP>
-Variant make_warp_variant() {  // one warp per simulation (sim_warp.cuh)
-  return Variant{32, CAP, WLayout<CAP>::bytes, 0, sim_warp_kernel<CAP>};
-}
-
 template <int NT, int CAP, int IPT_, bool GM>
 Variant make_variant() {
   using L = Smem<NT, CAP>;
   return Variant{NT, CAP, GM ? L::scal : L::bytes, GM ? L::arr_bytes : 0, sim_kernel<NT, CAP, IPT_, GM>};
 }
 
-#ifdef SIM_WARP_SMALL  // opt-in: the warp-per-simulation kernel for W <= 1024 (sim_warp.cuh)
-static Variant g_variants[N_VARIANTS] = {make_warp_variant<1024>(),
-#else
 static Variant g_variants[N_VARIANTS] = {make_variant<SIM_NT_SMALL, 1024, SIM_IPT_SMALL, false>(),
-#endif
                                          make_variant<512, 4096, 4, false>(), make_variant<512, SIM_MAX_WINDOW, 4, true>()};
 
 static int64_t workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int32_t* wls_n) {
