@@ -48,11 +48,16 @@ enum {
   SIM_RESERVE_PEAK = 1,   /* I + O - 1: the *^pf schedulers */
   SIM_RESERVE_CONTEXT = 2 /* S: Orca */
 };
+/* alternative readings (sim_config_t.knobs bits) */
+enum {
+  SIM_KNOB_HOL = 1 /* Q10 alternative: the first waiting candidate that is not admitted ends the visit of R_w for
+                      this step (vLLM's head-of-line blocking; a rank order skips the later waiting candidates) */
+};
 /* per-simulation status */
 enum {
   SIM_S_OK = 0,
   SIM_S_TOO_LONG = 1,   /* some request has I+O-1 > S */
-  SIM_S_NEVER_FITS = 2, /* I+O-1 > M, or > C without chunked prefill (reading Q35) */
+  SIM_S_NEVER_FITS = 2, /* I+O-1 (+ kv_watermark) > M, or > C without chunked prefill (reading Q35) */
   SIM_S_MAX_STEPS = 3,  /* more than max_steps batches */
   SIM_S_DEADLOCK = 4,   /* B empty, nothing arriving, requests unfinished (defensive) */
   SIM_S_CAPACITY = 5    /* more than SIM_MAX_WINDOW arrived-but-unfinished requests (only if n > SIM_MAX_WINDOW) */
@@ -60,7 +65,8 @@ enum {
 /* call-level errors */
 enum {
   SIM_EINVAL = -1,    /* NULL pointer, n <= 0, bad enum, C not in [1, 2^30], M > 2^30, S not in [1, 2^18), n_cost not 1..4,
-                         replacement == SIM_PF without a PEAK / CONTEXT reserve or vice versa */
+                         replacement == SIM_PF without a PEAK / CONTEXT reserve or vice versa, unknown knob bits,
+                         max_seqs < 0, kv_watermark not in [0, 2^30) */
   SIM_EWORKLOAD = -2, /* I < 1, O < 1, T not sorted, or T != 0 with n_cost > 1 */
   SIM_ECOST = -3,     /* cost-model index out of range or bad cost-model fields */
   SIM_ECUDA = -4,     /* a CUDA runtime error (device, allocation, launch) */
@@ -74,7 +80,7 @@ enum {
  * larger ones use a per-simulation arena of the caller's workspace. */
 #define SIM_MAX_WINDOW 32768
 
-/* One simulation.  72 bytes, naturally aligned. */
+/* One simulation.  88 bytes, naturally aligned. */
 typedef struct {
   int32_t order;       /* SIM_ORDER_* */
   int32_t hybrid;      /* 0/1: hybrid prefill+decode batches (step 2) */
@@ -88,6 +94,9 @@ typedef struct {
   int32_t n_cost;      /* 1..4 cost models charged on the same schedule; > 1 only for offline (all T = 0) */
   int32_t cost[SIM_MAX_COST]; /* indices into the cost-model table; the clock of cost[0] drives arrivals */
   int32_t reserve;     /* SIM_RESERVE_*; != SEQ iff replacement == SIM_PF */
+  int32_t knobs;       /* SIM_KNOB_* bits: alternative readings (0 = the frozen semantics) */
+  int32_t max_seqs;    /* Q16 alternative: at most this many entries per batch, like vLLM's max_num_seqs (0 = no cap) */
+  int64_t kv_watermark;/* Q16 alternative: KVs a waiting admission must leave free, like vLLM's watermark (0 = none) */
 } sim_config_t;
 
 /* One workload: n requests sorted by (T, id).  The pointers are HOST memory

@@ -232,6 +232,7 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
   if (cfg->replacement < OR_NRF || cfg->replacement > OR_PF) return -2;
   if (cfg->reserve < OR_RESERVE_SEQ || cfg->reserve > OR_RESERVE_CONTEXT) return -2;
   if ((cfg->replacement == OR_PF) != (cfg->reserve != OR_RESERVE_SEQ)) return -2;  // Q39
+  if ((cfg->knobs & ~OR_KNOB_HOL) || cfg->max_seqs < 0 || cfg->kv_watermark < 0) return -2;
   if (cfg->n_cost < 1 || cfg->n_cost > 4) return -3;
   if (cfg->C < 1 || cfg->S < 1 || cfg->max_steps < 1) return -4;
   for (int i = 0; i < n; i++) {
@@ -262,11 +263,13 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
       out->status = OR_TOO_LONG;
       return 0;
     }
+  const int64_t wm = cfg->kv_watermark;  // Q16 alternative: free KVs a waiting admission must leave
   for (int i = 0; i < n; i++) {
     int64_t peak = (int64_t)I[i] + O[i] - 1;  // peak KV usage I+O-1
-    // a CONTEXT reserve (Orca) of S > M can never be admitted either (Q35)
-    if ((finiteM && peak > M) || (!cfg->chunked && peak > C) ||
-        (finiteM && cfg->reserve == OR_RESERVE_CONTEXT && cfg->S > M)) {
+    // a CONTEXT reserve (Orca) of S > M can never be admitted either (Q35); nor, with a watermark, a request
+    // whose last refill (s = I + O - 1) could not be admitted into an empty cache
+    if ((finiteM && peak + wm > M) || (!cfg->chunked && peak > C) ||
+        (finiteM && cfg->reserve == OR_RESERVE_CONTEXT && cfg->S + wm > M)) {
       out->status = OR_NEVER_FITS;
       return 0;
     }
@@ -359,72 +362,86 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
       for (int z = 0; z < 5; z++) tr.pi(0);
     }
     evs.clear();
+    // one candidate of Algorithm 1's foreach: steps (2)-(4); admits r into B or leaves it
+    auto admit_one = [&](Req& r, int id) {
+      int ph = phase_of(r);
+      // (2) CheckHybridBatching; batch phase = first admitted entry (Q19)
+      if (!cfg->hybrid && bphase != PH_NONE && ph != bphase) return;
+      // Q16 alternative: at most max_seqs entries per batch (a cap failure never preempts, like Q11)
+      if (cfg->max_seqs > 0 && (int64_t)B.size() >= cfg->max_seqs) return;
+      // (3a) token limit C, chunked prefill cropping (Q12)
+      int64_t c;
+      if (ph == PH_DECODE)
+        c = 1;
+      else
+        c = cfg->chunked ? std::min(avail(r), C - tok) : avail(r);
+      if (c == 0 || tok + c > C) return;  // token failure never preempts (Q11)
+      // SRF+Hist: defer waiting candidates predicted to cause preemption (Q31)
+      if (repl == OR_SRF_HIST && r.st == WAITING && finiteM) {
+        bool any_running = false;
+        int64_t sumrem = 0;
+        for (const Req& q : R)
+          if (q.st == RUNNING) {
+            any_running = true;
+            sumrem += std::max(hist_predict(hist, q.I) - q.g, (int64_t)0);
+          }
+        int64_t rem = std::max(hist_predict(hist, r.I) - r.g, (int64_t)0);
+        if (any_running && U + sumrem + seq_len(r) + rem > M) return;
+      }
+      // (3b) KV limit M: post-batch holdings sum max(reserved, m+c) <= M (Q13, Fig. 3)
+      int64_t newheld = std::max(r.st == WAITING ? initial_reserve(r) : r.reserved, r.m + c);
+      int64_t delta = newheld - held(r);
+      bool fits = true;
+      // Q16 alternative: a waiting admission must also leave kv_watermark KVs free (it never preempts, Q5)
+      if (finiteM && r.st == WAITING && U + delta + wm > M) return;
+      while (finiteM && U + delta > M) {
+        if (r.st == WAITING) {  // holds no KVs: skipped, never preempts (Q5)
+          fits = false;
+          break;
+        }
+        if (repl == OR_PF) {  // preemption-free: skipped, never preempts (Table 2)
+          fits = false;
+          break;
+        }
+        // (4) PreemptLowerPriorityRequest: running, not in B, lower retention (Q4)
+        int victim = -1;
+        for (int j = 0; j < n; j++) {
+          const Req& q = R[j];
+          if (j == id || q.st != RUNNING || q.in_batch) continue;
+          if (!retained_longer(r, q, repl)) continue;
+          if (victim < 0 || retained_longer(R[victim], q, repl)) victim = j;
+        }
+        if (victim < 0) {  // "If no such request remains, cand is self-preempted" (Q8)
+          preempt(r);
+          fits = false;
+          break;
+        }
+        preempt(R[victim]);
+      }
+      if (!fits) return;
+      if (r.st == WAITING) {  // (re)admission: reserve the Table 2 "Initial KV reserve"
+        r.st = RUNNING;
+        r.reserved = initial_reserve(r);
+        r.filled = false;
+        r.seq = ++seq;
+      }
+      U += delta;
+      tok += c;
+      r.in_batch = true;
+      B.push_back(Entry{id, c, r.m, ph});
+      if (bphase == PH_NONE) bphase = ph;
+    };
+    const bool hol = cfg->knobs & OR_KNOB_HOL;
+    bool wblocked = false;  // Q10 alternative: a waiting candidate was not admitted in this step
     for (auto& grp : groups) {
       for (int id : grp) {
         Req& r = R[id];
         if (r.preempted_now) continue;  // Q9
-        int ph = phase_of(r);
-        // (2) CheckHybridBatching; batch phase = first admitted entry (Q19)
-        if (!cfg->hybrid && bphase != PH_NONE && ph != bphase) continue;
-        // (3a) token limit C, chunked prefill cropping (Q12)
-        int64_t c;
-        if (ph == PH_DECODE)
-          c = 1;
-        else
-          c = cfg->chunked ? std::min(avail(r), C - tok) : avail(r);
-        if (c == 0 || tok + c > C) continue;  // token failure never preempts (Q11)
-        // SRF+Hist: defer waiting candidates predicted to cause preemption (Q31)
-        if (repl == OR_SRF_HIST && r.st == WAITING && finiteM) {
-          bool any_running = false;
-          int64_t sumrem = 0;
-          for (const Req& q : R)
-            if (q.st == RUNNING) {
-              any_running = true;
-              sumrem += std::max(hist_predict(hist, q.I) - q.g, (int64_t)0);
-            }
-          int64_t rem = std::max(hist_predict(hist, r.I) - r.g, (int64_t)0);
-          if (any_running && U + sumrem + seq_len(r) + rem > M) continue;
-        }
-        // (3b) KV limit M: post-batch holdings sum max(reserved, m+c) <= M (Q13, Fig. 3)
-        int64_t newheld = std::max(r.st == WAITING ? initial_reserve(r) : r.reserved, r.m + c);
-        int64_t delta = newheld - held(r);
-        bool fits = true;
-        while (finiteM && U + delta > M) {
-          if (r.st == WAITING) {  // holds no KVs: skipped, never preempts (Q5)
-            fits = false;
-            break;
-          }
-          if (repl == OR_PF) {  // preemption-free: skipped, never preempts (Table 2)
-            fits = false;
-            break;
-          }
-          // (4) PreemptLowerPriorityRequest: running, not in B, lower retention (Q4)
-          int victim = -1;
-          for (int j = 0; j < n; j++) {
-            const Req& q = R[j];
-            if (j == id || q.st != RUNNING || q.in_batch) continue;
-            if (!retained_longer(r, q, repl)) continue;
-            if (victim < 0 || retained_longer(R[victim], q, repl)) victim = j;
-          }
-          if (victim < 0) {  // "If no such request remains, cand is self-preempted" (Q8)
-            preempt(r);
-            fits = false;
-            break;
-          }
-          preempt(R[victim]);
-        }
-        if (!fits) continue;
-        if (r.st == WAITING) {  // (re)admission: reserve the Table 2 "Initial KV reserve"
-          r.st = RUNNING;
-          r.reserved = initial_reserve(r);
-          r.filled = false;
-          r.seq = ++seq;
-        }
-        U += delta;
-        tok += c;
-        r.in_batch = true;
-        B.push_back(Entry{id, c, r.m, ph});
-        if (bphase == PH_NONE) bphase = ph;
+        const bool was_waiting = r.st == WAITING;
+        if (hol && was_waiting && wblocked) continue;  // head-of-line blocking: R_w's visit has ended
+        const size_t nb_before = B.size();
+        admit_one(r, id);
+        if (hol && was_waiting && B.size() == nb_before) wblocked = true;
       }
     }
     n_events = (int64_t)evs.size() / 2;

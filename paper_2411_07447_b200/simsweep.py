@@ -29,7 +29,11 @@ class SimConfig(ctypes.Structure):
     _fields_ = [("order", ctypes.c_int32), ("hybrid", ctypes.c_int32), ("chunked", ctypes.c_int32),
                 ("replacement", ctypes.c_int32), ("S", ctypes.c_int32), ("workload", ctypes.c_int32),
                 ("C", ctypes.c_int64), ("M", ctypes.c_int64), ("max_steps", ctypes.c_int64),
-                ("n_cost", ctypes.c_int32), ("cost", ctypes.c_int32 * SIM_MAX_COST), ("reserve", ctypes.c_int32)]
+                ("n_cost", ctypes.c_int32), ("cost", ctypes.c_int32 * SIM_MAX_COST), ("reserve", ctypes.c_int32),
+                ("knobs", ctypes.c_int32), ("max_seqs", ctypes.c_int32), ("kv_watermark", ctypes.c_int64)]
+
+
+KNOB_HOL = 1  # Q10 alternative: head-of-line blocking of the waiting group
 
 
 class SimWorkload(ctypes.Structure):
@@ -181,8 +185,9 @@ def unit_cost(d: float = 1.0) -> SimCostModel:
 
 # ------------------------------------------------------------ configs
 def make_config(order, hybrid, chunked, replacement, C, M, S=4096, workload=0, cost=(0,),
-                max_steps=10_000_000, reserve=0) -> SimConfig:
+                max_steps=10_000_000, reserve=0, knobs=0, max_seqs=0, kv_watermark=0) -> SimConfig:
     c = SimConfig()
+    c.knobs, c.max_seqs, c.kv_watermark = int(knobs), int(max_seqs), int(kv_watermark)
     c.order, c.hybrid, c.chunked, c.replacement = int(order), int(bool(hybrid)), int(bool(chunked)), int(replacement)
     c.reserve = int(reserve)
     c.S, c.workload, c.C, c.M, c.max_steps = int(S), int(workload), int(C), int(M), int(max_steps)

@@ -1,0 +1,62 @@
+"""Oracle pins: the alternative-reading knobs (Q10/Q16 alternatives).
+
+Hand traces under the unit cost (every batch costs 1, so times count batches), worked out in the comments, plus
+the log verifier and the knob invariants (|B| <= max_seqs; a waiting admission leaves the watermark free) on
+random configurations."""
+import numpy as np
+import pytest
+
+import oracle as o
+from tests_util_knobs import random_knob_case
+from verifier import verify
+
+UNIT = o.unit_cost(1.0)
+
+
+def run(I, O, order="prefill_first", hybrid=0, chunked=0, repl="nrf", C=4096, M=-1, **kw):
+    cfg = o.make_config(order, hybrid, chunked, repl, C=C, M=M, **kw)
+    return o.run(cfg, np.array(I, np.int32), np.array(O, np.int32), np.zeros(len(I)), UNIT, trace=True)
+
+
+def test_hol_blocks_the_rest_of_the_waiting_group():
+    # vLLM, M = 6: r0 = (2, 3), r1 = (5, 1), r2 = (1, 1).  Step 1 visits R_w in order: r0 fits (U = 2), r1 needs
+    # 2 + 5 > 6 and is skipped.  Frozen reading (Q10, continue): r2 fits (U = 3) and finishes at step 1; r0
+    # decodes at steps 2 and 3 (U = 3, 4) while r1 still does not fit; r1 runs alone at step 4.
+    # Head-of-line blocking: r1's failure ends R_w's visit, so r2 waits until step 4, where r1 (U = 5) and r2
+    # (U = 6) are admitted together.  Both take 4 batches; r2 finishes at 1 vs 4.
+    base = run([2, 5, 1], [3, 1, 1], M=6)
+    hol = run([2, 5, 1], [3, 1, 1], M=6, knobs=o.KNOB_HOL)
+    assert base.steps == hol.steps == 4
+    assert list(base.t_done[0]) == [3.0, 4.0, 1.0]
+    assert list(hol.t_done[0]) == [3.0, 4.0, 4.0]
+
+
+def test_max_seqs_caps_the_batch():
+    # vLLM, three (I=2, O=2) requests, max_seqs = 2: step 1 prefills r1, r2 (r3 hits the cap); step 2 prefills r3
+    # alone (the decodes fail the phase check, no hybrid); step 3 decodes r1, r2 (r3's decode hits the cap);
+    # step 4 decodes r3.  Without the cap: one prefill batch and one decode batch.
+    assert run([2, 2, 2], [2, 2, 2], max_seqs=2).steps == 4
+    assert run([2, 2, 2], [2, 2, 2]).steps == 2
+    r = run([2, 2, 2], [2, 2, 2], max_seqs=2)
+    assert max(len(s["entries"]) for s in r.steps_list) == 2
+
+
+def test_watermark_keeps_kvs_free_for_running_requests():
+    # vLLM, M = 10, watermark 3, two (I=4, O=2): r1 is admitted (0 + 4 + 3 <= 10), r2 is not (4 + 4 + 3 > 10)
+    # although it would fit (8 <= 10); r1 decodes and finishes at step 2, r2 prefills at step 3 and decodes at 4.
+    assert run([4, 4], [2, 2], M=10, kv_watermark=3).steps == 4
+    assert run([4, 4], [2, 2], M=10).steps == 2
+    # a request whose peak plus the watermark exceeds M can never be admitted into an empty cache (Q35)
+    assert run([4, 4], [2, 2], M=10, kv_watermark=6).status == "never_fits"
+
+
+@pytest.mark.parametrize("seed", range(120))
+def test_random_knob_configs_verify(seed):
+    wl, cfg, (C, M, hybrid), knobs = random_knob_case(seed)
+    r = o.run(cfg, wl.I, wl.O, wl.T, o.load_cost_models()["llama3-8b_a100_theoretical"], trace=True)
+    assert r.status == "ok"
+    outs = dict(t_first=list(r.t_first[0]), t_done=list(r.t_done[0]), n_preempt=list(r.n_preempt),
+                refill=list(r.refill))
+    assert verify(r.steps_list, list(wl.I), list(wl.O), list(wl.T), C, M, outs, hybrid=bool(hybrid)) == []
+    if knobs["max_seqs"]:
+        assert max(len(s["entries"]) for s in r.steps_list) <= knobs["max_seqs"]
