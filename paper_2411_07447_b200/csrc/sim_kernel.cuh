@@ -68,7 +68,7 @@ struct Scal {
   int vt, status, any_pre, cur, wbuilt, arena;
   int w_dirty, p_dirty, r_dirty, o_dirty, rank_dirty, removals;
   long long r_Rs;  // scalars handed back by thread 0 after a break
-  int r_tok, r_U, r_seq, r_new, r_running, r_bph, r_nB, r_wdone;
+  int r_tok, r_U, r_seq, r_new, r_running, r_bph, r_nB, r_wdone, r_wblk;
   int wmin[32];
   int wsum[32][6];
   int wcnt[32];

@@ -32,7 +32,7 @@ namespace simsweep {
 enum { K_NONE = 0, K_MARK = 1, K_EVENT = 2 };
 constexpr int WARP_MAX = 256;  // at most this many candidates left in a group: warp-level admission
 
-template <int NT, int CAP, int IPT_, bool GM>
+template <int NT, int CAP, int IPT_, bool GM, bool KN>
 __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) : 1)) sim_kernel(KParams p) {
   using L = Smem<NT, CAP>;
   constexpr int NW = NT / 32;
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   Scal& S = *reinterpret_cast<Scal*>(smem);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int ci = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
-  if (variant_of(p.wls[p.cfgs[ci].workload].n) != p.variant) return;
+  if (variant_of(p.wls[p.cfgs[ci].workload].n) + (has_knobs(p.cfgs[ci]) ? N_SIZES : 0) != p.variant) return;
   unsigned char* arr = smem + L::scal;
   if constexpr (GM) {  // claim a per-CTA arena of the workspace
     if (tid == 0) S.arena = (int)atomicAdd(reinterpret_cast<unsigned*>(p.ws), 1u);
@@ -89,6 +89,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   const int rmode = cfg.reserve;
   const bool kv1 = rmode == SIM_RESERVE_SEQ;
   const bool rank = order >= SIM_ORDER_RANK_ORG;
+  // alternative readings: head-of-line blocking of R_w (Q10), a cap on |B| and a KV watermark
+  // for waiting admissions (Q16); with the defaults (0) every check below is a no-op
+  // (KN = false: the kernel instance for configs without knobs, where all of these checks compile away)
+  const bool holk = KN && (cfg.knobs & SIM_KNOB_HOL) != 0;
+  const int capB = cfg.max_seqs > 0 ? (int)cfg.max_seqs : 0x3fffffff;
+  const int Mw = finiteM ? M - (int)cfg.kv_watermark : 0x3fffffff;  // the KV bound of a waiting admission
   const long long row0 = p.row_off[ci], tim0 = p.tim_off[ci];
   double* tf = p.req.t_first + tim0;
   double* td = p.req.t_done + tim0;
@@ -108,8 +114,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   for (int i = tid; i < n; i += NT) {
     long long pk = (long long)wl.I[i] + wl.O[i] - 1;  // peak KV usage
     bad_long |= pk > cfg.S;
-    bad_fit |= (finiteM && pk > cfg.M) || (!chunked && pk > cfg.C);
-    bad_fit |= finiteM && cfg.reserve == SIM_RESERVE_CONTEXT && cfg.S > cfg.M;  // the reserve never fits (Q35)
+    bad_fit |= (finiteM && pk + cfg.kv_watermark > cfg.M) || (!chunked && pk > cfg.C);
+    bad_fit |= finiteM && cfg.reserve == SIM_RESERVE_CONTEXT && cfg.S + cfg.kv_watermark > cfg.M;  // never fits (Q35)
   }
   bad_long = __syncthreads_or(bad_long);
   bad_fit = __syncthreads_or(bad_fit);
@@ -299,6 +305,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     // ---- (3) a4-a8: GetNextBatch (steps 2-4) ----
     int tok = 0, U = (int)S.U, n_new = 0, n_running = nrun, bph = -1, pos = 0, nB = 0;
     int seq = (int)S.seq;
+    int wblk = 0;  // head-of-line knob: a waiting candidate was not admitted in this step
 
     auto rnew = [&](const int4& rc, int sl) -> int {  // reserve taken at (re)admission
       return rmode == SIM_RESERVE_SEQ ? rc.x + rc.y : (rmode == SIM_RESERVE_PEAK ? rc.x + s_O[sl] - 1 : cfg.S);
@@ -318,12 +325,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       S.any_pre = 1;
       S.h_pre = 1;  // a preemption outside the closed form: the run list needs a full compaction
     };
-    auto handle = [&](int sl) {  // literal sequential resolution of one candidate (thread 0)
+    auto handle_one = [&](int sl) {  // literal sequential resolution of one candidate (thread 0)
       uint8_t fl = s_fl[sl];
-      if (fl & F_PRE) return;  // Q9
       const bool isW = (fl & ST_MASK) == ST_WAIT;
       const int ph = (isW || !(fl & F_FILLED)) ? PH_PRE : PH_DEC;
       if (!hybrid && bph >= 0 && ph != bph) return;  // step 2
+      if (KN && nB >= capB) return;                   // max_seqs knob: never preempts (Q16 alternative)
       const int4 rc = s_rec[sl];
       const int s = rc.x + rc.y, avail = s - rc.z;
       const int c = ph == PH_DEC ? 1 : (chunked ? min(avail, C - tok) : avail);
@@ -335,6 +342,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       }
       const int rw = isW ? rnew(rc, sl) : rc.w;
       const int nh = max(rw, rc.z + c), held = isW ? 0 : max(rc.w, rc.z), delta = nh - held;
+      if (KN && isW && finiteM && U + delta > Mw) return;  // watermark knob (a waiting candidate never preempts, Q5)
       while (finiteM && U + delta > M) {
         if (isW || pf) return;  // holds no KVs (Q5) / preemption-free: skipped
         const int pc = s_rpos[sl];
@@ -368,6 +376,15 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       tok += c;
       if (bph < 0) bph = ph;
     };
+    auto handle = [&](int sl) {
+      const uint8_t fl = s_fl[sl];
+      if (fl & F_PRE) return;  // Q9: preempted in this step -- not a candidate (and not a failure)
+      const bool isW = (fl & ST_MASK) == ST_WAIT;
+      if (holk && isW && wblk) return;  // head-of-line knob: R_w's visit has ended
+      const int nb0 = nB;
+      handle_one(sl);
+      if (holk && isW && nB == nb0) wblk = 1;
+    };
 
     // Warp-level admission over [b0, b1) (warp 0 only): positions in P (overWin = false) or offsets in
     // the waiting window (overWin = true: slot (lo + i) mod CAP, waiting and not preempted this step =
@@ -378,7 +395,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       while (i0 < b1) {
         PROF_CNT(13, 1);
         if (overWin) {  // the rest of R_w fails a monotone check: stop
-          const bool wrej = (!hybrid && bph == PH_DEC) || (finiteM && (long long)U + minSW > M) ||
+          const bool wrej = (!hybrid && bph == PH_DEC) || (KN && nB >= capB) || (finiteM && (long long)U + minSW > (KN ? Mw : M)) ||
                             (chunked ? tok >= C : minSW > C - tok);
           if (wrej) break;
         }
@@ -401,13 +418,15 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         const int rt0 = C - tok;
         const int c = ph == PH_DEC ? 1 : (chunked ? min(avail, rt0) : avail);
         int rem = 0;
-        bool ok = sl >= 0 && !(fl & F_PRE) && (hybrid || bph < 0 || ph == bph) && c >= 1 && c <= rt0;
+        const bool cand0 = sl >= 0 && !(fl & F_PRE) && !(holk && isW && wblk);  // a candidate at all
+        bool ok = cand0 && (hybrid || bph < 0 || ph == bph) && c >= 1 && c <= rt0 && (!KN || nB < capB);
         if (hist && isW) {
           rem = max(S.pred[bucket_of(rc.x)] - rc.y, 0);
           ok = ok && !(anyRun0 && (long long)U + Rs + s + rem > M);
         }
         const int rw = isW ? rnew(rc, sl < 0 ? 0 : sl) : rc.w;
         const int delta = max(rw, rc.z + c) - (isW ? 0 : max(rc.w, rc.z));
+        if (KN && isW && finiteM && U + delta > Mw) ok = false;  // watermark knob
         const bool kvfail = finiteM && U + delta > M;
         const int kind = !ok ? K_NONE : (kvfail ? ((isW || pf) ? K_NONE : K_EVENT) : K_MARK);
         const bool mk = kind == K_MARK;
@@ -434,9 +453,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           else
             brk |= cc > rt;
           if (hist && isW) brk |= (anyRun0 || ew > 0) && (long long)pU + Rs + er + s + rem > M;
-          if (finiteM) brk |= pU + dd > M;
+          if (finiteM) brk |= pU + dd > (KN && isW ? Mw : M);
+          if (KN) brk |= nB + ek >= capB;  // max_seqs knob
         } else if (kind == K_EVENT) {
           brk = tok + ec + 1 <= C;  // else a token reject (Q11)
+        } else if (holk && isW && cand0) {
+          brk = true;  // head-of-line knob: this waiting failure ends R_w's visit (resolved literally)
         }
         const unsigned bm = __ballot_sync(FM, brk);
         const int b = bm ? __ffs(bm) - 1 : 32;
@@ -467,6 +489,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           tok = __shfl_sync(FM, tok, 0), U = __shfl_sync(FM, U, 0), seq = __shfl_sync(FM, seq, 0);
           n_new = __shfl_sync(FM, n_new, 0), n_running = __shfl_sync(FM, n_running, 0);
           nB = __shfl_sync(FM, nB, 0), bph = __shfl_sync(FM, bph, 0), Rs = __shfl_sync(FM, Rs, 0);
+          wblk = __shfl_sync(FM, wblk, 0);
           i0 += b + 1;
         } else {
           i0 += 32;
@@ -486,7 +509,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     auto decode_group = [&](bool tail_sync) {  // heads = decodes (F_FILLED) of the run list, retention order
       const bool fM = finiteM && kv1;  // heads need one KV each (else none: admitted up to the token budget)
       const int F = fM ? M - U : 0x3fffffff;
-      const int T = C - tok;
+      const int T = KN ? min(C - tok, capB - nB) : C - tok;  // one token (and one batch slot, max_seqs knob) each
       // warps whose items all lie beyond the run list only meet the barriers and fold the active warps' partials
       const int nact = min(NW, (nrun + 32 * IPT_ - 1) / (32 * IPT_));
       TMARK(10);
@@ -655,8 +678,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       bool wcont = overWin;  // every waiting request at offsets [b0, i0) was admitted
       if (overWin) wnext = b0;
       for (int i0 = b0; i0 < b1; i0 += 32) {
-        if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining one fails
-        if (overWin && ((finiteM && (long long)U + minSW > M) || (!chunked && minSW > C - tok))) return;
+        if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C) || (KN && nB >= capB)) return;  // all remaining fail
+        if (overWin && ((finiteM && (long long)U + minSW > (KN ? Mw : M)) || (!chunked && minSW > C - tok))) return;
         PROF_CNT(13, 1);
         const int i = i0 + lane;
         int sl = -1;
@@ -681,10 +704,16 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         for (;;) {
           const int rt = C - tok;
           const bool anyRun0 = n_running > 0;
-          bool fit = alive && rt >= 1 && (chunked || avail <= rt) && (!finiteM || U + dkv <= M);
+          bool fit = alive && rt >= 1 && (chunked || avail <= rt) &&
+                     (!finiteM || U + dkv <= (KN && overWin ? Mw : M)) && (!KN || nB < capB);
           if (hist && overWin) fit = fit && !(anyRun0 && (long long)U + Rs + s + rem > M);
           const unsigned fm = __ballot_sync(FM, fit);
-          if (!fm) break;
+          // head-of-line knob: the first waiting lane that fails (alone or cumulatively) ends R_w's visit
+          const unsigned failm = (holk && overWin) ? __ballot_sync(FM, alive && !fit) : 0u;
+          if (!fm) {
+            if (failm) return;
+            break;
+          }
           const int cc = fit ? avail : 0, rr = fit ? rem : 0, dk = fit ? dkv : 0;
           const bool scand = overWin && !kv1;  // KV deltas differ from c only under a PEAK / CONTEXT reserve
           int xc = cc, xr = rr, xd = dk;
@@ -711,12 +740,14 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
               crop = prt < avail;  // cropped (c = prt >= 1) or exhausted (prt <= 0)
             else
               brk = avail > prt;
-            if (finiteM) brk |= U + ed + dkv > M;
+            if (finiteM) brk |= U + ed + dkv > (KN && overWin ? Mw : M);
             if (hist && overWin) brk |= (anyRun0 || ek > 0) && (long long)U + ed + Rs + er + s + rem > M;
             if (crop && prt <= 0) brk = true;
+            if (KN) brk |= nB + ek >= capB;  // max_seqs knob
           }
           const unsigned bm = __ballot_sync(FM, brk), cm = __ballot_sync(FM, crop && !brk);
-          const int b = bm ? __ffs(bm) - 1 : 32, cl = cm ? __ffs(cm) - 1 : 32;
+          const int b0_ = bm ? __ffs(bm) - 1 : 32, cl = cm ? __ffs(cm) - 1 : 32;
+          const int b = failm ? min(b0_, __ffs(failm) - 1) : b0_;                   // first failure
           const int stop = min(b, cl);                                             // lanes < stop: in full
           const bool adm = fit && lane < stop, adc = fit && lane == cl && cl < b;  // + the cropped one
           if (adm || adc) {
@@ -755,6 +786,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           nB += nall;
           if (nall > 0 && bph < 0) bph = PH_PRE;
           if (cropped) break;  // the token budget is exhausted: every later candidate is rejected
+          if (holk && overWin && b < 32) return;  // head-of-line knob: a waiting failure ends R_w's visit
           if (b < 32 && lane == b) alive = false;  // rejected (no state change)
           if (b >= 32) break;
         }
@@ -791,7 +823,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           if (rp_first < nrun) warp_np(2, rp_first, nrun);
           int wdone = nW == 0;
           if (!wdone) {
-            const bool wrej = (!hybrid && bph == PH_DEC) || (finiteM && (long long)U + minSW > M) ||
+            const bool wrej = (!hybrid && bph == PH_DEC) || (KN && nB >= capB) || (finiteM && (long long)U + minSW > (KN ? Mw : M)) ||
                               (chunked ? tok >= C : minSW > C - tok);
             long long amax = chunked ? (long long)(C - tok) : (long long)(C - tok) / max(minSW, 1);
             if (finiteM) amax = min(amax, (long long)(M - U) / max(minSW, 1));
@@ -805,12 +837,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           if (lane == 0) {
             if (wnext >= 0) S.wfirst = lo + wnext;
             S.r_tok = tok, S.r_U = U, S.r_seq = seq, S.r_Rs = Rs, S.r_nB = nB;
-            S.r_new = n_new, S.r_running = n_running, S.r_bph = bph, S.r_wdone = wdone;
+            S.r_new = n_new, S.r_running = n_running, S.r_bph = bph, S.r_wdone = wdone, S.r_wblk = wblk;
           }
         }
         __syncthreads();
         tok = S.r_tok, U = S.r_U, seq = S.r_seq, Rs = S.r_Rs, nB = S.r_nB;
-        n_new = S.r_new, n_running = S.r_running, bph = S.r_bph;
+        n_new = S.r_new, n_running = S.r_running, bph = S.r_bph, wblk = S.r_wblk;
         pos = S.r_wdone ? nP : len0;
         __syncthreads();
         continue;
@@ -818,7 +850,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       {  // warp-level mode when few candidates need a decision
         int mode = 0, lim = nP;
         if (pos >= wbeg && pos < wend) {
-          const bool wrej = (!hybrid && bph == PH_DEC) || (finiteM && (long long)U + minSW > M) ||
+          const bool wrej = (!hybrid && bph == PH_DEC) || (KN && nB >= capB) || (finiteM && (long long)U + minSW > (KN ? Mw : M)) ||
                             (chunked ? tok >= C : minSW > C - tok);
           if (wrej) {  // every remaining waiting candidate fails a monotone check: skip the group
             pos = wend;
@@ -847,13 +879,13 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
               warp_run(false, pos, lim);
             if (lane == 0) {
               S.r_tok = tok, S.r_U = U, S.r_seq = seq, S.r_Rs = Rs, S.r_nB = nB;
-              S.r_new = n_new, S.r_running = n_running, S.r_bph = bph;
+              S.r_new = n_new, S.r_running = n_running, S.r_bph = bph, S.r_wblk = wblk;
               if (wnext >= 0) S.wfirst = lo + wnext;
             }
           }
           __syncthreads();
           tok = S.r_tok, U = S.r_U, seq = S.r_seq, Rs = S.r_Rs, nB = S.r_nB;
-          n_new = S.r_new, n_running = S.r_running, bph = S.r_bph;
+          n_new = S.r_new, n_running = S.r_running, bph = S.r_bph, wblk = S.r_wblk;
           pos = lim;
           __syncthreads();
           continue;
@@ -888,7 +920,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         flv[j] = s_fl[sl];
       }
       int kind[IPT_], cc[IPT_], dd[IPT_], rr[IPT_], av[IPT_], ss[IPT_];
-      bool ww[IPT_], pre[IPT_];
+      bool ww[IPT_], pre[IPT_], holb[IPT_];
 #pragma unroll
       for (int j = 0; j < IPT_; j++) {
         const uint8_t fl = flv[j];
@@ -899,15 +931,18 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         const int rt = C - tok;
         const int c = ph == PH_DEC ? 1 : (chunked ? min(avail, rt) : avail);
         int rem = 0;
-        bool ok = slv[j] >= 0 && !(fl & F_PRE) && (hybrid || bph < 0 || ph == bph) && c >= 1 && c <= rt;
+        const bool cand0 = slv[j] >= 0 && !(fl & F_PRE) && !(holk && isW && wblk);  // a candidate at all
+        bool ok = cand0 && (hybrid || bph < 0 || ph == bph) && c >= 1 && c <= rt && (!KN || nB < capB);
         if (hist && isW) {
           rem = max(S.pred[bucket_of(rc.x)] - rc.y, 0);
           ok = ok && !(anyRun0 && (long long)U + Rs + s + rem > M);
         }
         const int rw = isW ? rnew(rc, slv[j] < 0 ? 0 : slv[j]) : rc.w;
         const int delta = max(rw, rc.z + c) - (isW ? 0 : max(rc.w, rc.z));
+        if (KN && isW && finiteM && U + delta > Mw) ok = false;  // watermark knob
         const bool kvfail = finiteM && U + delta > M;
         kind[j] = !ok ? K_NONE : (kvfail ? ((isW || pf) ? K_NONE : K_EVENT) : K_MARK);
+        holb[j] = holk && isW && cand0 && !ok;  // head-of-line knob: this waiting failure ends R_w's visit
         const bool mk = kind[j] == K_MARK;
         cc[j] = mk ? (ph == PH_DEC ? 1 : avail) : 0;
         dd[j] = mk ? delta : 0;
@@ -944,7 +979,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       }
       int mybrk = NOBRK;
       {
-        int pc = oc, pd = od, pw = ow, pr = orr;
+        int pc = oc, pd = od, pw = ow, pr = orr, pk = ok_;
 #pragma unroll
         for (int j = 0; j < IPT_; j++) {
           const int q = pos + tid * IPT_ + j;
@@ -960,11 +995,14 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
               const bool anyR = anyRun0 || pw > 0;
               brk |= anyR && (long long)pU + Rs + pr + ss[j] + rr[j] > M;
             }
-            if (finiteM) brk |= pU + dd[j] > M;
+            if (finiteM) brk |= pU + dd[j] > (KN && ww[j] ? Mw : M);
+            if (KN) brk |= nB + pk >= capB;  // max_seqs knob
             if (brk) mybrk = min(mybrk, q);
-            pc += cc[j], pd += dd[j], pw += ww[j], pr += rr[j];
+            pc += cc[j], pd += dd[j], pw += ww[j], pr += rr[j], pk++;
           } else if (kind[j] == K_EVENT) {
             if (tok + pc + 1 <= C) mybrk = min(mybrk, q);  // else a token reject (Q11)
+          } else if (holb[j]) {
+            mybrk = min(mybrk, q);  // resolved literally: it ends R_w's visit
           }
         }
       }
@@ -1011,11 +1049,11 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         n_running += (int)S.pref[2], nB += (int)S.pref[3], Rs += S.pref[4];
         handle(cand(b));
         S.r_tok = tok, S.r_U = U, S.r_seq = seq, S.r_Rs = Rs, S.r_nB = nB;
-        S.r_new = n_new, S.r_running = n_running, S.r_bph = bph;
+        S.r_new = n_new, S.r_running = n_running, S.r_bph = bph, S.r_wblk = wblk;
       }
       __syncthreads();
       tok = S.r_tok, U = S.r_U, seq = S.r_seq, Rs = S.r_Rs, nB = S.r_nB;
-      n_new = S.r_new, n_running = S.r_running, bph = S.r_bph;
+      n_new = S.r_new, n_running = S.r_running, bph = S.r_bph, wblk = S.r_wblk;
       pos = b + 1;
     }
     __syncthreads();  // admissions of the last round are visible

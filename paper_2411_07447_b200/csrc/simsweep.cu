@@ -53,7 +53,11 @@ __device__ int g_trn;
 // 0: W <= 1024 and 1: W <= 4096, state in shared memory (the window never exceeds n <= CAP);
 // 2: larger workloads, a 32768-slot ring in a per-CTA global-memory arena (SIM_MAX_WINDOW)
 __host__ __device__ inline int variant_of(int n) { return n <= 1024 ? 0 : (n <= 4096 ? 1 : 2); }
-constexpr int N_VARIANTS = 3;
+constexpr int N_SIZES = 3;
+// configs with an alternative-reading knob run in a second instance of each size (KN = true), so that the
+// default instances carry none of the knob checks
+__host__ __device__ inline bool has_knobs(const sim_config_t& c) { return c.knobs || c.max_seqs || c.kv_watermark; }
+constexpr int N_VARIANTS = 2 * N_SIZES;
 
 #ifndef SIM_NT_SMALL
 #define SIM_NT_SMALL 256  // threads per CTA of the W <= 1024 variant
@@ -90,14 +94,16 @@ struct Variant {
   void (*fn)(KParams);
 };
 
-template <int NT, int CAP, int IPT_, bool GM>
+template <int NT, int CAP, int IPT_, bool GM, bool KN>
 Variant make_variant() {
   using L = Smem<NT, CAP>;
-  return Variant{NT, CAP, GM ? L::scal : L::bytes, GM ? L::arr_bytes : 0, sim_kernel<NT, CAP, IPT_, GM>};
+  return Variant{NT, CAP, GM ? L::scal : L::bytes, GM ? L::arr_bytes : 0, sim_kernel<NT, CAP, IPT_, GM, KN>};
 }
 
-static Variant g_variants[N_VARIANTS] = {make_variant<SIM_NT_SMALL, 1024, SIM_IPT_SMALL, false>(),
-                                         make_variant<512, 4096, 4, false>(), make_variant<512, SIM_MAX_WINDOW, 4, true>()};
+static Variant g_variants[N_VARIANTS] = {
+    make_variant<SIM_NT_SMALL, 1024, SIM_IPT_SMALL, false, false>(), make_variant<512, 4096, 4, false, false>(),
+    make_variant<512, SIM_MAX_WINDOW, 4, true, false>(),           make_variant<SIM_NT_SMALL, 1024, SIM_IPT_SMALL, false, true>(),
+    make_variant<512, 4096, 4, false, true>(),                     make_variant<512, SIM_MAX_WINDOW, 4, true, true>()};
 
 static int64_t workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int32_t* wls_n) {
   int64_t big = 0;
@@ -171,8 +177,9 @@ int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* 
   if (!h_cfgs || !h_wls_n || !d_cfgs || !d_wls || !d_cms || n_cfgs <= 0 || n_cms <= 0 || !d_row_off ||
       !d_tim_off || !d_results || !d_req.t_first || !d_req.t_done || !d_req.n_preempt || !d_req.refill_tokens)
     return SIM_EINVAL;
-  bool need[N_VARIANTS] = {false, false, false};
-  for (int i = 0; i < n_cfgs; i++) need[variant_of(h_wls_n[h_cfgs[i].workload])] = true;
+  bool need[N_VARIANTS] = {false, false, false, false, false, false};
+  for (int i = 0; i < n_cfgs; i++)
+    need[variant_of(h_wls_n[h_cfgs[i].workload]) + (has_knobs(h_cfgs[i]) ? N_SIZES : 0)] = true;
   const int64_t wsb = workspace_bytes(h_cfgs, n_cfgs, h_wls_n);
   if (wsb > 0 && (!d_workspace || workspace_bytes_ < wsb)) return SIM_EINVAL;
   KParams kp;
@@ -188,7 +195,9 @@ int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* 
   kp.n_cfgs = n_cfgs;
   int launches = 0;
   // the large-window variants first: their simulations are the longest
-  for (int v = N_VARIANTS - 1; v >= 0; v--) {
+  static const int launch_order[N_VARIANTS] = {2, 2 + N_SIZES, 1, 1 + N_SIZES, 0, N_SIZES};
+  for (int vi = 0; vi < N_VARIANTS; vi++) {
+    const int v = launch_order[vi];
     if (!need[v]) continue;
     const Variant& V = g_variants[v];
     int dev = 0;
@@ -236,6 +245,8 @@ static int validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload
     if (c.replacement < SIM_NRF || c.replacement > SIM_PF) return SIM_EINVAL;
     if (c.reserve < SIM_RESERVE_SEQ || c.reserve > SIM_RESERVE_CONTEXT) return SIM_EINVAL;
     if ((c.replacement == SIM_PF) != (c.reserve != SIM_RESERVE_SEQ)) return SIM_EINVAL;  // Q39
+    if ((c.knobs & ~SIM_KNOB_HOL) || c.max_seqs < 0 || c.kv_watermark < 0 || c.kv_watermark >= (1 << 30))
+      return SIM_EINVAL;  // alternative-reading knobs
     if ((c.hybrid != 0 && c.hybrid != 1) || (c.chunked != 0 && c.chunked != 1)) return SIM_EINVAL;
     if (c.C < 1 || c.C > (1 << 30) || c.M > (1 << 30) || c.S < 1 || c.S > 262143 || c.max_steps < 1) return SIM_EINVAL;
     if (c.n_cost < 1 || c.n_cost > SIM_MAX_COST) return SIM_EINVAL;

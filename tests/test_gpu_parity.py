@@ -308,3 +308,29 @@ def test_large_window_variant():
         M = int(rng.integers(lo, 20 * lo + 1))
         cases.append((cfg(o_, hybrid, chunked, r, C, M, S=256, reserve=res), wl, A100))
     assert_parity(cases, processes=len(cases))
+
+
+@pytest.mark.parametrize("block", range(3))
+def test_random_knobs(block):
+    # alternative readings: head-of-line blocking, max_seqs, KV watermark, on random configs
+    from tests_util_knobs import random_knob_case
+    cases = []
+    for seed in range(block * 80, block * 80 + 80):
+        wl, oc, _, knobs = random_knob_case(seed)
+        c = cfg(oc.order, oc.hybrid, oc.chunked, oc.replacement, oc.C, oc.M, S=oc.S, **knobs)
+        names = A100 if seed % 2 else ["llama3-70b_h100x4_theoretical"]
+        cases.append((c, wl, names))
+    assert_parity(cases)
+
+
+def test_knob_hand_traces_and_grid_sample():
+    # the oracle's hand traces (tests/test_oracle_knobs.py) and vLLM-like caps on full-size grid cells
+    cases = [(cfg(0, 0, 0, 0, 4096, 6, knobs=simsweep.KNOB_HOL), W([2, 5, 1], [3, 1, 1]), UNIT),
+             (cfg(0, 0, 0, 0, 4096, -1, max_seqs=2), W([2, 2, 2], [2, 2, 2]), UNIT),
+             (cfg(0, 0, 0, 0, 4096, 10, kv_watermark=3), W([4, 4], [2, 2]), UNIT)]
+    for name in ("vllm", "sarathi", "vllm-srf", "sarathi-srf"):
+        for (I, O) in ((16, 256), (128, 512), (1, 1024)):
+            cases.append((simsweep.preset_config(name, 100_000, knobs=simsweep.KNOB_HOL, max_seqs=256,
+                                                 kv_watermark=1000), workloads.fixed(I, O, 1024), A100))
+    g, ors = assert_parity(cases)
+    assert [int(g.results["steps"][i]) for i in range(3)] == [4, 4, 4]
