@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       TMARK(11);
       // (ii) a_kv = #{heads i : F + RS(p_i + 1) >= i}, i = k - HS(p_i) + 1 (monotone in i)
       int akv = k;
-      if (fM) {
+      if (fM && F < k) {  // with F >= k every head passes (F + RS(p_i + 1) >= F >= k >= i): no pass needed
         if (act) {
           int cnt = 0;
 #pragma unroll
