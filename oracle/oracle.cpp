@@ -52,7 +52,10 @@ int64_t held(const Req& r) { return r.st == RUNNING ? std::max(r.reserved, r.m) 
 // SRF: "prioritizes running long requests (having large m) and preempts short
 //      requests"; ties: later admission is preempted first (Q7).
 // PF: never preempts; its running order is admission order, as NRF (Q39).
-bool retained_longer(const Req& a, const Req& b, int repl) {
+// retention priority (Q3, Q6, Q7): NRF keeps the earlier ADMITTED request (or, with the Q6 alternative, the
+// earlier ARRIVAL: (T, id) = index order), SRF the one with more cached KVs
+bool retained_longer(const Req& a, const Req& b, int repl, bool by_arrival = false) {
+  if (by_arrival) return a.id < b.id;
   if (repl == OR_NRF || repl == OR_PF) return a.seq < b.seq;
   if (a.m != b.m) return a.m > b.m;
   return a.seq < b.seq;
@@ -232,7 +235,8 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
   if (cfg->replacement < OR_NRF || cfg->replacement > OR_PF) return -2;
   if (cfg->reserve < OR_RESERVE_SEQ || cfg->reserve > OR_RESERVE_CONTEXT) return -2;
   if ((cfg->replacement == OR_PF) != (cfg->reserve != OR_RESERVE_SEQ)) return -2;  // Q39
-  if ((cfg->knobs & ~OR_KNOB_HOL) || cfg->max_seqs < 0 || cfg->kv_watermark < 0) return -2;
+  if ((cfg->knobs & ~(OR_KNOB_HOL | OR_KNOB_NRF_ARRIVAL)) || cfg->max_seqs < 0 || cfg->kv_watermark < 0) return -2;
+  if ((cfg->knobs & OR_KNOB_NRF_ARRIVAL) && cfg->replacement != OR_NRF) return -2;
   if (cfg->n_cost < 1 || cfg->n_cost > 4) return -3;
   if (cfg->C < 1 || cfg->S < 1 || cfg->max_steps < 1) return -4;
   for (int i = 0; i < n; i++) {
@@ -242,6 +246,7 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
   }
   const int K = cfg->n_cost;
   const int repl = cfg->replacement;
+  const bool by_arrival = (cfg->knobs & OR_KNOB_NRF_ARRIVAL) != 0;  // Q6 alternative
   const bool finiteM = cfg->M >= 0;
   const int64_t M = cfg->M, C = cfg->C;
 
@@ -332,7 +337,7 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
     for (int i = 0; i < n; i++)
       if (R[i].st == RUNNING) Rr.push_back(i);
     std::stable_sort(Rr.begin(), Rr.end(),
-                     [&](int a, int b) { return retained_longer(R[a], R[b], repl); });  // Q3
+                     [&](int a, int b) { return retained_longer(R[a], R[b], repl, by_arrival); });  // Q3, Q6
     for (int i : Rr) (phase_of(R[i]) == PH_DECODE ? Rd : Rp).push_back(i);
     std::vector<std::vector<int>> groups;
     if (cfg->order == OR_PREFILL_FIRST) {  // vLLM {R_w, R_r}
@@ -408,8 +413,8 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
         for (int j = 0; j < n; j++) {
           const Req& q = R[j];
           if (j == id || q.st != RUNNING || q.in_batch) continue;
-          if (!retained_longer(r, q, repl)) continue;
-          if (victim < 0 || retained_longer(R[victim], q, repl)) victim = j;
+          if (!retained_longer(r, q, repl, by_arrival)) continue;
+          if (victim < 0 || retained_longer(R[victim], q, repl, by_arrival)) victim = j;
         }
         if (victim < 0) {  // "If no such request remains, cand is self-preempted" (Q8)
           preempt(r);

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   // for waiting admissions (Q16); with the defaults (0) every check below is a no-op
   // (KN = false: the kernel instance for configs without knobs, where all of these checks compile away)
   const bool holk = KN && (cfg.knobs & SIM_KNOB_HOL) != 0;
+  const bool arr_ord = KN && (cfg.knobs & SIM_KNOB_NRF_ARRIVAL) != 0;  // NRF run list in arrival order (Q6 alt.)
   const int capB = cfg.max_seqs > 0 ? (int)cfg.max_seqs : 0x3fffffff;
   const int Mw = finiteM ? M - (int)cfg.kv_watermark : 0x3fffffff;  // the KV bound of a waiting admission
   const long long row0 = p.row_off[ci], tim0 = p.tim_off[ci];
@@ -1253,7 +1254,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           if (S.w_dirty) S.wstale = 0;
           S.rank_dirty = ndn > 0;
           // SRF order can change unless every running request was a decode in B (all +1)
-          S.o_dirty = srf && (changed || f.np > 0 || f.nd != nrun);
+          S.o_dirty = (srf && (changed || f.np > 0 || f.nd != nrun)) || (arr_ord && n_new > 0);
           S.p_dirty = changed || tt[9] > 0;
           S.r_new = n_new;
         }
@@ -1407,8 +1408,9 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         }
       }
       TMARK(50);
-      if (od) {  // SRF retention order: m descending, then admission order (Q3, Q7)
+      if (od) {  // SRF retention order: m descending, then admission order (Q3, Q7); or arrival order (Q6 alt.)
         auto key = [&](int sl) -> unsigned long long {
+          if (arr_ord) return (unsigned long long)(unsigned)(lo + ((sl - lo) & (CAP - 1)));  // (T, id) = index
           return ((unsigned long long)(0x3FFFF - s_rec[sl].z) << 46) |
                  ((unsigned long long)(unsigned)s_seq[sl] << SLB) | (unsigned long long)sl;
         };

@@ -60,3 +60,13 @@ def test_random_knob_configs_verify(seed):
     assert verify(r.steps_list, list(wl.I), list(wl.O), list(wl.T), C, M, outs, hybrid=bool(hybrid)) == []
     if knobs["max_seqs"]:
         assert max(len(s["entries"]) for s in r.steps_list) <= knobs["max_seqs"]
+
+
+def test_nrf_by_arrival_keeps_a_refilled_request_in_place():
+    # vLLM, M = 5: r0 = (3, 1), r1 = (3, 2), r2 = (1, 2).  Step 1: r0 (U = 3) and r2 (U = 4) prefill, r1 does not fit
+    # (6 > 5); r0 finishes.  Step 2: r1 prefills (U = 4; r2's decode fails the phase check).  Step 3 decodes:
+    # * frozen NRF (admission order, Q6): r2 (seq 2) first -> U = 5; r1 (seq 3) needs 6 > 5 with no newer admission
+    #   to evict -> self-preempts; r2 finishes at 3; r1 refills (4 tokens) and finishes at 4;
+    # * by arrival (T, id): r1 (id 1) first -> U = 5; r2 (id 2) self-preempts; r1 finishes at 3, r2 at 4.
+    assert list(run([3, 3, 1], [1, 2, 2], M=5).t_done[0]) == [1.0, 4.0, 3.0]
+    assert list(run([3, 3, 1], [1, 2, 2], M=5, knobs=o.KNOB_NRF_ARRIVAL).t_done[0]) == [1.0, 3.0, 4.0]
