@@ -54,7 +54,9 @@ enum {
                        this step (vLLM's head-of-line blocking; a rank order skips the later waiting candidates) */
   SIM_KNOB_NRF_ARRIVAL = 2 /* Q6 alternative (NRF only): running requests are visited and retained in arrival
                               order (T, id) -- vLLM's FCFS running queue -- instead of admission order, so a refilled
-                              request keeps its place and the newest ARRIVAL is preempted first */
+                              request keeps its place and the newest ARRIVAL is preempted first */,
+  SIM_KNOB_SRF_VISIT_ADMISSION = 4 /* Q3 alternative (SRF / SRF+Hist only): running requests are visited in admission
+                                      order; SRF only chooses the victims (smallest m, later admission first) */
 };
 /* per-simulation status */
 enum {
@@ -69,7 +71,7 @@ enum {
 enum {
   SIM_EINVAL = -1,    /* NULL pointer, n <= 0, bad enum, C not in [1, 2^30], M > 2^30, S not in [1, 2^18), n_cost not 1..4,
                          replacement == SIM_PF without a PEAK / CONTEXT reserve or vice versa, unknown knob bits,
-                         SIM_KNOB_NRF_ARRIVAL without SIM_NRF,
+                         SIM_KNOB_NRF_ARRIVAL without SIM_NRF, SIM_KNOB_SRF_VISIT_ADMISSION without SRF,
                          max_seqs < 0, kv_watermark not in [0, 2^30) */
   SIM_EWORKLOAD = -2, /* I < 1, O < 1, T not sorted, or T != 0 with n_cost > 1 */
   SIM_ECOST = -3,     /* cost-model index out of range or bad cost-model fields */

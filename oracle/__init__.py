@@ -47,6 +47,7 @@ class OracleConfig(ctypes.Structure):
 
 KNOB_HOL = 1  # Q10 alternative: head-of-line blocking of the waiting group
 KNOB_NRF_ARRIVAL = 2  # Q6 alternative: NRF retention / running order by arrival (T, id)
+KNOB_SRF_VISIT_ADMISSION = 4  # Q3 alternative: SRF visits running requests in admission order
 
 
 class OracleCost(ctypes.Structure):

@@ -235,8 +235,12 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
   if (cfg->replacement < OR_NRF || cfg->replacement > OR_PF) return -2;
   if (cfg->reserve < OR_RESERVE_SEQ || cfg->reserve > OR_RESERVE_CONTEXT) return -2;
   if ((cfg->replacement == OR_PF) != (cfg->reserve != OR_RESERVE_SEQ)) return -2;  // Q39
-  if ((cfg->knobs & ~(OR_KNOB_HOL | OR_KNOB_NRF_ARRIVAL)) || cfg->max_seqs < 0 || cfg->kv_watermark < 0) return -2;
+  if ((cfg->knobs & ~(OR_KNOB_HOL | OR_KNOB_NRF_ARRIVAL | OR_KNOB_SRF_VISIT_ADMISSION)) || cfg->max_seqs < 0 ||
+      cfg->kv_watermark < 0)
+    return -2;
   if ((cfg->knobs & OR_KNOB_NRF_ARRIVAL) && cfg->replacement != OR_NRF) return -2;
+  if ((cfg->knobs & OR_KNOB_SRF_VISIT_ADMISSION) && cfg->replacement != OR_SRF && cfg->replacement != OR_SRF_HIST)
+    return -2;
   if (cfg->n_cost < 1 || cfg->n_cost > 4) return -3;
   if (cfg->C < 1 || cfg->S < 1 || cfg->max_steps < 1) return -4;
   for (int i = 0; i < n; i++) {
@@ -337,7 +341,10 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
     for (int i = 0; i < n; i++)
       if (R[i].st == RUNNING) Rr.push_back(i);
     std::stable_sort(Rr.begin(), Rr.end(),
-                     [&](int a, int b) { return retained_longer(R[a], R[b], repl, by_arrival); });  // Q3, Q6
+                     [&](int a, int b) {  // Q3 (or its alternative: SRF visits in admission order), Q6
+                       if (cfg->knobs & OR_KNOB_SRF_VISIT_ADMISSION) return R[a].seq < R[b].seq;
+                       return retained_longer(R[a], R[b], repl, by_arrival);
+                     });
     for (int i : Rr) (phase_of(R[i]) == PH_DECODE ? Rd : Rp).push_back(i);
     std::vector<std::vector<int>> groups;
     if (cfg->order == OR_PREFILL_FIRST) {  // vLLM {R_w, R_r}

@@ -39,7 +39,8 @@ typedef struct {
   int64_t kv_watermark; /* Q16 alternative: KVs a waiting admission must leave free (0 = none) */
 } oracle_config_t;
 enum { OR_KNOB_HOL = 1 /* Q10 alternative: the first waiting candidate not admitted ends R_w's visit */,
-       OR_KNOB_NRF_ARRIVAL = 2 /* Q6 alternative: NRF visits and retains running requests in arrival order */ };
+       OR_KNOB_NRF_ARRIVAL = 2 /* Q6 alternative: NRF visits and retains running requests in arrival order */,
+       OR_KNOB_SRF_VISIT_ADMISSION = 4 /* Q3 alternative: SRF visits in admission order, SRF only for victims */ };
 
 typedef struct {
   int32_t mode; /* 0 = linear, 1 = theoretical (Eq. 3) */

@@ -94,6 +94,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   // (KN = false: the kernel instance for configs without knobs, where all of these checks compile away)
   const bool holk = KN && (cfg.knobs & SIM_KNOB_HOL) != 0;
   const bool arr_ord = KN && (cfg.knobs & SIM_KNOB_NRF_ARRIVAL) != 0;  // NRF run list in arrival order (Q6 alt.)
+  // Q3 alternative: SRF visits in admission order (the run list is not re-sorted) and only picks victims by m,
+  // so the victim pool is not the run list's tail: the closed form is off and victims are searched literally
+  const bool q3alt = KN && (cfg.knobs & SIM_KNOB_SRF_VISIT_ADMISSION) != 0;
+  const bool srf_order = srf && !q3alt;
   const int capB = cfg.max_seqs > 0 ? (int)cfg.max_seqs : 0x3fffffff;
   const int Mw = finiteM ? M - (int)cfg.kv_watermark : 0x3fffffff;  // the KV bound of a waiting admission
   const long long row0 = p.row_off[ci], tim0 = p.tim_off[ci];
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       __syncthreads();
     }
     int nRd = 0;
-    if (order == SIM_ORDER_DECODE_FIRST && nrun > CH) {  // fallback path only: stable split of the run list
+    if (order == SIM_ORDER_DECODE_FIRST && (nrun > CH || q3alt)) {  // general path: stable split of the run list
       if (S.p_dirty) {
         const int nrd = block_partition<NT, IPT_>(
             nrun, [&](int q) { return (s_fl[run[q]] & F_FILLED) != 0; }, [&](int q) { return run[q]; }, s_pl, S);
@@ -346,6 +350,24 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       if (KN && isW && finiteM && U + delta > Mw) return;  // watermark knob (a waiting candidate never preempts, Q5)
       while (finiteM && U + delta > M) {
         if (isW || pf) return;  // holds no KVs (Q5) / preemption-free: skipped
+        if (q3alt) {  // lowest SRF retention among running requests outside B retained less than sl (Q3 alt.)
+          const int cm = rc.z, cs = s_seq[sl];
+          int best = -1, bm = 0, bs = 0;
+          for (int q = 0; q < nrun; q++) {
+            const int v = run[q];
+            const uint8_t f = s_fl[v];
+            if (v == sl || (f & F_INB) || (f & ST_MASK) != ST_RUN) continue;
+            const int vm = s_rec[v].z, vs = s_seq[v];
+            if (!(cm > vm || (cm == vm && cs < vs))) continue;
+            if (best < 0 || vm < bm || (vm == bm && vs > bs)) best = v, bm = vm, bs = vs;
+          }
+          if (best < 0) {  // self-preemption (Q8)
+            preempt(sl);
+            return;
+          }
+          preempt(best);
+          continue;
+        }
         const int pc = s_rpos[sl];
         int vt = S.vt;
         while (vt > pc) {  // lowest retention = tail of the retention-ordered run list
@@ -808,13 +830,13 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     while (pos < nP) {
       TMARK(20);
       // running decodes in closed form
-      if (order == SIM_ORDER_PREFILL_FIRST && pos == nW && nW < nP && !chunked && nrun <= CH) {
+      if (order == SIM_ORDER_PREFILL_FIRST && pos == nW && nW < nP && !chunked && nrun <= CH && !q3alt) {
         if (hybrid || bph != PH_PRE) decode_group(false);  // else every decode fails step 2 (no running prefills)
         pos = nP;
         PROF_CNT(12, 1);
         continue;
       }
-      if (order == SIM_ORDER_DECODE_FIRST && pos == 0 && !rfast && nrun <= CH) {
+      if (order == SIM_ORDER_DECODE_FIRST && pos == 0 && !rfast && nrun <= CH && !q3alt) {
         rfast = true;
         // {R_r^d, R_r^p, R_w}: decodes in closed form, then running prefills and (if warp-suitable) the
         // waiting group in one pass of warp 0
@@ -1254,7 +1276,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           if (S.w_dirty) S.wstale = 0;
           S.rank_dirty = ndn > 0;
           // SRF order can change unless every running request was a decode in B (all +1)
-          S.o_dirty = (srf && (changed || f.np > 0 || f.nd != nrun)) || (arr_ord && n_new > 0);
+          S.o_dirty = (srf_order && (changed || f.np > 0 || f.nd != nrun)) || (arr_ord && n_new > 0);
           S.p_dirty = changed || tt[9] > 0;
           S.r_new = n_new;
         }
@@ -1366,7 +1388,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           S.U = U0 + E * du - fr2;
           S.n_done += (int)nd2t;
           if (nd2t > 0) S.r_dirty = 1, S.removals = 2, S.rank_dirty = 1, S.p_dirty = 1;
-          if (srf && E > 0 && ndd != nrun) S.o_dirty = 1;
+          if (srf_order && E > 0 && ndd != nrun) S.o_dirty = 1;
         }
         __syncthreads();
       }

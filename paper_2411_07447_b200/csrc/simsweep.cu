@@ -245,8 +245,9 @@ static int validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload
     if (c.replacement < SIM_NRF || c.replacement > SIM_PF) return SIM_EINVAL;
     if (c.reserve < SIM_RESERVE_SEQ || c.reserve > SIM_RESERVE_CONTEXT) return SIM_EINVAL;
     if ((c.replacement == SIM_PF) != (c.reserve != SIM_RESERVE_SEQ)) return SIM_EINVAL;  // Q39
-    if ((c.knobs & ~(SIM_KNOB_HOL | SIM_KNOB_NRF_ARRIVAL)) || c.max_seqs < 0 || c.kv_watermark < 0 ||
-        c.kv_watermark >= (1 << 30) || ((c.knobs & SIM_KNOB_NRF_ARRIVAL) && c.replacement != SIM_NRF))
+    if ((c.knobs & ~(SIM_KNOB_HOL | SIM_KNOB_NRF_ARRIVAL | SIM_KNOB_SRF_VISIT_ADMISSION)) || c.max_seqs < 0 ||
+        c.kv_watermark < 0 || c.kv_watermark >= (1 << 30) || ((c.knobs & SIM_KNOB_NRF_ARRIVAL) && c.replacement != SIM_NRF) ||
+        ((c.knobs & SIM_KNOB_SRF_VISIT_ADMISSION) && c.replacement != SIM_SRF && c.replacement != SIM_SRF_HIST))
       return SIM_EINVAL;  // alternative-reading knobs
     if ((c.hybrid != 0 && c.hybrid != 1) || (c.chunked != 0 && c.chunked != 1)) return SIM_EINVAL;
     if (c.C < 1 || c.C > (1 << 30) || c.M > (1 << 30) || c.S < 1 || c.S > 262143 || c.max_steps < 1) return SIM_EINVAL;

@@ -70,3 +70,14 @@ def test_nrf_by_arrival_keeps_a_refilled_request_in_place():
     # * by arrival (T, id): r1 (id 1) first -> U = 5; r2 (id 2) self-preempts; r1 finishes at 3, r2 at 4.
     assert list(run([3, 3, 1], [1, 2, 2], M=5).t_done[0]) == [1.0, 4.0, 3.0]
     assert list(run([3, 3, 1], [1, 2, 2], M=5, knobs=o.KNOB_NRF_ARRIVAL).t_done[0]) == [1.0, 3.0, 4.0]
+
+
+def test_srf_visiting_in_admission_order():
+    # vLLM-SRF, M = 4: r0 = (1, 3), r1 = (2, 3).  Step 1 prefills both (U = 3).  Step 2 decodes:
+    # * frozen SRF (visit by m descending, Q3): r1 (m 2) decodes (U = 4); r0 (m 1) has no lower-retention
+    #   victim and self-preempts; r1 finishes at 3 while r0's refill (2 tokens) waits, refills at 4, ends at 5;
+    # * admission order, SRF only for victims: r0 (seq 1) decodes first (U = 4); r1's only lower-m request r0 is
+    #   already in B, so r1 self-preempts; r0 finishes at 3, r1 refills (3 tokens) at 4 and ends at 5.
+    base = run([1, 2], [3, 3], repl="srf", M=4)
+    alt = run([1, 2], [3, 3], repl="srf", M=4, knobs=o.KNOB_SRF_VISIT_ADMISSION)
+    assert list(base.t_done[0]) == [5.0, 3.0] and list(alt.t_done[0]) == [3.0, 5.0]

@@ -22,6 +22,7 @@ def random_knob_case(seed):
     wm = int(rng.integers(0, 6)) if rng.random() < 0.5 else 0
     M = -1 if rng.random() < 0.1 else int(rng.integers(peak + wm, 4 * peak + wm + 1))
     bits = (o.KNOB_HOL if rng.random() < 0.6 else 0) | (o.KNOB_NRF_ARRIVAL if repl == "nrf" and rng.random() < 0.5 else 0)
+    bits |= o.KNOB_SRF_VISIT_ADMISSION if repl != "nrf" and rng.random() < 0.5 else 0
     knobs = dict(knobs=bits, max_seqs=int(rng.integers(1, 6)) if rng.random() < 0.5 else 0,
                  kv_watermark=wm if M >= 0 else 0)
     cfg = o.make_config(order, hybrid, chunked, repl, C=C, M=M, S=96, **knobs)
