@@ -72,7 +72,7 @@ enum {
   SIM_EINVAL = -1,    /* NULL pointer, n <= 0, bad enum, C not in [1, 2^30], M > 2^30, S not in [1, 2^18), n_cost not 1..4,
                          replacement == SIM_PF without a PEAK / CONTEXT reserve or vice versa, unknown knob bits,
                          SIM_KNOB_NRF_ARRIVAL without SIM_NRF, SIM_KNOB_SRF_VISIT_ADMISSION without SRF,
-                         max_seqs < 0, kv_watermark not in [0, 2^30) */
+                         max_seqs < 0, kv_watermark not in [0, 2^30), kv_block not in [0, 2^16] or > 1 with SRF+Hist */
   SIM_EWORKLOAD = -2, /* I < 1, O < 1, T not sorted, or T != 0 with n_cost > 1 */
   SIM_ECOST = -3,     /* cost-model index out of range or bad cost-model fields */
   SIM_ECUDA = -4,     /* a CUDA runtime error (device, allocation, launch) */
@@ -86,7 +86,7 @@ enum {
  * larger ones use a per-simulation arena of the caller's workspace. */
 #define SIM_MAX_WINDOW 32768
 
-/* One simulation.  88 bytes, naturally aligned. */
+/* One simulation.  96 bytes, naturally aligned. */
 typedef struct {
   int32_t order;       /* SIM_ORDER_* */
   int32_t hybrid;      /* 0/1: hybrid prefill+decode batches (step 2) */
@@ -103,6 +103,9 @@ typedef struct {
   int32_t knobs;       /* SIM_KNOB_* bits: alternative readings (0 = the frozen semantics) */
   int32_t max_seqs;    /* Q16 alternative: at most this many entries per batch, like vLLM's max_num_seqs (0 = no cap) */
   int64_t kv_watermark;/* Q16 alternative: KVs a waiting admission must leave free, like vLLM's watermark (0 = none) */
+  int32_t kv_block;    /* Q15 alternative: KVs are allocated in blocks of this many tokens, like vLLM's paged cache;
+                          M and kv_watermark stay in tokens (capacity floor(M / kv_block) blocks); 0 or 1 = per token */
+  int32_t pad;
 } sim_config_t;
 
 /* One workload: n requests sorted by (T, id).  The pointers are HOST memory

@@ -42,7 +42,7 @@ class OracleConfig(ctypes.Structure):
                 ("replacement", ctypes.c_int32), ("S", ctypes.c_int32), ("n_cost", ctypes.c_int32),
                 ("C", ctypes.c_int64), ("M", ctypes.c_int64), ("max_steps", ctypes.c_int64),
                 ("reserve", ctypes.c_int32), ("knobs", ctypes.c_int32), ("max_seqs", ctypes.c_int32),
-                ("pad", ctypes.c_int32), ("kv_watermark", ctypes.c_int64)]
+                ("kv_block", ctypes.c_int32), ("kv_watermark", ctypes.c_int64)]
 
 
 KNOB_HOL = 1  # Q10 alternative: head-of-line blocking of the waiting group
@@ -155,9 +155,9 @@ class OracleResult:
 
 
 def make_config(order, hybrid, chunked, replacement, C, M, S=4096, max_steps=10_000_000, n_cost=1,
-                reserve=0, knobs=0, max_seqs=0, kv_watermark=0) -> OracleConfig:
+                reserve=0, knobs=0, max_seqs=0, kv_watermark=0, kv_block=0) -> OracleConfig:
     c = OracleConfig()
-    c.knobs, c.max_seqs, c.kv_watermark = int(knobs), int(max_seqs), int(kv_watermark)
+    c.knobs, c.max_seqs, c.kv_watermark, c.kv_block = int(knobs), int(max_seqs), int(kv_watermark), int(kv_block)
     c.order = ORDERS[order] if isinstance(order, str) else int(order)
     c.hybrid, c.chunked = int(bool(hybrid)), int(bool(chunked))
     c.replacement = REPLACEMENTS[replacement] if isinstance(replacement, str) else int(replacement)

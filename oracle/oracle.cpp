@@ -43,8 +43,10 @@ int64_t seq_len(const Req& r) { return r.I + r.g; }
 int64_t avail(const Req& r) { return seq_len(r) - r.m; }
 // Phase: prefill iff waiting or running with an incomplete (re)fill (Q17)
 int phase_of(const Req& r) { return (r.st == WAITING || !r.filled) ? PH_PREFILL : PH_DECODE; }
-// KVs held in the cache (Q13): running requests hold max(reserved, m)
-int64_t held(const Req& r) { return r.st == RUNNING ? std::max(r.reserved, r.m) : 0; }
+// KVs held in the cache (Q13): running requests hold max(reserved, m) -- counted in blocks of b tokens under the
+// Q15 alternative (paged KV), b = 1 otherwise
+int64_t blocks(int64_t x, int64_t b) { return (x + b - 1) / b; }
+int64_t held(const Req& r, int64_t b) { return r.st == RUNNING ? blocks(std::max(r.reserved, r.m), b) : 0; }
 
 // true iff a is retained longer than b under the replacement policy.
 // NRF: "newest request first" is preempted first (Table 2), newest
@@ -241,6 +243,7 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
   if ((cfg->knobs & OR_KNOB_NRF_ARRIVAL) && cfg->replacement != OR_NRF) return -2;
   if ((cfg->knobs & OR_KNOB_SRF_VISIT_ADMISSION) && cfg->replacement != OR_SRF && cfg->replacement != OR_SRF_HIST)
     return -2;
+  if (cfg->kv_block < 0 || (cfg->kv_block > 1 && cfg->replacement == OR_SRF_HIST)) return -2;
   if (cfg->n_cost < 1 || cfg->n_cost > 4) return -3;
   if (cfg->C < 1 || cfg->S < 1 || cfg->max_steps < 1) return -4;
   for (int i = 0; i < n; i++) {
@@ -252,7 +255,8 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
   const int repl = cfg->replacement;
   const bool by_arrival = (cfg->knobs & OR_KNOB_NRF_ARRIVAL) != 0;  // Q6 alternative
   const bool finiteM = cfg->M >= 0;
-  const int64_t M = cfg->M, C = cfg->C;
+  const int64_t kvb = cfg->kv_block > 1 ? cfg->kv_block : 1;  // Q15 alternative: KV block size
+  const int64_t M = finiteM ? cfg->M / kvb : cfg->M, C = cfg->C;   // the KV capacity in blocks
 
   std::memset(out, 0, sizeof(*out));
   for (int64_t x = 0; x < (int64_t)K * n; x++) {
@@ -272,13 +276,13 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
       out->status = OR_TOO_LONG;
       return 0;
     }
-  const int64_t wm = cfg->kv_watermark;  // Q16 alternative: free KVs a waiting admission must leave
+  const int64_t wm = blocks(cfg->kv_watermark, kvb);  // Q16 alternative: free blocks a waiting admission leaves
   for (int i = 0; i < n; i++) {
     int64_t peak = (int64_t)I[i] + O[i] - 1;  // peak KV usage I+O-1
     // a CONTEXT reserve (Orca) of S > M can never be admitted either (Q35); nor, with a watermark, a request
     // whose last refill (s = I + O - 1) could not be admitted into an empty cache
-    if ((finiteM && peak + wm > M) || (!cfg->chunked && peak > C) ||
-        (finiteM && cfg->reserve == OR_RESERVE_CONTEXT && cfg->S + wm > M)) {
+    if ((finiteM && blocks(peak, kvb) + wm > M) || (!cfg->chunked && peak > C) ||
+        (finiteM && cfg->reserve == OR_RESERVE_CONTEXT && blocks(cfg->S, kvb) + wm > M)) {
       out->status = OR_NEVER_FITS;
       return 0;
     }
@@ -309,7 +313,7 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
 
   std::vector<int64_t> evs;  // preemption events of the current step: (id, m discarded)
   auto preempt = [&](Req& r) {  // PAPER.md:1644-1646; refill semantics PAPER.md:1570
-    U -= held(r);
+    U -= held(r, kvb);
     r.refill += r.m;
     r.n_preempt++;
     out->preemptions++;
@@ -401,8 +405,8 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
         if (any_running && U + sumrem + seq_len(r) + rem > M) return;
       }
       // (3b) KV limit M: post-batch holdings sum max(reserved, m+c) <= M (Q13, Fig. 3)
-      int64_t newheld = std::max(r.st == WAITING ? initial_reserve(r) : r.reserved, r.m + c);
-      int64_t delta = newheld - held(r);
+      int64_t newheld = blocks(std::max(r.st == WAITING ? initial_reserve(r) : r.reserved, r.m + c), kvb);
+      int64_t delta = newheld - held(r, kvb);
       bool fits = true;
       // Q16 alternative: a waiting admission must also leave kv_watermark KVs free (it never preempts, Q5)
       if (finiteM && r.st == WAITING && U + delta + wm > M) return;
@@ -516,7 +520,7 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
           for (int k = 0; k < K; k++) r.t_first[k] = clock[k];
         }
         if (r.g == r.O) {
-          U -= held(r);
+          U -= held(r, kvb);
           r.st = DONE;
           for (int k = 0; k < K; k++) r.t_done[k] = clock[k];
           hist[bucket_of(r.I) * 18 + bucket_of(r.O)]++;
@@ -528,7 +532,7 @@ int oracle_run(const oracle_config_t* cfg, int32_t n, const int32_t* I, const in
     for (Req& q : R) q.preempted_now = false;
     // self-check: U equals the recomputed holdings (c.3 note)
     int64_t Uchk = 0;
-    for (const Req& q : R) Uchk += held(q);
+    for (const Req& q : R) Uchk += held(q, kvb);
     if (Uchk != U) return -100;
   }
 

@@ -35,7 +35,7 @@ typedef struct {
   int32_t reserve;   /* OR_RESERVE_*; != SEQ iff replacement == OR_PF (reading Q39) */
   int32_t knobs;     /* OR_KNOB_* alternative readings */
   int32_t max_seqs;  /* Q16 alternative: |B| <= max_seqs (0 = no cap) */
-  int32_t pad;
+  int32_t kv_block;  /* Q15 alternative: KVs allocated in blocks of this many tokens (0 / 1 = per token) */
   int64_t kv_watermark; /* Q16 alternative: KVs a waiting admission must leave free (0 = none) */
 } oracle_config_t;
 enum { OR_KNOB_HOL = 1 /* Q10 alternative: the first waiting candidate not admitted ends R_w's visit */,

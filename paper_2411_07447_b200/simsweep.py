@@ -30,7 +30,8 @@ class SimConfig(ctypes.Structure):
                 ("replacement", ctypes.c_int32), ("S", ctypes.c_int32), ("workload", ctypes.c_int32),
                 ("C", ctypes.c_int64), ("M", ctypes.c_int64), ("max_steps", ctypes.c_int64),
                 ("n_cost", ctypes.c_int32), ("cost", ctypes.c_int32 * SIM_MAX_COST), ("reserve", ctypes.c_int32),
-                ("knobs", ctypes.c_int32), ("max_seqs", ctypes.c_int32), ("kv_watermark", ctypes.c_int64)]
+                ("knobs", ctypes.c_int32), ("max_seqs", ctypes.c_int32), ("kv_watermark", ctypes.c_int64),
+                ("kv_block", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 KNOB_HOL = 1  # Q10 alternative: head-of-line blocking of the waiting group
@@ -187,9 +188,9 @@ def unit_cost(d: float = 1.0) -> SimCostModel:
 
 # ------------------------------------------------------------ configs
 def make_config(order, hybrid, chunked, replacement, C, M, S=4096, workload=0, cost=(0,),
-                max_steps=10_000_000, reserve=0, knobs=0, max_seqs=0, kv_watermark=0) -> SimConfig:
+                max_steps=10_000_000, reserve=0, knobs=0, max_seqs=0, kv_watermark=0, kv_block=0) -> SimConfig:
     c = SimConfig()
-    c.knobs, c.max_seqs, c.kv_watermark = int(knobs), int(max_seqs), int(kv_watermark)
+    c.knobs, c.max_seqs, c.kv_watermark, c.kv_block = int(knobs), int(max_seqs), int(kv_watermark), int(kv_block)
     c.order, c.hybrid, c.chunked, c.replacement = int(order), int(bool(hybrid)), int(bool(chunked)), int(replacement)
     c.reserve = int(reserve)
     c.S, c.workload, c.C, c.M, c.max_steps = int(S), int(workload), int(C), int(M), int(max_steps)

@@ -31,7 +31,7 @@ def cost_models():
 def oracle_config(c: simsweep.SimConfig) -> o.OracleConfig:
     return o.make_config(c.order, c.hybrid, c.chunked, c.replacement, C=c.C, M=c.M, S=c.S, max_steps=c.max_steps,
                          n_cost=c.n_cost, reserve=c.reserve, knobs=c.knobs, max_seqs=c.max_seqs,
-                         kv_watermark=c.kv_watermark)
+                         kv_watermark=c.kv_watermark, kv_block=c.kv_block)
 
 
 def _oracle_job(args):

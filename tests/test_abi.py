@@ -56,7 +56,7 @@ def test_struct_layout_matches_header(tmp_path):
             ctypes.sizeof(simsweep.SimBatchShape), ctypes.sizeof(simsweep.SimSloQuery), simsweep.SimSloQuery.tau.offset,
             ctypes.sizeof(simsweep.SimOptProblem), simsweep.SimOptProblem.C.offset, ctypes.sizeof(simsweep.SimOptResult)]
     assert got == want
-    assert got[0] == 88
+    assert got[0] == 96
 
 
 def test_version_and_strerror(L):

@@ -57,7 +57,8 @@ def test_random_knob_configs_verify(seed):
     assert r.status == "ok"
     outs = dict(t_first=list(r.t_first[0]), t_done=list(r.t_done[0]), n_preempt=list(r.n_preempt),
                 refill=list(r.refill))
-    assert verify(r.steps_list, list(wl.I), list(wl.O), list(wl.T), C, M, outs, hybrid=bool(hybrid)) == []
+    assert verify(r.steps_list, list(wl.I), list(wl.O), list(wl.T), C, cfg.M, outs, hybrid=bool(hybrid),
+                  kv_block=knobs.get("kv_block", 1)) == []
     if knobs["max_seqs"]:
         assert max(len(s["entries"]) for s in r.steps_list) <= knobs["max_seqs"]
 
@@ -81,3 +82,16 @@ def test_srf_visiting_in_admission_order():
     base = run([1, 2], [3, 3], repl="srf", M=4)
     alt = run([1, 2], [3, 3], repl="srf", M=4, knobs=o.KNOB_SRF_VISIT_ADMISSION)
     assert list(base.t_done[0]) == [5.0, 3.0] and list(alt.t_done[0]) == [3.0, 5.0]
+
+
+def test_paged_kv_blocks():
+    # vLLM, KV in blocks of 4 tokens, M = 12 tokens = 3 blocks: r0 = r1 = (I=4, O=2), r2 = (1, 1).  Step 1 admits
+    # all three (one block each: U = 3); r2 finishes (U = 2).  Step 2: r0's decode opens its second block (U = 3);
+    # r1's needs a fourth block, and with no newer admission to evict r1 self-preempts; r0 finishes.  Step 3: r1
+    # refills its 5 tokens (2 blocks) and finishes.  Per token (Q15 frozen) nothing is short: 2 steps.
+    per_token = run([4, 4, 1], [2, 2, 1], M=12)
+    paged = run([4, 4, 1], [2, 2, 1], M=12, kv_block=4)
+    assert (per_token.steps, per_token.preemptions) == (2, 0) and list(per_token.t_done[0]) == [2.0, 2.0, 1.0]
+    assert (paged.steps, paged.preemptions) == (3, 1) and list(paged.t_done[0]) == [2.0, 3.0, 1.0]
+    # the capacity is floor(M / b) blocks: a peak of 5 tokens needs 2 blocks, M = 7 tokens holds only one
+    assert run([3, 1], [3, 2], M=7).status == "ok" and run([3, 1], [3, 2], M=7, kv_block=4).status == "never_fits"

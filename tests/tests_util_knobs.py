@@ -25,5 +25,11 @@ def random_knob_case(seed):
     bits |= o.KNOB_SRF_VISIT_ADMISSION if repl != "nrf" and rng.random() < 0.5 else 0
     knobs = dict(knobs=bits, max_seqs=int(rng.integers(1, 6)) if rng.random() < 0.5 else 0,
                  kv_watermark=wm if M >= 0 else 0)
+    if repl != "srf_hist" and rng.random() < 0.4:  # paged KV (Q15 alternative): capacity floor(M / b) blocks
+        b = int(rng.integers(2, 9))
+        knobs["kv_block"] = b
+        if M >= 0:
+            need = -(-peak // b) + -(-wm // b)  # blocks of the largest peak plus the watermark
+            M = max(M, need * b + int(rng.integers(0, 3 * b)))
     cfg = o.make_config(order, hybrid, chunked, repl, C=C, M=M, S=96, **knobs)
     return wl, cfg, (C, M, hybrid), knobs

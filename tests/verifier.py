@@ -16,7 +16,7 @@ trace: list of dict(step, U, tok, start, d, entries=[(id, phase, c, m_before)],
 from __future__ import annotations
 
 
-def verify(steps, I, O, T, C, M, K_out=None, hybrid=True, reserve="seq", S=None):
+def verify(steps, I, O, T, C, M, K_out=None, hybrid=True, reserve="seq", S=None, kv_block=1):
     """Returns a list of violation strings (empty = valid).
 
     reserve: the Table 2 "Initial KV reserve" taken at (re)admission:
@@ -97,11 +97,12 @@ def verify(steps, I, O, T, C, M, K_out=None, hybrid=True, reserve="seq", S=None)
         if st.get("tok") is not None and st["tok"] != sum_c:
             v.append(f"step {j}: reported tok {st['tok']} != sum c {sum_c}")
         cmap = {i: c for (i, _, c, _) in ents}
-        U = sum(max(res[i], m[i] + cmap.get(i, 0)) for i in range(n) if running[i])
+        b = max(kv_block, 1)  # paged KV (Q15 alternative): holdings in blocks of b tokens, capacity floor(M / b)
+        U = sum(-(-max(res[i], m[i] + cmap.get(i, 0)) // b) for i in range(n) if running[i])
         if st.get("U") is not None and st["U"] != U:
             v.append(f"step {j}: reported U {st['U']} != recomputed {U}")
-        if M >= 0 and U > M:  # Eq. (7) memory
-            v.append(f"step {j}: KV holdings {U} > M = {M}")
+        if M >= 0 and U > M // b:  # Eq. (7) memory
+            v.append(f"step {j}: KV holdings {U} > M = {M // b}")
         end = start + d
         for (i, ph, c, mb) in ents:
             s = I[i] + g[i]
