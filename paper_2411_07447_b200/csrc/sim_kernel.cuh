@@ -61,9 +61,9 @@ struct Scal {
   int runEx;
   long long pref[6];  // exclusive prefixes (c, dKV, admitted-waiting, admitted, SRF+Hist rem) at the break
   long long featsum[16];
-  long long wred[16][18];  // per-warp partials of the process pass
+  long long wred[16][20];  // per-warp partials of the process pass
   int next, new_next, lo, n_done, n_run, nW, nrank, minSW, n_ev, n_vic, nB, nRd;
-  int cf_red[32][8];
+  int cf_red[32][10];
   int pa, cut, h_pre, vmin, wstale, wfirst;
   int vt, status, any_pre, cur, wbuilt, arena;
   int w_dirty, p_dirty, r_dirty, o_dirty, rank_dirty, removals;

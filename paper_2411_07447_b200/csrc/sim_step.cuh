@@ -77,7 +77,11 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   const sim_workload_t wl = p.wls[cfg.workload];
   const int n = wl.n;
   const int K = cfg.n_cost;
-  const int M = cfg.M >= 0 ? (int)cfg.M : 0, C = (int)cfg.C;  // host-validated < 2^30
+  // Q15 alternative (paged KV): every KV quantity below (U, M, holdings, deltas) counts blocks of kvb tokens
+  const bool paged = KN && cfg.kv_block > 1;
+  const int kvb = paged ? cfg.kv_block : 1;
+  auto blk = [&](int x) -> int { return paged ? (x + kvb - 1) / kvb : x; };
+  const int M = cfg.M >= 0 ? (int)(cfg.M / kvb) : 0, C = (int)cfg.C;  // host-validated < 2^30
   const bool finiteM = cfg.M >= 0, hybrid = cfg.hybrid != 0, chunked = cfg.chunked != 0;
   const int order = cfg.order;
   const bool srf = cfg.replacement == SIM_SRF || cfg.replacement == SIM_SRF_HIST;
@@ -99,7 +103,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   const bool q3alt = KN && (cfg.knobs & SIM_KNOB_SRF_VISIT_ADMISSION) != 0;
   const bool srf_order = srf && !q3alt;
   const int capB = cfg.max_seqs > 0 ? (int)cfg.max_seqs : 0x3fffffff;
-  const int Mw = finiteM ? M - (int)cfg.kv_watermark : 0x3fffffff;  // the KV bound of a waiting admission
+  const int Mw = finiteM ? M - blk((int)cfg.kv_watermark) : 0x3fffffff;  // the KV bound of a waiting admission
   const long long row0 = p.row_off[ci], tim0 = p.tim_off[ci];
   double* tf = p.req.t_first + tim0;
   double* td = p.req.t_done + tim0;
@@ -119,8 +123,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   for (int i = tid; i < n; i += NT) {
     long long pk = (long long)wl.I[i] + wl.O[i] - 1;  // peak KV usage
     bad_long |= pk > cfg.S;
-    bad_fit |= (finiteM && pk + cfg.kv_watermark > cfg.M) || (!chunked && pk > cfg.C);
-    bad_fit |= finiteM && cfg.reserve == SIM_RESERVE_CONTEXT && cfg.S + cfg.kv_watermark > cfg.M;  // never fits (Q35)
+    bad_fit |= (finiteM && blk((int)pk) + blk((int)cfg.kv_watermark) > M) || (!chunked && pk > cfg.C);
+    bad_fit |= finiteM && cfg.reserve == SIM_RESERVE_CONTEXT && blk(cfg.S) + blk((int)cfg.kv_watermark) > M;  // Q35
   }
   bad_long = __syncthreads_or(bad_long);
   bad_fit = __syncthreads_or(bad_fit);
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     };
     auto preempt = [&](int v) {  // thread 0 only (refill P:1570)
       const int4 rc = s_rec[v];
-      U -= max(rc.w, rc.z);
+      U -= blk(max(rc.w, rc.z));
       if (hist) Rs -= max(S.pred[bucket_of(rc.x)] - rc.y, 0);
       const int idx = lo + ((v - lo) & (CAP - 1));
       atomicAdd(&npre[idx], 1ull);
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         if (n_running > 0 && (long long)U + Rs + s + rem > M) return;  // deferred (Q31)
       }
       const int rw = isW ? rnew(rc, sl) : rc.w;
-      const int nh = max(rw, rc.z + c), held = isW ? 0 : max(rc.w, rc.z), delta = nh - held;
+      const int nh = blk(max(rw, rc.z + c)), held = isW ? 0 : blk(max(rc.w, rc.z)), delta = nh - held;
       if (KN && isW && finiteM && U + delta > Mw) return;  // watermark knob (a waiting candidate never preempts, Q5)
       while (finiteM && U + delta > M) {
         if (isW || pf) return;  // holds no KVs (Q5) / preemption-free: skipped
@@ -418,7 +422,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       while (i0 < b1) {
         PROF_CNT(13, 1);
         if (overWin) {  // the rest of R_w fails a monotone check: stop
-          const bool wrej = (!hybrid && bph == PH_DEC) || (KN && nB >= capB) || (finiteM && (long long)U + minSW > (KN ? Mw : M)) ||
+          const bool wrej = (!hybrid && bph == PH_DEC) || (KN && nB >= capB) || (finiteM && (long long)U + blk(minSW) > (KN ? Mw : M)) ||
                             (chunked ? tok >= C : minSW > C - tok);
           if (wrej) break;
         }
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           ok = ok && !(anyRun0 && (long long)U + Rs + s + rem > M);
         }
         const int rw = isW ? rnew(rc, sl < 0 ? 0 : sl) : rc.w;
-        const int delta = max(rw, rc.z + c) - (isW ? 0 : max(rc.w, rc.z));
+        const int delta = blk(max(rw, rc.z + c)) - (isW ? 0 : blk(max(rc.w, rc.z)));
         if (KN && isW && finiteM && U + delta > Mw) ok = false;  // watermark knob
         const bool kvfail = finiteM && U + delta > M;
         const int kind = !ok ? K_NONE : (kvfail ? ((isW || pf) ? K_NONE : K_EVENT) : K_MARK);
@@ -537,50 +541,59 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       const int nact = min(NW, (nrun + 32 * IPT_ - 1) / (32 * IPT_));
       TMARK(10);
       const bool act = wid < nact;
-      // (i) reverse scan over run positions of (held, is-head): RS(q) = sum held at >= q, HS(q) = heads at >= q
-      int hv[IPT_], rsv[IPT_], hsv[IPT_], ls = 0, lh = 0;
+      // (i) reverse scan over run positions of (held, is-head): RS(q) = sum held at >= q, HS(q) = heads at >= q.
+      // Paged KV (Q15 alternative): a head needs 0 or 1 new block, so the closed form counts NS(i), the blocks
+      // heads 1..i need (= i per token), with NSS(q) = the needs at >= q from a third scan component.
+      int hv[IPT_], rsv[IPT_], hsv[IPT_], nv[IPT_], nsv[IPT_], ls = 0, lh = 0, ln = 0;
       bool hh[IPT_];
       int16_t sls[IPT_];
 #pragma unroll
       for (int j = 0; j < IPT_; j++) {
         const int q = nrun - 1 - (tid * IPT_ + j);
-        hv[j] = 0, hh[j] = false, sls[j] = 0;
+        hv[j] = 0, hh[j] = false, sls[j] = 0, nv[j] = 0;
         if (q >= 0) {
           const int sl = run[q];
           sls[j] = (int16_t)sl;
           const int4 rc = s_rec[sl];
-          hv[j] = max(rc.w, rc.z);
+          hv[j] = blk(max(rc.w, rc.z));
           hh[j] = (s_fl[sl] & F_FILLED) != 0;
+          if (paged && hh[j]) nv[j] = blk(max(rc.w, rc.z + 1)) - hv[j];
         }
-        ls += hv[j], lh += hh[j];
+        ls += hv[j], lh += hh[j], ln += nv[j];
       }
-      int xs = ls, xh = lh;
+      int xs = ls, xh = lh, xn = ln;
       if (act) {
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int ys = __shfl_up_sync(FM, xs, o), yh = __shfl_up_sync(FM, xh, o);
           if (lane >= o) xs += ys, xh += yh;
+          if (paged) {
+            const int yn = __shfl_up_sync(FM, xn, o);
+            if (lane >= o) xn += yn;
+          }
         }
-        if (lane == 31) S.cf_red[wid][0] = xs, S.cf_red[wid][1] = xh;
+        if (lane == 31) S.cf_red[wid][0] = xs, S.cf_red[wid][1] = xh, S.cf_red[wid][8] = xn;
       }
       __syncthreads();
-      int os = xs - ls, oh = xh - lh, k = 0;
+      int os = xs - ls, oh = xh - lh, on = xn - ln, k = 0, kn = 0;
       for (int w = 0; w < nact; w++) {
-        const int a0 = S.cf_red[w][0], a1 = S.cf_red[w][1];
-        if (w < wid) os += a0, oh += a1;
-        k += a1;
+        const int a0 = S.cf_red[w][0], a1 = S.cf_red[w][1], a8 = paged ? S.cf_red[w][8] : 0;
+        if (w < wid) os += a0, oh += a1, on += a8;
+        k += a1, kn += a8;
       }
 #pragma unroll
-      for (int j = 0; j < IPT_; j++) os += hv[j], oh += hh[j], rsv[j] = os, hsv[j] = oh;
+      for (int j = 0; j < IPT_; j++) os += hv[j], oh += hh[j], on += nv[j], rsv[j] = os, hsv[j] = oh, nsv[j] = on;
+      if (!paged) kn = k;
+      auto NS = [&](int j) { return paged ? kn - nsv[j] + nv[j] : k - hsv[j] + 1; };  // blocks heads 1..i need
       TMARK(11);
       // (ii) a_kv = #{heads i : F + RS(p_i + 1) >= i}, i = k - HS(p_i) + 1 (monotone in i)
       int akv = k;
-      if (fM && F < k) {  // with F >= k every head passes (F + RS(p_i + 1) >= F >= k >= i): no pass needed
+      if (fM && F < kn) {  // with F >= kn every head passes (F + RS(p_i + 1) >= F >= kn >= NS(i)): no pass needed
         if (act) {
           int cnt = 0;
 #pragma unroll
           for (int j = 0; j < IPT_; j++)
-            if (hh[j]) cnt += F + (rsv[j] - hv[j]) >= k - hsv[j] + 1;
+            if (hh[j]) cnt += F + (rsv[j] - hv[j]) >= NS(j);
           cnt = (int)__reduce_add_sync(FM, (unsigned)cnt);
           if (lane == 0) S.cf_red[wid][2] = cnt;
         }
@@ -590,8 +603,22 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       }
       TMARK(12);
       const int a = min(min(akv, T), k);
-      // (iii) q* = max{q : F + RS(q) >= a}; the position of head a+1
-      const bool needq = fM && F < a;
+      int NSa = a;  // blocks heads 1..a need (a per token)
+      if (paged) {
+        if (act) {
+          int sn = 0;
+#pragma unroll
+          for (int j = 0; j < IPT_; j++)
+            if (hh[j] && k - hsv[j] + 1 <= a) sn += nv[j];
+          sn = (int)__reduce_add_sync(FM, (unsigned)sn);
+          if (lane == 0) S.cf_red[wid][9] = sn;
+        }
+        __syncthreads();
+        NSa = 0;
+        for (int w = 0; w < nact; w++) NSa += S.cf_red[w][9];
+      }
+      // (iii) q* = max{q : F + RS(q) >= NS(a)}; the position of head a+1
+      const bool needq = fM && F < NSa;
       const bool needp = fM && a == akv && a < min(k, T);
       int qs = nrun, selfp = -1;
       if (needq || needp) {
@@ -601,7 +628,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           for (int j = 0; j < IPT_; j++) {
             const int q = nrun - 1 - (tid * IPT_ + j);
             if (q >= 0) {
-              if (needq) cq += F + rsv[j] >= a;
+              if (needq) cq += F + rsv[j] >= NSa;
               if (hh[j] && k - hsv[j] + 1 == a + 1) S.pa = q;
             }
           }
@@ -670,7 +697,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         rp_first = min(rp_first, S.cf_red[w][7]);
       }
       tok += a;
-      U += (kv1 ? a : 0) - teh;
+      U += (kv1 ? NSa : 0) - teh;
       nB += a;
       n_running -= tev;
       Rs -= ter;
@@ -702,7 +729,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       if (overWin) wnext = b0;
       for (int i0 = b0; i0 < b1; i0 += 32) {
         if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C) || (KN && nB >= capB)) return;  // all remaining fail
-        if (overWin && ((finiteM && (long long)U + minSW > (KN ? Mw : M)) || (!chunked && minSW > C - tok))) return;
+        if (overWin && ((finiteM && (long long)U + blk(minSW) > (KN ? Mw : M)) || (!chunked && minSW > C - tok))) return;
         PROF_CNT(13, 1);
         const int i = i0 + lane;
         int sl = -1;
@@ -721,7 +748,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         const int4 rc = s_rec[sl < 0 ? 0 : sl];
         const uint8_t fl = s_fl[sl < 0 ? 0 : sl];
         const int s = rc.x + rc.y, avail = s - rc.z;
-        const int dkv = overWin ? rnew(rc, sl < 0 ? 0 : sl) : 0;  // KV delta: the initial reserve >= s >= c (Q13)
+        const int rtok = overWin ? rnew(rc, sl < 0 ? 0 : sl) : 0;  // the initial reserve >= s >= c (Q13), tokens
+        const int dkv = blk(rtok);                                   // its KV delta (blocks when paged)
         const int rem = (hist && overWin) ? max(S.pred[bucket_of(rc.x)] - rc.y, 0) : 0;
         bool alive = sl >= 0, admitted = false;
         for (;;) {
@@ -738,7 +766,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             break;
           }
           const int cc = fit ? avail : 0, rr = fit ? rem : 0, dk = fit ? dkv : 0;
-          const bool scand = overWin && !kv1;  // KV deltas differ from c only under a PEAK / CONTEXT reserve
+          const bool scand = overWin && (!kv1 || paged);  // KV deltas differ from c under PEAK / CONTEXT or in blocks
           int xc = cc, xr = rr, xd = dk;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -778,7 +806,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             s_bl[nB + ek] = (int16_t)sl;
             if (overWin) {
               s_seq[sl] = seq + ek + 1;
-              s_rec[sl] = make_int4(rc.x, rc.y, 0, dkv);
+              s_rec[sl] = make_int4(rc.x, rc.y, 0, rtok);
               s_fl[sl] = ST_RUN | F_INB | (fl & F_FIRST);
               s_new[n_new + ek] = (int16_t)sl;
             } else {
@@ -846,7 +874,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           if (rp_first < nrun) warp_np(2, rp_first, nrun);
           int wdone = nW == 0;
           if (!wdone) {
-            const bool wrej = (!hybrid && bph == PH_DEC) || (KN && nB >= capB) || (finiteM && (long long)U + minSW > (KN ? Mw : M)) ||
+            const bool wrej = (!hybrid && bph == PH_DEC) || (KN && nB >= capB) || (finiteM && (long long)U + blk(minSW) > (KN ? Mw : M)) ||
                               (chunked ? tok >= C : minSW > C - tok);
             long long amax = chunked ? (long long)(C - tok) : (long long)(C - tok) / max(minSW, 1);
             if (finiteM) amax = min(amax, (long long)(M - U) / max(minSW, 1));
@@ -873,7 +901,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       {  // warp-level mode when few candidates need a decision
         int mode = 0, lim = nP;
         if (pos >= wbeg && pos < wend) {
-          const bool wrej = (!hybrid && bph == PH_DEC) || (KN && nB >= capB) || (finiteM && (long long)U + minSW > (KN ? Mw : M)) ||
+          const bool wrej = (!hybrid && bph == PH_DEC) || (KN && nB >= capB) || (finiteM && (long long)U + blk(minSW) > (KN ? Mw : M)) ||
                             (chunked ? tok >= C : minSW > C - tok);
           if (wrej) {  // every remaining waiting candidate fails a monotone check: skip the group
             pos = wend;
@@ -961,7 +989,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           ok = ok && !(anyRun0 && (long long)U + Rs + s + rem > M);
         }
         const int rw = isW ? rnew(rc, slv[j] < 0 ? 0 : slv[j]) : rc.w;
-        const int delta = max(rw, rc.z + c) - (isW ? 0 : max(rc.w, rc.z));
+        const int delta = blk(max(rw, rc.z + c)) - (isW ? 0 : blk(max(rc.w, rc.z)));
         if (KN && isW && finiteM && U + delta > Mw) ok = false;  // watermark knob
         const bool kvfail = finiteM && U + delta > M;
         kind[j] = !ok ? K_NONE : (kvfail ? ((isW || pf) ? K_NONE : K_EVENT) : K_MARK);
@@ -1106,7 +1134,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     // ---- (4) a9 + a10: Process(B) and the exact integer features in one pass over B ----
     {
       unsigned N = 0, np_ = 0, cp = 0, mp = 0, nd = 0, md = 0, freed = 0, ndone = 0, mdn = 0, nfill = 0;
-      int minrem = NOBRK;
+      int minrem = NOBRK, minfree = NOBRK;  // minfree (paged KV): decodes left before some entry opens a block
       long long c2 = 0, mc = 0, pcm = 0, pce[SIM_MAX_COST] = {0, 0, 0, 0};
       const int nwa = min(NW, (nB + 31) >> 5);  // warps holding batch entries; the others only meet the barrier
       if (wid < nwa) {
@@ -1153,7 +1181,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             done = true;
             fl = (fl & ~ST_MASK) | ST_DONE;
             evc |= 2;
-            freed += max(rc.w, m);
+            freed += blk(max(rc.w, m));
             ndone++;
             if (hist) atomicAdd(&S.hist[bucket_of(rc.x) * 18 + bucket_of(O)], 1);
           }
@@ -1161,6 +1189,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         }
         if (!done) {
           minrem = min(minrem, O - g);
+          if (paged) minfree = min(minfree, blk(max(rc.w, m)) * kvb - m);
           mdn += m;
         }
         s_rec[sl] = make_int4(rc.x, g, m, rc.w);
@@ -1172,6 +1201,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       freed = __reduce_add_sync(FM, freed), ndone = __reduce_add_sync(FM, ndone);
       mdn = __reduce_add_sync(FM, mdn), nfill = __reduce_add_sync(FM, nfill);
       minrem = (int)__reduce_min_sync(FM, (unsigned)minrem);
+      if (paged) minfree = (int)__reduce_min_sync(FM, (unsigned)minfree);
       if (np_ > 0) {  // prefill squares: 64-bit, only in warps holding prefill entries
         c2 = warp_sum(c2);
         mc = warp_sum(mc);
@@ -1184,7 +1214,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       if (lane == 0) {  // per-warp partials (plain stores; folded by warp 0 after the barrier)
         long long* w = S.wred[wid];
         w[0] = N, w[1] = np_, w[2] = cp, w[3] = mp, w[4] = nd, w[5] = md, w[6] = freed, w[7] = ndone;
-        w[8] = mdn, w[9] = nfill, w[10] = minrem, w[11] = c2, w[12] = mc, w[13] = pcm;
+        w[8] = mdn, w[9] = nfill, w[10] = minrem, w[11] = c2, w[12] = mc, w[13] = pcm, w[18] = minfree;
 #pragma unroll
         for (int k = 0; k < SIM_MAX_COST; k++) w[14 + k] = pce[k];
       }
@@ -1210,18 +1240,18 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         }
       }
       __syncthreads();
-      long long tt[18];
+      long long tt[19];
       TMARK(33);
       if (wid == 0) {  // lane z folds column z of the per-warp partials; thread 0 gathers them
-        long long v = lane == 10 ? (long long)NOBRK : 0;
-        if (lane < 18) {
+        long long v = (lane == 10 || lane == 18) ? (long long)NOBRK : 0;
+        if (lane < (paged ? 19 : 18)) {
           for (int w = 0; w < nwa; w++) {
             const long long x = S.wred[w][lane];
-            v = lane == 10 ? min(v, x) : v + x;
+            v = (lane == 10 || lane == 18) ? min(v, x) : v + x;
           }
         }
 #pragma unroll
-        for (int z = 0; z < 18; z++) tt[z] = __shfl_sync(FM, v, z);
+        for (int z = 0; z < 19; z++) tt[z] = __shfl_sync(FM, v, z);
       }
       TMARK(34);
       if (tid == 0) {
@@ -1255,7 +1285,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           long long Lr = 0;
           if (ndn == 0 && f.np == 0 && !S.any_pre && f.nd > 0) {
             Lr = tt[10];
-            if (finiteM && kv1) Lr = min(Lr, (long long)(M - Uafter) / f.nd);
+            if (paged)  // no entry opens a block during the run: U stays constant
+              Lr = min(Lr, tt[18]);
+            else if (finiteM && kv1)
+              Lr = min(Lr, (long long)(M - Uafter) / f.nd);
             Lr = min(Lr, cfg.max_steps - S.steps);
           }
           S.runL = Lr;
@@ -1302,7 +1335,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       if (Lr > 0) {
         constexpr int DB = CAP / 2;
         const int cmax = min(NT, DB / K);
-        const long long ndd = S.last_nd, MD = S.runMD, U0 = S.U, du = kv1 ? ndd : 0;  // KV growth per run step
+        const long long ndd = S.last_nd, MD = S.runMD, U0 = S.U, du = (kv1 && !paged) ? ndd : 0;  // KV growth/step
         long long E = 0;
         while (E < Lr) {
           const int chunk = (int)min((long long)cmax, Lr - E);
@@ -1362,7 +1395,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
               const int idx = lo + ((sl - lo) & (CAP - 1));
               s_fl[sl] = (s_fl[sl] & ~ST_MASK) | ST_DONE;
               for (int k = 0; k < K; k++) td[(long long)k * n + idx] = S.clock[k];
-              fr2 += max(rc.w, m);
+              fr2 += blk(max(rc.w, m));
               nd2++;
               if (hist) atomicAdd(&S.hist[bucket_of(rc.x) * 18 + bucket_of(O)], 1);
             }

@@ -56,7 +56,9 @@ __host__ __device__ inline int variant_of(int n) { return n <= 1024 ? 0 : (n <= 
 constexpr int N_SIZES = 3;
 // configs with an alternative-reading knob run in a second instance of each size (KN = true), so that the
 // default instances carry none of the knob checks
-__host__ __device__ inline bool has_knobs(const sim_config_t& c) { return c.knobs || c.max_seqs || c.kv_watermark; }
+__host__ __device__ inline bool has_knobs(const sim_config_t& c) {
+  return c.knobs || c.max_seqs || c.kv_watermark || c.kv_block > 1;
+}
 constexpr int N_VARIANTS = 2 * N_SIZES;
 
 #ifndef SIM_NT_SMALL
@@ -247,7 +249,8 @@ static int validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload
     if ((c.replacement == SIM_PF) != (c.reserve != SIM_RESERVE_SEQ)) return SIM_EINVAL;  // Q39
     if ((c.knobs & ~(SIM_KNOB_HOL | SIM_KNOB_NRF_ARRIVAL | SIM_KNOB_SRF_VISIT_ADMISSION)) || c.max_seqs < 0 ||
         c.kv_watermark < 0 || c.kv_watermark >= (1 << 30) || ((c.knobs & SIM_KNOB_NRF_ARRIVAL) && c.replacement != SIM_NRF) ||
-        ((c.knobs & SIM_KNOB_SRF_VISIT_ADMISSION) && c.replacement != SIM_SRF && c.replacement != SIM_SRF_HIST))
+        ((c.knobs & SIM_KNOB_SRF_VISIT_ADMISSION) && c.replacement != SIM_SRF && c.replacement != SIM_SRF_HIST) ||
+        c.kv_block < 0 || c.kv_block > (1 << 16) || (c.kv_block > 1 && c.replacement == SIM_SRF_HIST))
       return SIM_EINVAL;  // alternative-reading knobs
     if ((c.hybrid != 0 && c.hybrid != 1) || (c.chunked != 0 && c.chunked != 1)) return SIM_EINVAL;
     if (c.C < 1 || c.C > (1 << 30) || c.M > (1 << 30) || c.S < 1 || c.S > 262143 || c.max_steps < 1) return SIM_EINVAL;

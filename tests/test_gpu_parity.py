@@ -329,13 +329,16 @@ def test_knob_hand_traces_and_grid_sample():
              (cfg(0, 0, 0, 0, 4096, -1, max_seqs=2), W([2, 2, 2], [2, 2, 2]), UNIT),
              (cfg(0, 0, 0, 0, 4096, 10, kv_watermark=3), W([4, 4], [2, 2]), UNIT),
              (cfg(0, 0, 0, 0, 4096, 5, knobs=simsweep.KNOB_NRF_ARRIVAL), W([3, 3, 1], [1, 2, 2]), UNIT),
-             (cfg(0, 0, 0, 1, 4096, 4, knobs=simsweep.KNOB_SRF_VISIT_ADMISSION), W([1, 2], [3, 3]), UNIT)]
+             (cfg(0, 0, 0, 1, 4096, 4, knobs=simsweep.KNOB_SRF_VISIT_ADMISSION), W([1, 2], [3, 3]), UNIT),
+             (cfg(0, 0, 0, 0, 4096, 12, kv_block=4), W([4, 4, 1], [2, 2, 1]), UNIT)]
     for name in ("vllm", "sarathi", "vllm-srf", "sarathi-srf"):
         for (I, O) in ((16, 256), (128, 512), (1, 1024)):
             arr = simsweep.KNOB_NRF_ARRIVAL if name == "vllm" else (simsweep.KNOB_SRF_VISIT_ADMISSION if "srf" in name else 0)
             cases.append((simsweep.preset_config(name, 100_000, knobs=simsweep.KNOB_HOL | arr, max_seqs=256,
                                                  kv_watermark=1000), workloads.fixed(I, O, 1024), A100))
+            cases.append((simsweep.preset_config(name, 100_000, kv_block=16), workloads.fixed(I, O, 1024), A100))
     g, ors = assert_parity(cases)
     assert [int(g.results["steps"][i]) for i in range(3)] == [4, 4, 4]
     assert g.request_times(3)[1][0].tolist() == [1.0, 3.0, 4.0]
     assert g.request_times(4)[1][0].tolist() == [3.0, 5.0]
+    assert g.request_times(5)[1][0].tolist() == [2.0, 3.0, 1.0] and int(g.results["preemptions"][5]) == 1
