@@ -342,3 +342,18 @@ def test_knob_hand_traces_and_grid_sample():
     assert g.request_times(3)[1][0].tolist() == [1.0, 3.0, 4.0]
     assert g.request_times(4)[1][0].tolist() == [3.0, 5.0]
     assert g.request_times(5)[1][0].tolist() == [2.0, 3.0, 1.0] and int(g.results["preemptions"][5]) == 1
+
+
+def test_knobs_on_the_online_traces():
+    # the knob kernel instances of the n <= 4096 (LongForm, n = 2000) and global-arena (AzureConv, n = 19 700)
+    # variants, with vLLM's system defaults: head-of-line blocking, FCFS running order, max_num_seqs 256, a
+    # watermark and blocks of 16 tokens
+    lf, az = workloads.longform(5), workloads.azureconv(1)
+    vllm_sys = dict(knobs=simsweep.KNOB_HOL | simsweep.KNOB_NRF_ARRIVAL, max_seqs=256, kv_watermark=1000, kv_block=16)
+    cases = [(simsweep.preset_config("vllm", 100_000, S=131072, **vllm_sys), lf, A100),
+             (simsweep.preset_config("sarathi-srf", 100_000, S=131072, knobs=simsweep.KNOB_SRF_VISIT_ADMISSION,
+                                     max_seqs=128, kv_block=16), lf, A100),
+             (simsweep.preset_config("vllm", 100_000, S=131072, **vllm_sys), az, A100),
+             (simsweep.preset_config("sarathi", 100_000, S=131072, knobs=simsweep.KNOB_HOL, kv_watermark=500), az, A100)]
+    g, _ = assert_parity(cases, processes=len(cases))
+    assert all(g.status(i) == "ok" for i in range(len(cases)))
