@@ -728,6 +728,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       bool wcont = overWin;  // every waiting request at offsets [b0, i0) was admitted
       if (overWin) wnext = b0;
       for (int i0 = b0; i0 < b1; i0 += 32) {
+        TMARK(70);
         if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C) || (KN && nB >= capB)) return;  // all remaining fail
         if (overWin && ((finiteM && (long long)U + blk(minSW) > (KN ? Mw : M)) || (!chunked && minSW > C - tok))) return;
         PROF_CNT(13, 1);
@@ -744,6 +745,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             const int s2 = cand(i);
             if (!(s_fl[s2] & F_PRE)) sl = s2;
           }
+        }
+        if (!__any_sync(FM, sl >= 0)) {  // no candidate in this chunk: nothing to admit or reject
+          if (wcont) wnext = min(i0 + 32, b1);
+          continue;
         }
         const int4 rc = s_rec[sl < 0 ? 0 : sl];
         const uint8_t fl = s_fl[sl < 0 ? 0 : sl];
@@ -876,11 +881,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           if (!wdone) {
             const bool wrej = (!hybrid && bph == PH_DEC) || (KN && nB >= capB) || (finiteM && (long long)U + blk(minSW) > (KN ? Mw : M)) ||
                               (chunked ? tok >= C : minSW > C - tok);
-            long long amax = chunked ? (long long)(C - tok) : (long long)(C - tok) / max(minSW, 1);
-            if (finiteM) amax = min(amax, (long long)(M - U) / max(minSW, 1));
+            const long long q1 = max(minSW, 1);  // at most 128 admissions possible (no 64-bit division)
+            const bool few = (chunked ? (long long)(C - tok) <= 128 : (long long)(C - tok) < 129 * q1) ||
+                             (finiteM && (long long)(M - U) < 129 * q1);
             if (wrej) {
               wdone = 1;
-            } else if (amax <= 128 || nx1 - lo <= WARP_MAX) {
+            } else if (few || nx1 - lo <= WARP_MAX) {
               warp_np(1, w0, nx1 - lo);
               wdone = 1;
             }
@@ -908,9 +914,11 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             continue;
           }
           if (pos == wbeg) {
-            long long amax = chunked ? (long long)(C - tok) : (long long)(C - tok) / max(minSW, 1);
-            if (finiteM) amax = min(amax, (long long)(M - U) / max(minSW, 1));
-            if (amax <= 128 || nx1 - lo <= WARP_MAX) mode = 2, lim = wend;
+            // at most 128 admissions possible (floor(x / q) <= 128 <=> x < 129 q): warp-level admission
+            const long long q1 = max(minSW, 1);
+            const bool few = (chunked ? (long long)(C - tok) <= 128 : (long long)(C - tok) < 129 * q1) ||
+                             (finiteM && (long long)(M - U) < 129 * q1);
+            if (few || nx1 - lo <= WARP_MAX) mode = 2, lim = wend;
           }
         } else if (!rank) {
           const int rend = order == SIM_ORDER_DECODE_FIRST ? len0 : nP;  // end of the running group(s)
@@ -921,6 +929,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         }
         if (mode) {
           PROF_CNT(11, 1);
+          TMARK(60 + mode);
           if (wid == 0) {
             if (mode == 2)
               warp_np(1, w0, nx1 - lo);
@@ -934,11 +943,14 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
               if (wnext >= 0) S.wfirst = lo + wnext;
             }
           }
+          TMARK(65);
           __syncthreads();
+          TMARK(66);
           tok = S.r_tok, U = S.r_U, seq = S.r_seq, Rs = S.r_Rs, nB = S.r_nB;
           n_new = S.r_new, n_running = S.r_running, bph = S.r_bph, wblk = S.r_wblk;
           pos = lim;
           __syncthreads();
+          TMARK(67);
           continue;
         }
       }
