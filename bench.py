@@ -350,9 +350,13 @@ def bench_ours(args, rank, world, local_rank):
         jobs = oracle_sample(stride, M=rank_M(0))
         cores = min(host_cores(), len(jobs))
         s, dt = run_oracle(jobs, cores)
+        jobs1 = oracle_sample(48, M=rank_M(0))  # one core: "single-thread" next to "all host cores"
+        s1, dt1 = run_oracle(jobs1, 1)
         line["cpu_baseline"] = {"value": s / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
                                 "sample": f"every {stride}th simulation of the grid ({len(jobs)} of 1452), "
-                                          f"{s} steps in {dt:.2f} s wall on {cores} host cores"}
+                                          f"{s} steps in {dt:.2f} s wall on {cores} host cores",
+                                "value_1core": s1 / dt1,
+                                "sample_1core": f"every 48th simulation ({len(jobs1)}), {s1} steps in {dt1:.2f} s on 1 core"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
