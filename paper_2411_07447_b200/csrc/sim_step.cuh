@@ -1294,8 +1294,16 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           // j+1 repeats it exactly (waiting candidates were rejected for reasons that persist: KV and SRF+Hist
           // deferral are monotone in U, token/hybrid rejections are unchanged) until a completion, the KV
           // limit (U + k n_d <= M) or an arrival.  Those steps are charged below without re-forming batches.
+          // After an eviction step the same holds when every running request was a decode in B and every
+          // waiting candidate (the victims included) fails the KV test at step j+1 already (U only grows).
+          bool steady = ndn == 0 && f.np == 0 && f.nd > 0;
+          if (steady && S.any_pre) {
+            const int nWn = nW - n_new + S.n_vic, minSWn = min(minSW, vmin);
+            steady = !rank && f.nd == nrun - S.n_vic &&
+                     (nWn == 0 || (finiteM && (long long)Uafter + blk(minSWn) > (KN ? Mw : M)));
+          }
           long long Lr = 0;
-          if (ndn == 0 && f.np == 0 && !S.any_pre && f.nd > 0) {
+          if (steady) {
             Lr = tt[10];
             if (paged)  // no entry opens a block during the run: U stays constant
               Lr = min(Lr, tt[18]);
