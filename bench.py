@@ -265,7 +265,9 @@ def bench_ours(args, rank, world, local_rank):
     # sweep can never be shorter than its longest simulation (each simulation is one dependent chain of steps).
     critical = None
     if rank == 0 and not args.no_critical:
-        top = order[:16]  # LPT order: the largest step-count estimates first
+        # the 48 largest step-count estimates plus the 16 largest visit counts of this sweep (the estimate misses
+        # vLLM's preemption thrash at small I, whose steps are all full steps)
+        top = list(dict.fromkeys([int(i) for i in order[:48]] + [int(i) for i in np.argsort(-res["visits"])[:16]]))
         alone = []
         for i in top:
             one = simsweep.DeviceSweep([simsweep.SimConfig.from_buffer_copy(cfgs[int(i)])], wls, cms, device=dev)
@@ -279,7 +281,7 @@ def bench_ours(args, rank, world, local_rank):
         lm, li = max(alone)
         critical = {"longest_simulation_alone_ms": lm, "longest_simulation": "%s I=%d O=%d" % labels[li],
                     "its_steps": int(res["steps"][li]), "sweep_kernel_over_longest": kms / lm,
-                    "probed": "the 16 simulations with the largest LPT estimates, each launched alone"}
+                    "probed": f"{len(top)} simulations (largest LPT estimates and visit counts), each launched alone"}
 
     # e2e: the public host API (sim_sweep: pinned H2D + kernel + D2H, blocking), every step
     e2e = None
