@@ -193,6 +193,50 @@ int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* 
                      sim_result_t* d_results, sim_request_out_t d_req, void* d_workspace,
                      int64_t workspace_bytes, void* stream);
 
+/* ---- per-step schedule trace of one simulation (the schedule log of PAPER.md:714-719) ----
+ * One record per step j (a batch B_j; an idle arrival jump is not a step), in step order; the entries of B_j in
+ * admission order (Algorithm 1's B); the preemptions of step j in the order they happened
+ * (PAPER.md:1644-1646). */
+typedef struct {
+  int64_t step;      /* j, 0-based */
+  int32_t n_entries; /* |B_j| (its entries follow the previous steps' in `entries`) */
+  int32_t n_events;  /* preemptions during step j */
+  int64_t U;         /* KV holdings after B_j was formed (before its completions free theirs) */
+  int64_t tok;       /* sum of c over B_j */
+  double start;      /* clock (cost model cost[0]) when the batch starts */
+  double d;          /* its batch time d_j under cost[0] */
+} sim_trace_step_t; /* 48 bytes */
+
+typedef struct {
+  int32_t id;       /* request index in the workload */
+  int32_t phase;    /* 1 = prefill (incl. refills and chunks), 0 = decode */
+  int32_t c;        /* tokens processed in this step */
+  int32_t m_before; /* m of the request before the step */
+} sim_trace_entry_t; /* 16 bytes */
+
+typedef struct {
+  int32_t id; /* the preempted request */
+  int32_t m;  /* its m when it was preempted (the KVs discarded) */
+} sim_trace_event_t; /* 8 bytes */
+
+typedef struct {            /* HOST buffers, caller-owned */
+  sim_trace_step_t* steps;  /* [cap_steps] */
+  int64_t cap_steps;
+  sim_trace_entry_t* entries; /* [cap_entries] */
+  int64_t cap_entries;
+  sim_trace_event_t* events; /* [cap_events] */
+  int64_t cap_events;
+  int64_t n_steps, n_entries, n_events; /* out: the totals; records beyond a cap are not written (call again
+                                           with caps >= the totals for the whole log) */
+} sim_trace_t;
+
+/* Simulate ONE configuration (cfg->workload indexes wls) and record its schedule.  Same semantics, inputs and
+ * outputs as sim_sweep() with n_cfgs = 1 (result[1], req sized for it), plus `trace`.  Steady decode runs are
+ * not compressed while tracing (every step is formed), which changes no result.  Returns 0 / SIM_E*
+ * (SIM_EINVAL for a NULL trace or negative caps).  Blocking. */
+int sim_run_traced(const sim_config_t* cfg, const sim_workload_t* wls, int32_t n_wls, const sim_cost_model_t* cms,
+                   int32_t n_cms, sim_result_t* result, sim_request_out_t req, sim_trace_t* trace, int32_t device);
+
 /* Device workspace bytes sim_sweep_device() needs for these configs (host
  * arrays; wls_n = n of each workload): ~1.7 MB per simulation whose workload
  * has n > 4096 requests, 0 if there is none.  Returns >= 0 or SIM_EINVAL. */

@@ -32,6 +32,14 @@ constexpr uint8_t F_FILLED = 4, F_INB = 8, F_PRE = 16, F_FIRST = 32, F_LAST = 64
 constexpr int PH_DEC = 0, PH_PRE = 1;
 constexpr int NOBRK = 0x7fffffff;
 
+// per-step schedule trace of the launch's only simulation (sim_run_traced), else steps == nullptr
+struct TraceDev {
+  sim_trace_step_t* steps;
+  sim_trace_entry_t* entries;
+  sim_trace_event_t* events;
+  long long cap_steps, cap_entries, cap_events;
+};
+
 struct KParams {
   unsigned char* ws;  // large-window variant: [WS_HEADER | arenas], the counter at ws[0]
   const sim_config_t* cfgs;
@@ -44,6 +52,7 @@ struct KParams {
   sim_request_out_t req;
   int32_t n_cfgs;
   int32_t variant;
+  TraceDev tr;
 };
 
 // exact integer features of one batch (Table 3 variables; Eq. (1)-(2) sums)
@@ -58,6 +67,7 @@ struct Scal {
   long long U, seq;
   long long steps, preempt, entries, processed, sumU, pentries, idle, visits;
   long long runL, runMD, last_nd;
+  long long tr_ent, tr_ev;  // trace records written before this step
   int runEx;
   long long pref[6];  // exclusive prefixes (c, dKV, admitted-waiting, admitted, SRF+Hist rem) at the break
   long long featsum[16];

@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   // for waiting admissions (Q16); with the defaults (0) every check below is a no-op
   // (KN = false: the kernel instance for configs without knobs, where all of these checks compile away)
   const bool holk = KN && (cfg.knobs & SIM_KNOB_HOL) != 0;
+  const bool trc = KN && p.tr.steps != nullptr;  // schedule trace (sim_run_traced; the KN instance)
   const bool arr_ord = KN && (cfg.knobs & SIM_KNOB_NRF_ARRIVAL) != 0;  // NRF run list in arrival order (Q6 alt.)
   // Q3 alternative: SRF visits in admission order (the run list is not re-sorted) and only picks victims by m,
   // so the victim pool is not the run list's tail: the closed form is off and victims are searched literally
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     S.steps = S.preempt = S.entries = S.processed = S.sumU = S.pentries = S.idle = S.visits = 0;
     S.next = S.new_next = S.lo = S.n_done = S.n_run = 0;
     S.nrank = S.nW = S.minSW = S.n_ev = S.n_vic = S.nB = 0;
+    if (KN) S.tr_ent = S.tr_ev = 0;
     S.r_dirty = S.o_dirty = S.rank_dirty = S.removals = S.wbuilt = 0;
     S.status = 0;
     S.cur = 0;
@@ -328,6 +330,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       atomicAdd(&refill[idx], (unsigned long long)rc.z);
       s_rec[v] = make_int4(rc.x, rc.y, 0, 0);
       s_fl[v] = ST_WAIT | F_PRE | (s_fl[v] & F_FIRST);
+      if (trc) {
+        const long long e = S.tr_ev + S.n_vic;
+        if (e < p.tr.cap_events) p.tr.events[e] = sim_trace_event_t{idx, rc.z};
+      }
       s_vic[S.n_vic++] = (int16_t)v;
       n_running--;
       S.preempt++;
@@ -672,6 +678,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             s_rec[sl] = make_int4(rc.x, rc.y, 0, 0);
             s_fl[sl] = ST_WAIT | F_PRE | (s_fl[sl] & F_FIRST);
             s_vic[nvic0 + (q == selfp ? nrun - qs : q - qs)] = (int16_t)sl;
+            if (trc) {  // the oracle's order: the lowest retention (the run list's tail) first, head a+1 last
+              const long long e = S.tr_ev + nvic0 + (q == selfp ? nrun - qs : nrun - 1 - q);
+              if (e < p.tr.cap_events) p.tr.events[e] = sim_trace_event_t{idx, rc.z};
+            }
           } else if (hh[j]) {
             const int i = k - hsv[j] + 1;
             if (i <= a) {
@@ -1158,6 +1168,11 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         const int m0 = rc.z;
         int g = rc.y;
         const int s = rc.x + g, m = m0 + c;
+        if (trc) {
+          const long long x = S.tr_ent + e;
+          if (x < p.tr.cap_entries)
+            p.tr.entries[x] = sim_trace_entry_t{lo + ((sl - lo) & (CAP - 1)), (fl & F_FILLED) ? 0 : 1, c, m0};
+        }
         N += c;
         if (!(fl & F_FILLED)) {  // prefill entry (incl. refills and chunks)
           np_++;
@@ -1273,7 +1288,15 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           f.N = tt[0], f.np = tt[1], f.cp = tt[2], f.mp = tt[3], f.nd = tt[4], f.md = tt[5];
           f.c2 = tt[11], f.mc = tt[12], f.pcm = tt[13];
           f.pceil[0] = tt[14], f.pceil[1] = tt[15], f.pceil[2] = tt[16], f.pceil[3] = tt[17];
+          const double start = trc ? S.clock[0] : 0.0;
           for (int k = 0; k < K; k++) S.clock[k] = dadd(S.clock[k], batch_time(S.cm[k], f, k));  // Q36
+          if (trc) {  // (d_j under cost[0] evaluated again: the same expression, the same bits)
+            if (S.steps < p.tr.cap_steps)
+              p.tr.steps[S.steps] = sim_trace_step_t{S.steps, nB, S.n_vic, (long long)U, (long long)tok, start,
+                                                     batch_time(S.cm[0], f, 0)};
+            S.tr_ent += nB;
+            S.tr_ev += S.n_vic;
+          }
           TMARK(35);
 #ifdef SIMSWEEP_PROFILE
           if (ci == 0 && S.steps < DBG_STEPS) {
@@ -1303,7 +1326,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
                      (nWn == 0 || (finiteM && (long long)Uafter + blk(minSWn) > (KN ? Mw : M)));
           }
           long long Lr = 0;
-          if (steady) {
+          if (steady && !trc) {  // (tracing forms every step)
             Lr = tt[10];
             if (paged)  // no entry opens a block during the run: U stays constant
               Lr = min(Lr, tt[18]);

@@ -56,6 +56,7 @@ __host__ __device__ inline int variant_of(int n) { return n <= 1024 ? 0 : (n <= 
 constexpr int N_SIZES = 3;
 // configs with an alternative-reading knob run in a second instance of each size (KN = true), so that the
 // default instances carry none of the knob checks
+constexpr int32_t SIM_KNOB_TRACE_INTERNAL = 1 << 30;  // set by sim_run_traced only (routes to the KN instance)
 __host__ __device__ inline bool has_knobs(const sim_config_t& c) {
   return c.knobs || c.max_seqs || c.kv_watermark || c.kv_block > 1;
 }
@@ -171,11 +172,13 @@ int64_t sim_workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int3
   return workspace_bytes(cfgs, n_cfgs, wls_n);
 }
 
-int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, const sim_config_t* d_cfgs,
-                     const sim_workload_t* d_wls, const sim_cost_model_t* d_cms, int32_t n_cms,
-                     const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
-                     sim_result_t* d_results, sim_request_out_t d_req, void* d_workspace, int64_t workspace_bytes_,
-                     void* stream) {
+}  // extern "C"
+
+static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, const sim_config_t* d_cfgs,
+                        const sim_workload_t* d_wls, const sim_cost_model_t* d_cms, int32_t n_cms,
+                        const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
+                        sim_result_t* d_results, sim_request_out_t d_req, void* d_workspace, int64_t workspace_bytes_,
+                        void* stream, const TraceDev& tr) {
   if (!h_cfgs || !h_wls_n || !d_cfgs || !d_wls || !d_cms || n_cfgs <= 0 || n_cms <= 0 || !d_row_off ||
       !d_tim_off || !d_results || !d_req.t_first || !d_req.t_done || !d_req.n_preempt || !d_req.refill_tokens)
     return SIM_EINVAL;
@@ -195,6 +198,7 @@ int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* 
   kp.results = d_results;
   kp.req = d_req;
   kp.n_cfgs = n_cfgs;
+  kp.tr = tr;
   int launches = 0;
   // the large-window variants first: their simulations are the longest
   static const int launch_order[N_VARIANTS] = {2, 2 + N_SIZES, 1, 1 + N_SIZES, 0, N_SIZES};
@@ -222,6 +226,18 @@ int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* 
     launches++;
   }
   return launches;
+}
+
+extern "C" {
+
+int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, const sim_config_t* d_cfgs,
+                     const sim_workload_t* d_wls, const sim_cost_model_t* d_cms, int32_t n_cms,
+                     const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
+                     sim_result_t* d_results, sim_request_out_t d_req, void* d_workspace, int64_t workspace_bytes_,
+                     void* stream) {
+  const TraceDev none{nullptr, nullptr, nullptr, 0, 0, 0};
+  return launch_sweep(h_cfgs, n_cfgs, h_wls_n, d_cfgs, d_wls, d_cms, n_cms, d_order, d_row_off, d_tim_off, d_results,
+                      d_req, d_workspace, workspace_bytes_, stream, none);
 }
 
 static int validate_cms(const sim_cost_model_t* cms, int32_t n_cms) {
@@ -331,12 +347,26 @@ static int cache_reserve(DevCache& c, size_t dbytes, size_t hbytes) {
   return 0;
 }
 
-int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
-              const sim_cost_model_t* cms, int32_t n_cms, sim_result_t* results, sim_request_out_t req,
-              int32_t device) {
-  int rc = validate(cfgs, n_cfgs, wls, n_wls, cms, n_cms);
+}  // extern "C"
+
+// the host entry points: validate, stage inputs (one H2D), launch, copy outputs (and the trace) back
+static int host_run(const sim_config_t* cfgs_in, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
+                    const sim_cost_model_t* cms, int32_t n_cms, sim_result_t* results, sim_request_out_t req,
+                    int32_t device, sim_trace_t* trace) {
+  int rc = validate(cfgs_in, n_cfgs, wls, n_wls, cms, n_cms);
   if (rc) return rc;
   if (!results) return SIM_EINVAL;
+  if (trace && (n_cfgs != 1 || trace->cap_steps < 0 || trace->cap_entries < 0 || trace->cap_events < 0 ||
+                (trace->cap_steps && !trace->steps) || (trace->cap_entries && !trace->entries) ||
+                (trace->cap_events && !trace->events)))
+    return SIM_EINVAL;
+  sim_config_t tcfg;
+  const sim_config_t* cfgs = cfgs_in;
+  if (trace) {  // a traced simulation runs in the knob instance (KN), which carries the trace writes
+    tcfg = cfgs_in[0];
+    tcfg.knobs |= SIM_KNOB_TRACE_INTERNAL;
+    cfgs = &tcfg;
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return SIM_ENODEV;
   if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return SIM_ECUDA;
@@ -405,6 +435,12 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
   const int64_t wsb = workspace_bytes(cfgs, n_cfgs, wn.data());
   const size_t o_ws = off;
   off = al(off + (size_t)wsb);
+  const size_t o_ts = off;
+  off = al(off + (trace ? sizeof(sim_trace_step_t) * (size_t)trace->cap_steps : 0));
+  const size_t o_te = off;
+  off = al(off + (trace ? sizeof(sim_trace_entry_t) * (size_t)trace->cap_entries : 0));
+  const size_t o_tv = off;
+  off = al(off + (trace ? sizeof(sim_trace_event_t) * (size_t)trace->cap_events : 0));
   if ((rc = cache_reserve(cache, off, in_bytes))) return rc;
   char* base = cache.dbuf;
   char* h = cache.hbuf;
@@ -434,14 +470,21 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
   dreq.t_done = reinterpret_cast<double*>(base + o_td);
   dreq.n_preempt = reinterpret_cast<int64_t*>(base + o_np);
   dreq.refill_tokens = reinterpret_cast<int64_t*>(base + o_rf);
+  TraceDev tr{nullptr, nullptr, nullptr, 0, 0, 0};
+  if (trace) {
+    tr.steps = reinterpret_cast<sim_trace_step_t*>(base + o_ts);
+    tr.entries = reinterpret_cast<sim_trace_entry_t*>(base + o_te);
+    tr.events = reinterpret_cast<sim_trace_event_t*>(base + o_tv);
+    tr.cap_steps = trace->cap_steps, tr.cap_entries = trace->cap_entries, tr.cap_events = trace->cap_events;
+  }
   if (!rc) {
-    int l = sim_sweep_device(cfgs, n_cfgs, wn.data(), reinterpret_cast<const sim_config_t*>(base + o_cfg),
+    int l = launch_sweep(cfgs, n_cfgs, wn.data(), reinterpret_cast<const sim_config_t*>(base + o_cfg),
                              reinterpret_cast<const sim_workload_t*>(base + o_wl),
                              reinterpret_cast<const sim_cost_model_t*>(base + o_cm), n_cms,
                              reinterpret_cast<const int32_t*>(base + o_ord),
                              reinterpret_cast<const int64_t*>(base + o_ro), reinterpret_cast<const int64_t*>(base + o_to),
                              reinterpret_cast<sim_result_t*>(base + o_res), dreq, wsb ? base + o_ws : nullptr, wsb,
-                             s);
+                             s, tr);
     if (l < 0) rc = l;
   }
   if (!rc) {
@@ -454,7 +497,33 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
       rc |= check_cuda(cudaMemcpyAsync(req.refill_tokens, dreq.refill_tokens, 8 * rows, cudaMemcpyDeviceToHost, s));
   }
   rc |= check_cuda(cudaStreamSynchronize(s));
+  if (!rc && trace) {  // totals from the result (every step, entry and preemption is counted there)
+    trace->n_steps = results[0].steps;
+    trace->n_entries = results[0].batch_entries;
+    trace->n_events = results[0].preemptions;
+    const int64_t ns = std::min(trace->n_steps, trace->cap_steps), ne = std::min(trace->n_entries, trace->cap_entries),
+                  nv = std::min(trace->n_events, trace->cap_events);
+    if (ns > 0) rc |= check_cuda(cudaMemcpy(trace->steps, tr.steps, sizeof(sim_trace_step_t) * ns, cudaMemcpyDeviceToHost));
+    if (ne > 0)
+      rc |= check_cuda(cudaMemcpy(trace->entries, tr.entries, sizeof(sim_trace_entry_t) * ne, cudaMemcpyDeviceToHost));
+    if (nv > 0)
+      rc |= check_cuda(cudaMemcpy(trace->events, tr.events, sizeof(sim_trace_event_t) * nv, cudaMemcpyDeviceToHost));
+  }
   return rc ? (rc < 0 ? rc : SIM_ECUDA) : 0;
+}
+
+extern "C" {
+
+int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
+              const sim_cost_model_t* cms, int32_t n_cms, sim_result_t* results, sim_request_out_t req,
+              int32_t device) {
+  return host_run(cfgs, n_cfgs, wls, n_wls, cms, n_cms, results, req, device, nullptr);
+}
+
+int sim_run_traced(const sim_config_t* cfg, const sim_workload_t* wls, int32_t n_wls, const sim_cost_model_t* cms,
+                   int32_t n_cms, sim_result_t* result, sim_request_out_t req, sim_trace_t* trace, int32_t device) {
+  if (!trace) return SIM_EINVAL;
+  return host_run(cfg, 1, wls, n_wls, cms, n_cms, result, req, device, trace);
 }
 
 }  // extern "C"

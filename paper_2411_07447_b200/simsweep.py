@@ -89,6 +89,18 @@ class SimRequestOut(ctypes.Structure):
                 ("refill_tokens", ctypes.c_void_p)]
 
 
+class SimTrace(ctypes.Structure):  # == sim_trace_t
+    _fields_ = [("steps", ctypes.c_void_p), ("cap_steps", ctypes.c_int64), ("entries", ctypes.c_void_p),
+                ("cap_entries", ctypes.c_int64), ("events", ctypes.c_void_p), ("cap_events", ctypes.c_int64),
+                ("n_steps", ctypes.c_int64), ("n_entries", ctypes.c_int64), ("n_events", ctypes.c_int64)]
+
+
+# == sim_trace_step_t / sim_trace_entry_t / sim_trace_event_t
+TRACE_STEP_DTYPE = np.dtype([("step", "<i8"), ("n_entries", "<i4"), ("n_events", "<i4"), ("U", "<i8"), ("tok", "<i8"),
+                             ("start", "<f8"), ("d", "<f8")])
+TRACE_ENTRY_DTYPE = np.dtype([("id", "<i4"), ("phase", "<i4"), ("c", "<i4"), ("m_before", "<i4")])
+TRACE_EVENT_DTYPE = np.dtype([("id", "<i4"), ("m", "<i4")])
+
 RESULT_DTYPE = np.dtype([("status", "<i4"), ("pad", "<i4"), ("steps", "<i8"), ("preemptions", "<i8"),
                          ("batch_entries", "<i8"), ("processed_tokens", "<i8"), ("sum_U", "<i8"),
                          ("prefill_entries", "<i8"), ("idle_jumps", "<i8"), ("visits", "<i8"), ("makespan", "<f8", (4,)),
@@ -115,6 +127,9 @@ def lib() -> ctypes.CDLL:
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, SimRequestOut,
                                        ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.sim_run_traced.restype = ctypes.c_int
+        L.sim_run_traced.argtypes = [P(SimConfig), P(SimWorkload), ctypes.c_int32, P(SimCostModel), ctypes.c_int32,
+                                     P(SimResult), SimRequestOut, P(SimTrace), ctypes.c_int32]
         L.sim_workspace_bytes.restype = ctypes.c_int64
         L.sim_workspace_bytes.argtypes = [P(SimConfig), ctypes.c_int32, P(ctypes.c_int32)]
         L.sim_request_rows.restype = ctypes.c_int
@@ -140,7 +155,7 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-EXPORTED_SYMBOLS = ["sim_sweep", "sim_sweep_device", "sim_workspace_bytes", "sim_request_rows", "sim_strerror",
+EXPORTED_SYMBOLS = ["sim_sweep", "sim_sweep_device", "sim_run_traced", "sim_workspace_bytes", "sim_request_rows", "sim_strerror",
                     "sim_version", "sim_batch_times", "sim_slo_frontier", "sim_kv_break_even", "sim_optimum"]
 
 
@@ -266,11 +281,8 @@ def io_bytes(cfgs, wls, n_cms):
     return int(h2d), int(d2h)
 
 
-def sim_sweep(cfgs, wls: list[Workload], cms, device: int = -1, out=None) -> SweepResult:
-    """Host-buffer entry point: validates, copies in, simulates, copies out (blocking).
-    `out` = alloc_outputs(...) to reuse (e.g. pinned) output buffers."""
-    cfgs = list(cfgs)
-    n_of, k_of, row_off, tim_off, rows, trows = _offsets(cfgs, wls)
+def _wl_array(wls):
+    """sim_workload_t[] over host arrays (returned with the arrays it points into, to keep them alive)."""
     keep = []
     warr = (SimWorkload * len(wls))()
     for j, w in enumerate(wls):
@@ -280,6 +292,15 @@ def sim_sweep(cfgs, wls: list[Workload], cms, device: int = -1, out=None) -> Swe
         keep += [I, O, T]
         warr[j].n = int(I.shape[0])
         warr[j].I, warr[j].O, warr[j].T = I.ctypes.data, O.ctypes.data, T.ctypes.data
+    return warr, keep
+
+
+def sim_sweep(cfgs, wls: list[Workload], cms, device: int = -1, out=None) -> SweepResult:
+    """Host-buffer entry point: validates, copies in, simulates, copies out (blocking).
+    `out` = alloc_outputs(...) to reuse (e.g. pinned) output buffers."""
+    cfgs = list(cfgs)
+    n_of, k_of, row_off, tim_off, rows, trows = _offsets(cfgs, wls)
+    warr, _keep = _wl_array(wls)
     res, tf, td, npre, rf = out if out is not None else alloc_outputs(cfgs, wls)
     req = SimRequestOut(tf.ctypes.data, td.ctypes.data, npre.ctypes.data, rf.ctypes.data)
     rc = lib().sim_sweep(_cfg_array(cfgs), len(cfgs), warr, len(wls), _cm_array(cms), len(cms),
@@ -349,6 +370,61 @@ class DeviceSweep:
         res = np.frombuffer(self.d_results.cpu().numpy().tobytes(), RESULT_DTYPE).copy()
         return SweepResult(res, self.t_first.cpu().numpy(), self.t_done.cpu().numpy(), self.n_preempt.cpu().numpy(),
                            self.refill.cpu().numpy(), self.row_off_np, self.tim_off_np, self.n_of, self.k_of)
+
+
+@dataclass
+class ScheduleLog:
+    """The per-step schedule of one simulation (sim_run_traced): record arrays in step order."""
+    steps: np.ndarray    # TRACE_STEP_DTYPE [n_steps]
+    entries: np.ndarray  # TRACE_ENTRY_DTYPE [sum n_entries], each step's batch in admission order
+    events: np.ndarray   # TRACE_EVENT_DTYPE [sum n_events], each step's preemptions in order
+
+    def steps_list(self) -> list:
+        """-> [dict(step, U, tok, start, d, entries=[(id, phase, c, m_before)], events=[(id, m)])]."""
+        out, p, q = [], 0, 0
+        ent = self.entries.tolist()
+        ev = self.events.tolist()
+        for st in self.steps.tolist():
+            j, ne, nv, U, tok, start, d = st
+            out.append(dict(step=j, U=U, tok=tok, start=start, d=d, entries=[tuple(x) for x in ent[p:p + ne]],
+                            events=[tuple(x) for x in ev[q:q + nv]]))
+            p += ne
+            q += nv
+        return out
+
+    def to_csv(self, fh) -> None:
+        """SPEC's ScheduleLog columns: batch,start_s,duration_s,request,phase,c,m_before,event -- one row per batch
+        entry, then one row per preemption of that step (phase empty, c = 0, m_before = the discarded m)."""
+        fh.write("batch,start_s,duration_s,request,phase,c,m_before,event\n")
+        for st in self.steps_list():
+            head = f"{st['step']},{st['start']!r},{st['d']!r}"
+            for (rid, ph, c, m) in st["entries"]:
+                fh.write(f"{head},{rid},{'prefill' if ph else 'decode'},{c},{m},\n")
+            for (rid, m) in st["events"]:
+                fh.write(f"{head},{rid},,0,{m},preempt\n")
+
+
+def sim_run_traced(cfg, wls: list[Workload], cms, device: int = -1, caps=(1 << 16, 1 << 20, 1 << 16)):
+    """One simulation with its schedule: -> (SweepResult of that one config, ScheduleLog).  Buffers start at
+    `caps` (steps, entries, events); a longer log is fetched again with exact sizes."""
+    cfgs = [cfg]
+    warr, _keep = _wl_array(wls)
+    cs, ce, cv = (int(x) for x in caps)
+    while True:
+        res, tf, td, npre, rf = alloc_outputs(cfgs, wls)
+        req = SimRequestOut(tf.ctypes.data, td.ctypes.data, npre.ctypes.data, rf.ctypes.data)
+        st = np.zeros(max(cs, 1), TRACE_STEP_DTYPE)
+        en = np.zeros(max(ce, 1), TRACE_ENTRY_DTYPE)
+        ev = np.zeros(max(cv, 1), TRACE_EVENT_DTYPE)
+        tr = SimTrace(st.ctypes.data, cs, en.ctypes.data, ce, ev.ctypes.data, cv, 0, 0, 0)
+        _check(lib().sim_run_traced(_cfg_array(cfgs), warr, len(wls), _cm_array(cms), len(cms),
+                                    res.ctypes.data_as(ctypes.POINTER(SimResult)), req, ctypes.byref(tr), int(device)))
+        if tr.n_steps <= cs and tr.n_entries <= ce and tr.n_events <= cv:
+            break
+        cs, ce, cv = max(cs, tr.n_steps), max(ce, tr.n_entries), max(cv, tr.n_events)
+    n_of, k_of, row_off, tim_off, _, _ = _offsets(cfgs, wls)
+    log = ScheduleLog(st[:tr.n_steps].copy(), en[:tr.n_entries].copy(), ev[:tr.n_events].copy())
+    return SweepResult(res, tf, td, npre, rf, row_off, tim_off, n_of, k_of), log
 
 
 def lpt_order(cfgs, wls) -> np.ndarray:

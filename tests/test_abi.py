@@ -45,6 +45,8 @@ def test_struct_layout_matches_header(tmp_path):
                    'printf("%zu\\n", offsetof(sim_config_t, reserve));'
                    'printf("%zu %zu %zu\\n", sizeof(sim_batch_shape_t), sizeof(sim_slo_query_t), offsetof(sim_slo_query_t, tau));'
                    'printf("%zu %zu %zu\\n", sizeof(sim_opt_problem_t), offsetof(sim_opt_problem_t, C), sizeof(sim_opt_result_t));'
+                   'printf("%zu %zu %zu %zu %zu\\n", sizeof(sim_trace_step_t), offsetof(sim_trace_step_t, start), '
+                   'sizeof(sim_trace_entry_t), sizeof(sim_trace_event_t), sizeof(sim_trace_t));'
                    'return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
@@ -54,9 +56,11 @@ def test_struct_layout_matches_header(tmp_path):
             ctypes.sizeof(simsweep.SimRequestOut), simsweep.SimConfig.n_cost.offset,
             simsweep.SimResult.makespan.offset, simsweep.SimConfig.reserve.offset,
             ctypes.sizeof(simsweep.SimBatchShape), ctypes.sizeof(simsweep.SimSloQuery), simsweep.SimSloQuery.tau.offset,
-            ctypes.sizeof(simsweep.SimOptProblem), simsweep.SimOptProblem.C.offset, ctypes.sizeof(simsweep.SimOptResult)]
+            ctypes.sizeof(simsweep.SimOptProblem), simsweep.SimOptProblem.C.offset, ctypes.sizeof(simsweep.SimOptResult),
+            simsweep.TRACE_STEP_DTYPE.itemsize, simsweep.TRACE_STEP_DTYPE.fields["start"][1],
+            simsweep.TRACE_ENTRY_DTYPE.itemsize, simsweep.TRACE_EVENT_DTYPE.itemsize, ctypes.sizeof(simsweep.SimTrace)]
     assert got == want
-    assert got[0] == 96
+    assert got[0] == 96 and got[-5:] == [48, 32, 16, 8, 72]
 
 
 def test_version_and_strerror(L):
@@ -96,6 +100,8 @@ def test_no_gpu_fails_loudly(L):
         simsweep.sim_kv_break_even([simsweep.unit_cost()], [4], 64e9, 100)
     with pytest.raises(simsweep.SimError, match="no sm_100"):
         simsweep.sim_optimum([([2, 2], [4, 4], 4096, 6)], simsweep.unit_cost())
+    with pytest.raises(simsweep.SimError, match="no sm_100"):
+        simsweep.sim_run_traced(simsweep.preset_config("vllm", 100), [wl], [simsweep.unit_cost()])
 
 
 def test_invalid_calls_rejected_before_device(L):
@@ -116,6 +122,18 @@ def test_invalid_calls_rejected_before_device(L):
     bad_cm.mode = 7
     with pytest.raises(simsweep.SimError, match="cost"):
         simsweep.sim_slo_frontier([bad_cm], [(1, 1, 1, 10, 1.0)])
+    # the schedule trace: a NULL trace, negative or unbacked capacities, a bad config -- before any device work
+    cfgs = simsweep._cfg_array([simsweep.preset_config("vllm", 100)])
+    warr, _keep = simsweep._wl_array([wl])
+    cm = simsweep._cm_array([simsweep.unit_cost()])
+    res = np.zeros(1, simsweep.RESULT_DTYPE)
+    req = simsweep.SimRequestOut(None, None, None, None)
+    rp = res.ctypes.data_as(ctypes.POINTER(simsweep.SimResult))
+    assert L.sim_run_traced(cfgs, warr, 1, cm, 1, rp, req, None, -1) == -1
+    for tr in (simsweep.SimTrace(None, -1, None, 0, None, 0, 0, 0, 0), simsweep.SimTrace(None, 4, None, 0, None, 0, 0, 0, 0)):
+        assert L.sim_run_traced(cfgs, warr, 1, cm, 1, rp, req, ctypes.byref(tr), -1) == -1
+    with pytest.raises(simsweep.SimError, match="invalid argument"):
+        simsweep.sim_run_traced(bad, [wl], [simsweep.unit_cost()])
     with pytest.raises(simsweep.SimError, match="invalid argument"):  # the optimum: C >= 1
         simsweep.sim_optimum([([2], [2], 0, 6)], simsweep.unit_cost())
 
