@@ -38,7 +38,8 @@ def test_random_configs_verify(seed):
     assert r.status == "ok"
     outs = dict(t_first=list(r.t_first[0]), t_done=list(r.t_done[0]), n_preempt=list(r.n_preempt),
                 refill=list(r.refill))
-    viol = verify(r.steps_list, list(wl.I), list(wl.O), list(wl.T), C, M, outs, hybrid=bool(hybrid))
+    viol = verify(r.steps_list, list(wl.I), list(wl.O), list(wl.T), C, M, outs, hybrid=bool(hybrid),
+                  replacement=REPLS[int(cfg.replacement)])
     assert viol == []
     assert r.steps == len(r.steps_list) and r.steps >= int(wl.O.max())
     assert r.preemptions == int(r.n_preempt.sum())
@@ -79,3 +80,21 @@ def test_verifier_accepts_valid_and_rejects_mutations():
     assert verify(bad, *args) != []
     # memory bound violated: tighten M
     assert any("KV holdings" in x for x in verify(st, [1, 1, 5], [6, 6, 4], [0.0] * 3, 4096, 11))
+
+
+def test_verifier_checks_victim_order():
+    # two victims in one step: NRF evicts the newest admission first (Table 2); swapping the
+    # two events (or reading them under SRF's key where the m order differs) is a violation
+    for repl in ("nrf", "srf"):
+        I, O = [2, 6, 7, 1, 2], [2, 3, 3, 2, 7]
+        cfg = o.make_config("prefill_first", 0, 0, repl, C=4096, M=11)
+        r = o.run(cfg, I, O, [0.0] * 5, o.unit_cost(), trace=True)
+        st = r.steps_list
+        args = (I, O, [0.0] * 5, 4096, 11)
+        assert verify(st, *args, replacement=repl) == []
+        multi = [k for k, x in enumerate(st) if len(x["events"]) >= 2]
+        assert multi, repl
+        bad = copy.deepcopy(st)
+        k = multi[0]
+        bad[k]["events"] = bad[k]["events"][::-1]
+        assert any("lower retention" in x for x in verify(bad, *args, replacement=repl)), repl

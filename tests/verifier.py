@@ -16,7 +16,7 @@ trace: list of dict(step, U, tok, start, d, entries=[(id, phase, c, m_before)],
 from __future__ import annotations
 
 
-def verify(steps, I, O, T, C, M, K_out=None, hybrid=True, reserve="seq", S=None, kv_block=1):
+def verify(steps, I, O, T, C, M, K_out=None, hybrid=True, reserve="seq", S=None, kv_block=1, replacement=None):
     """Returns a list of violation strings (empty = valid).
 
     reserve: the Table 2 "Initial KV reserve" taken at (re)admission:
@@ -25,6 +25,11 @@ def verify(steps, I, O, T, C, M, K_out=None, hybrid=True, reserve="seq", S=None,
 
     K_out: optional dict(t_first=[...], t_done=[...], n_preempt=[...], refill=[...])
     to cross-check the reported per-request outputs against the trace.
+
+    replacement: "nrf", "srf" or "srf_hist" also checks WHICH requests were preempted, in order
+    (PAPER.md:1644-1646): when v is preempted, no running request outside the step's batch has
+    a lower retention than v (NRF: later admission; SRF: smaller m, ties later admission).  Admission order
+    is re-derived from the trace (a request's (re)admission is its first entry while not running).
     """
     n = len(I)
     v = []
@@ -39,6 +44,13 @@ def verify(steps, I, O, T, C, M, K_out=None, hybrid=True, reserve="seq", S=None,
     t_done = [None] * n
     total_c = 0
     prev_end = None
+    seq = [0] * n
+    nseq = 0
+
+    def lower(a, b):  # retention of a below that of b
+        if replacement == "nrf":
+            return seq[a] > seq[b]
+        return m[a] < m[b] or (m[a] == m[b] and seq[a] > seq[b])
     for st in steps:
         j, ents, evs = st["step"], st["entries"], st["events"]
         start, d = st["start"], st["d"]
@@ -53,7 +65,13 @@ def verify(steps, I, O, T, C, M, K_out=None, hybrid=True, reserve="seq", S=None,
                 v.append(f"step {j}: clock jumped to {start} which is no arrival time")
         prev_end = start + d
         # preemption events (Eq. 4: m := 0 when e = 1); refill keeps g
+        inB = {e[0] for e in ents}
         for (i, md) in evs:
+            if replacement is not None and running[i]:
+                for r in range(n):
+                    if r != i and running[r] and r not in inB and lower(r, i):
+                        v.append(f"step {j}: preempted {i} while {r} (running, not in the batch) has lower retention")
+                        break
             if reserve != "seq":
                 v.append(f"step {j}: preemption of {i} under a preemption-free reserve")
             if not running[i]:
@@ -88,6 +106,8 @@ def verify(steps, I, O, T, C, M, K_out=None, hybrid=True, reserve="seq", S=None,
             phases.add(ph)
             if not running[i]:  # (re)admission reserves the initial reserve
                 running[i] = True
+                nseq += 1
+                seq[i] = nseq
                 res[i] = s if reserve == "seq" else (I[i] + O[i] - 1 if reserve == "peak" else S)
             sum_c += c
         if not hybrid and len(phases) > 1:
