@@ -32,6 +32,55 @@ namespace simsweep {
 enum { K_NONE = 0, K_MARK = 1, K_EVENT = 2 };
 constexpr int WARP_MAX = 256;  // at most this many candidates left in a group: warp-level admission
 
+// Cold blocks of the step loop, kept out of line so that the hot path stays contiguous in the instruction cache
+// (DESIGN.md 6).  Each is called by all threads of the CTA.
+
+// rank orders: drop finished entries of the rank list before their slots are reused
+template <int NT, int IPT_>
+__device__ __noinline__ int rank_drop_done(int16_t* s_rank, int16_t* s_new, const uint8_t* s_fl, int nrank, Scal& S) {
+  nrank = block_compact<NT, IPT_>(
+      nrank, [&](int q) { return (s_fl[s_rank[q]] & ST_MASK) != ST_DONE; }, [&](int q) { return s_rank[q]; }, s_new, S);
+  for (int q = threadIdx.x; q < nrank; q += NT) s_rank[q] = s_new[q];
+  __syncthreads();  // the compacted list is read by other threads before the next barrier otherwise
+  return nrank;
+}
+
+// rank orders: append the arrivals [nx0, nx1) and sort the one group by (key, T, id) (App. D, Q20, Q37)
+template <int NT, int CAP>
+__device__ __noinline__ int rank_regroup(int16_t* s_rank, unsigned long long* s_keys, const int4* s_rec,
+                                         const int32_t* s_O, int nrank, int nx0, int nx1, int lo, int order) {
+  const int tid = threadIdx.x;
+  for (int idx = nx0 + tid; idx < nx1; idx += NT) s_rank[nrank + idx - nx0] = (int16_t)(idx & (CAP - 1));
+  const int nr = nrank + (nx1 - nx0);
+  __syncthreads();
+  for (int q = tid; q < nr; q += NT) {
+    const int sl = s_rank[q];
+    const unsigned idx = (unsigned)(lo + ((sl - lo) & (CAP - 1)));
+    const unsigned key = order == SIM_ORDER_RANK_I ? (unsigned)s_rec[sl].x
+                         : order == SIM_ORDER_RANK_O ? (unsigned)s_O[sl]
+                                                     : 0u;
+    s_keys[q] = ((unsigned long long)key << 32) | idx;
+  }
+  block_bitonic<NT>(s_keys, nr);
+  for (int q = tid; q < nr; q += NT) s_rank[q] = (int16_t)(s_keys[q] & (CAP - 1));
+  __syncthreads();
+  return nr;
+}
+
+// SRF+Hist: predictions of the current histogram; sum of the remaining outputs of the running requests
+template <int NT>
+__device__ __noinline__ long long hist_running_rem(const int16_t* run, const int4* s_rec, int nrun, Scal& S) {
+  if (threadIdx.x < 18) S.pred[threadIdx.x] = hist_pred_row(S.hist, threadIdx.x);
+  __syncthreads();
+  long long r = 0;
+  for (int q = threadIdx.x; q < nrun; q += NT) {
+    const int4 rc = s_rec[run[q]];
+    const int rem = S.pred[bucket_of(rc.x)] - rc.y;
+    r += rem > 0 ? rem : 0;
+  }
+  return block_sum_ll<NT>(r, S);
+}
+
 template <int NT, int CAP, int IPT_, bool GM, bool KN>
 __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) : 1)) sim_kernel(KParams p) {
   using L = Smem<NT, CAP>;
@@ -206,12 +255,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     const int nrun = S.n_run;
     int16_t* run = S.cur ? s_runB : s_runA;
     int nrank = S.nrank;
-    if (rank && (arrived || S.rank_dirty) && nrank > 0) {  // drop finished entries before slot reuse
-      nrank = block_compact<NT, IPT_>(
-          nrank, [&](int q) { return (s_fl[s_rank[q]] & ST_MASK) != ST_DONE; }, [&](int q) { return s_rank[q]; },
-          s_new, S);
-      for (int q = tid; q < nrank; q += NT) s_rank[q] = s_new[q];
-    }
+    if (rank && (arrived || S.rank_dirty) && nrank > 0)  // drop finished entries before slot reuse
+      nrank = rank_drop_done<NT, IPT_>(s_rank, s_new, s_fl, nrank, S);
     for (int idx = nx0 + tid; idx < nx1; idx += NT) {
       const int sl = idx & (CAP - 1);
       s_rec[sl] = make_int4(wl.I[idx], 0, 0, 0);
@@ -224,23 +269,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     PROF_MARK(0);
     TMARK(2);
     // ---- (2) a3: GroupRequests (step 1) ----
-    if (rank && arrived) {  // one group sorted by (key, T, id) (App. D, Q20, Q37)
-      for (int idx = nx0 + tid; idx < nx1; idx += NT) s_rank[nrank + idx - nx0] = (int16_t)(idx & (CAP - 1));
-      const int nr = nrank + (nx1 - nx0);
-      __syncthreads();
-      for (int q = tid; q < nr; q += NT) {
-        const int sl = s_rank[q];
-        const unsigned idx = (unsigned)(lo + ((sl - lo) & (CAP - 1)));
-        const unsigned key = order == SIM_ORDER_RANK_I ? (unsigned)s_rec[sl].x
-                             : order == SIM_ORDER_RANK_O ? (unsigned)s_O[sl]
-                                                         : 0u;
-        s_keys[q] = ((unsigned long long)key << 32) | idx;
-      }
-      block_bitonic<NT>(s_keys, nr);
-      for (int q = tid; q < nr; q += NT) s_rank[q] = (int16_t)(s_keys[q] & (CAP - 1));
-      nrank = nr;
-      __syncthreads();
-    }
+    if (rank && arrived)  // one group sorted by (key, T, id) (App. D, Q20, Q37)
+      nrank = rank_regroup<NT, CAP>(s_rank, s_keys, s_rec, s_O, nrank, nx0, nx1, lo, order);
     int nW = S.nW, minSW = S.minSW, wbuilt = S.wbuilt;
     const int w0 = max(S.wfirst - lo, 0);  // window offsets below w0 hold no waiting request
     if (!rank && (S.w_dirty || arrived)) {  // |R_w| and its smallest s (the skip test); list built lazily
@@ -290,17 +320,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     const int wend = order == SIM_ORDER_PREFILL_FIRST ? nW : nP;
 
     long long Rs = 0;
-    if (hist) {  // SRF+Hist: predictions of the current histogram; sum of remaining outputs of running requests
-      if (tid < 18) S.pred[tid] = hist_pred_row(S.hist, tid);
-      __syncthreads();
-      long long r = 0;
-      for (int q = tid; q < nrun; q += NT) {
-        const int4 rc = s_rec[run[q]];
-        const int rem = S.pred[bucket_of(rc.x)] - rc.y;
-        r += rem > 0 ? rem : 0;
-      }
-      Rs = block_sum_ll<NT>(r, S);
-    }
+    if (hist)  // SRF+Hist: predictions of the current histogram; sum of remaining outputs of running requests
+      Rs = hist_running_rem<NT>(run, s_rec, nrun, S);
     if (tid == 0) {
       S.vt = nrun - 1;
       S.any_pre = 0;
