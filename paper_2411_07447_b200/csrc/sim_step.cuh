@@ -67,6 +67,42 @@ __device__ __noinline__ int rank_regroup(int16_t* s_rank, unsigned long long* s_
   return nr;
 }
 
+// |R_w| and the smallest s among the waiting requests at window offsets [w0, L), into S.nW / S.minSW
+template <int NT, int CAP>
+__device__ __noinline__ void waiting_count(const uint8_t* s_fl, const int4* s_rec, int w0, int L, int lo, Scal& S) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int cnt = 0, mn = 0x7fffffff;
+  for (int q = w0 + (int)threadIdx.x; q < L; q += NT) {
+    const int sl = (lo + q) & (CAP - 1);
+    if ((s_fl[sl] & ST_MASK) == ST_WAIT) {
+      const int4 r = s_rec[sl];
+      cnt++;
+      mn = min(mn, r.x + r.y);
+    }
+  }
+  cnt = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
+  mn = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
+  if (lane == 0) S.wsum[wid][0] = cnt, S.wsum[wid][1] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int nW = 0, minSW = 0x7fffffff;
+#pragma unroll
+    for (int w = 0; w < NW; w++) nW += S.wsum[w][0], minSW = min(minSW, S.wsum[w][1]);
+    S.nW = nW, S.minSW = minSW;
+  }
+  __syncthreads();
+}
+
+// decode-first general path: stable split of the run list into running decodes, then running prefills
+template <int NT, int IPT_>
+__device__ __noinline__ void run_split(const int16_t* run, int16_t* s_pl, const uint8_t* s_fl, int nrun, Scal& S) {
+  const int nrd = block_partition<NT, IPT_>(
+      nrun, [&](int q) { return (s_fl[run[q]] & F_FILLED) != 0; }, [&](int q) { return run[q]; }, s_pl, S);
+  if (threadIdx.x == 0) S.nRd = nrd;
+  __syncthreads();
+}
+
 // SRF+Hist: predictions of the current histogram; sum of the remaining outputs of the running requests
 template <int NT>
 __device__ __noinline__ long long hist_running_rem(const int16_t* run, const int4* s_rec, int nrun, Scal& S) {
@@ -274,33 +310,12 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     int nW = S.nW, minSW = S.minSW, wbuilt = S.wbuilt;
     const int w0 = max(S.wfirst - lo, 0);  // window offsets below w0 hold no waiting request
     if (!rank && (S.w_dirty || arrived)) {  // |R_w| and its smallest s (the skip test); list built lazily
-      int cnt = 0, mn = 0x7fffffff;
-      for (int q = w0 + tid; q < nx1 - lo; q += NT) {
-        const int sl = (lo + q) & (CAP - 1);
-        if ((s_fl[sl] & ST_MASK) == ST_WAIT) {
-          const int4 r = s_rec[sl];
-          cnt++;
-          mn = min(mn, r.x + r.y);
-        }
-      }
-      cnt = (int)__reduce_add_sync(FM, (unsigned)cnt);
-      mn = (int)__reduce_min_sync(FM, (unsigned)mn);
-      if (lane == 0) S.wsum[wid][0] = cnt, S.wsum[wid][1] = mn;
-      __syncthreads();
-      nW = 0, minSW = 0x7fffffff;
-#pragma unroll
-      for (int w = 0; w < NW; w++) nW += S.wsum[w][0], minSW = min(minSW, S.wsum[w][1]);
-      wbuilt = 0;
-      __syncthreads();
+      waiting_count<NT, CAP>(s_fl, s_rec, w0, nx1 - lo, lo, S);
+      nW = S.nW, minSW = S.minSW, wbuilt = 0;
     }
     int nRd = 0;
     if (order == SIM_ORDER_DECODE_FIRST && (nrun > CH || q3alt)) {  // general path: stable split of the run list
-      if (S.p_dirty) {
-        const int nrd = block_partition<NT, IPT_>(
-            nrun, [&](int q) { return (s_fl[run[q]] & F_FILLED) != 0; }, [&](int q) { return run[q]; }, s_pl, S);
-        if (tid == 0) S.nRd = nrd;
-        __syncthreads();
-      }
+      if (S.p_dirty) run_split<NT, IPT_>(run, s_pl, s_fl, nrun, S);
       nRd = S.nRd;
     }
     const int16_t* seg0;
