@@ -4,13 +4,16 @@
 One bench STEP = one pass of the whole hot path (rows a1-a12) over BASELINE
 configs[1]: the high-contention grid, 6 schedulers x I, O in {1, 2, ..., 1024}
 x W = 1024 x {NRF, SRF}, A100 Llama-3-8B linear cost model, KV recomputation,
-M = 100 000 (1 452 simulations, one sim_sweep_device launch + the result gather).
+M = 100 000 (1 452 simulations, one sim_sweep_device launch [+ the gather at N > 1]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun, one rank per GPU, NCCL): WEAK scaling -- rank r sweeps the
-same grid at its own KV capacity M_r = 100 000 + 12 500 r (an M sweep,
-PAPER.md:183-190); value = steps simulated by all ranks / max-over-ranks time.
+N > 1 (torchrun, one rank per GPU, NCCL): STRONG scaling -- the one sweep is
+LPT-sharded over the ranks (sweep.ShardedSweep), each rank simulates its shard
+and all outputs (result rows + per-request slabs) are gathered to rank 0 by one
+all_gather over NVLink inside the timed step; value = steps of the sweep /
+max-over-ranks time.  The floor is the longest single simulation (a dependent
+chain of steps), reported as config.critical_path.
 --impl reference times the CPU oracle (oracle/, the only other thing this file
 may run) on the host cores over a bounded sample of the same grid.
 """
@@ -50,16 +53,12 @@ def _measured_peaks():
         return {}
 
 
-def rank_M(rank: int) -> int:
-    return 100_000 + 12_500 * rank
-
-
 def workload_desc(world: int):
     return {"workload": "BASELINE configs[1] grid: 6 presets (vllm, sarathi, sarathi-cs, sarathi-nocp, vllm-hy, "
-                        "sarathi-nohy) x I,O in {1..1024 pow2} x W=1024 x {NRF,SRF} = 1452 simulations/rank, "
-                        "llama3-8b A100 linear cost model, offline",
-            "simulations_per_rank": 1452, "W": 1024, "S": 4096,
-            "M_per_rank": [rank_M(r) for r in range(world)], "l2": "flushed between timed iterations (256 MiB)"}
+                        "sarathi-nohy) x I,O in {1..1024 pow2} x W=1024 x {NRF,SRF} = 1452 simulations, "
+                        "llama3-8b A100 linear cost model, M=100000, offline; LPT-sharded over the GPUs",
+            "simulations": 1452, "W": 1024, "S": 4096, "M": 100_000,
+            "l2": "flushed between timed iterations (256 MiB)"}
 
 
 # ---------------------------------------------------------------- oracle (CPU) legs
@@ -128,7 +127,7 @@ def bench_reference(args, rank, world):
     sample = f"every {stride}th simulation of the rank-0 grid ({len(jobs)} of 1452), all cores, multiprocessing"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
             "config": workload_desc(1) | {"reference": "CPU oracle (oracle/oracle.cpp), g++ -O2"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -197,19 +196,18 @@ def bench_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfgs, wls, cms, labels = sweep.grid_sweep(M=rank_M(rank))
-    order = sweep.partition_lpt(sweep.estimate(cfgs, wls), 1)[0]  # longest first within the rank
-    ds = simsweep.DeviceSweep(cfgs, wls, cms, device=dev, order=np.asarray(order, np.int32))
+    cfgs, wls, cms, labels = sweep.grid_sweep(M=100_000)
+    # ONE sweep, LPT-sharded over the ranks (strong scaling); each shard longest-first on its GPU
+    sh = sweep.ShardedSweep(cfgs, wls, cms, device=dev)
+    order = sh.mine
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    slab = ds.d_results
-    gathered = torch.empty(world * slab.numel(), dtype=torch.uint8, device=dev) if world > 1 else None
 
     def one_step():
-        n = ds.launch(stream)
-        if world > 1:  # a12: the only collective -- gather per-simulation result rows (NCCL over NVLink)
+        n = sh.launch(stream)
+        if world > 1:  # a12: the only collective -- all outputs (rows + per-request slabs) to rank 0 over NVLink
             with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(gathered, slab)
+                sh.gather()
         return n
 
     with torch.cuda.stream(stream):
@@ -229,10 +227,10 @@ def bench_ours(args, rank, world, local_rank):
             flush.fill_(k & 0xFF)
             e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record(stream)
-            launches += ds.launch(stream)
+            launches += sh.launch(stream)
             e1.record(stream)
             if world > 1:
-                dist.all_gather_into_tensor(gathered, slab)
+                sh.gather()
             e2.record(stream)
             ev.append((e0, e1, e2))
     stream.synchronize()
@@ -242,7 +240,7 @@ def bench_ours(args, rank, world, local_rank):
     clk = clocks.stop()
     step_ms = [a.elapsed_time(c) for a, b, c in ev]
     kern_ms = [a.elapsed_time(b) for a, b, c in ev]
-    res = ds.fetch().results
+    res = sh.local().results
     bad = int((res["status"] != 0).sum())
     steps_rank = int(res["steps"].sum())
     visits_rank = int(res["visits"].sum())
@@ -259,7 +257,7 @@ def bench_ours(args, rank, world, local_rank):
     else:
         steps_all, visits_all, entries_all, launches_all = steps_rank, visits_rank, entries_rank, launches
     value = steps_all / (ms / 1000.0)
-    n_sims = len(cfgs) * world
+    n_sims = len(cfgs)
 
     # critical path (outside the timed region): the longest-estimated simulations, each launched alone.  The
     # sweep can never be shorter than its longest simulation (each simulation is one dependent chain of steps).
@@ -267,7 +265,8 @@ def bench_ours(args, rank, world, local_rank):
     if rank == 0 and not args.no_critical:
         # the 48 largest step-count estimates plus the 16 largest visit counts of this sweep (the estimate misses
         # vLLM's preemption thrash at small I, whose steps are all full steps)
-        top = list(dict.fromkeys([int(i) for i in order[:48]] + [int(i) for i in np.argsort(-res["visits"])[:16]]))
+        top = list(dict.fromkeys([int(order[j]) for j in range(min(48, len(order)))] +
+                                 [int(order[j]) for j in np.argsort(-res["visits"])[:16]]))
         alone = []
         for i in top:
             one = simsweep.DeviceSweep([simsweep.SimConfig.from_buffer_copy(cfgs[int(i)])], wls, cms, device=dev)
@@ -280,7 +279,7 @@ def bench_ours(args, rank, world, local_rank):
             alone.append((e0.elapsed_time(e1), int(i)))
         lm, li = max(alone)
         critical = {"longest_simulation_alone_ms": lm, "longest_simulation": "%s I=%d O=%d" % labels[li],
-                    "its_steps": int(res["steps"][li]), "sweep_kernel_over_longest": kms / lm,
+                    "its_steps": int(res["steps"][order.index(li)]), "sweep_kernel_over_longest": kms / lm,
                     "probed": f"{len(top)} simulations (largest LPT estimates and visit counts), each launched alone"}
 
     # e2e: the public host API (sim_sweep: pinned H2D + kernel + D2H, blocking), every step
@@ -288,30 +287,38 @@ def bench_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         pin = lambda n, dt: torch.empty(int(n), dtype={np.uint8: torch.uint8, np.float64: torch.float64,
                                                        np.int64: torch.int64}[dt], pin_memory=True).numpy()
-        out = simsweep.alloc_outputs(cfgs, wls, alloc=pin)
         pwls = []
         for w in wls:
             Ip = torch.from_numpy(w.I.copy()).pin_memory().numpy()
             Op = torch.from_numpy(w.O.copy()).pin_memory().numpy()
             Tp = torch.from_numpy(w.T.copy()).pin_memory().numpy()
             pwls.append(type(w)(Ip, Op, Tp, w.name))
-        sub_order = [simsweep.SimConfig.from_buffer_copy(cfgs[i]) for i in range(len(cfgs))]
-        simsweep.sim_sweep(sub_order, pwls, cms, device=local_rank, out=out)  # warm
+        sub = sh.plan.shard_configs(rank)  # this rank's shard, in LPT order
+        out = simsweep.alloc_outputs(sub, wls, alloc=pin) if sub else None
+
+        def e2e_step():
+            r = simsweep.sim_sweep(sub, pwls, cms, device=local_rank, out=out) if sub else sweep._empty_result()
+            if world > 1:  # host results -> rank 0 (rows + per-request slabs), one all_gather
+                sweep.gather_results(r, sh.plan, rank, device=dev)
+                torch.cuda.synchronize(dev)
+
+        e2e_step()  # warm
         if world > 1:
             dist.barrier()
         walls = []
         for _ in range(args.steps):
             t0 = time.perf_counter()
-            r = simsweep.sim_sweep(sub_order, pwls, cms, device=local_rank, out=out)
+            e2e_step()
             walls.append(time.perf_counter() - t0)
         ems = 1000.0 * statistics.mean(walls)
         if world > 1:
             t = torch.tensor([ems], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t[0])
-        h2d, d2h = simsweep.io_bytes(cfgs, wls, len(cms))
+        io = [simsweep.io_bytes(sh.plan.shard_configs(r), wls, len(cms)) for r in range(world)
+              if sh.plan.shards[r]]
         e2e = {"value": steps_all / (ems / 1000.0), "unit": UNIT, "ms_per_step": ems,
-               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+               "h2d_bytes_per_step": sum(a for a, _ in io), "d2h_bytes_per_step": sum(b for _, b in io),
                "api": "simsweep.sim_sweep (C-ABI sim_sweep, pinned host buffers, blocking)"}
 
     if rank != 0:
@@ -333,7 +340,7 @@ def bench_ours(args, rank, world, local_rank):
             traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
         "data": "synthetic",
         "config": workload_desc(world) | {"configs_per_s": n_sims / (ms / 1000.0), "kernel_ms": kms,
                                           "steps_per_sweep": steps_all, "batch_entries_per_sweep": entries_all,
@@ -349,10 +356,10 @@ def bench_ours(args, rank, world, local_rank):
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu_baseline:
         stride = 4
-        jobs = oracle_sample(stride, M=rank_M(0))
+        jobs = oracle_sample(stride)
         cores = min(host_cores(), len(jobs))
         s, dt = run_oracle(jobs, cores)
-        jobs1 = oracle_sample(48, M=rank_M(0))  # one core: "single-thread" next to "all host cores"
+        jobs1 = oracle_sample(48)  # one core: "single-thread" next to "all host cores"
         s1, dt1 = run_oracle(jobs1, 1)
         line["cpu_baseline"] = {"value": s / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
                                 "sample": f"every {stride}th simulation of the grid ({len(jobs)} of 1452), "

@@ -65,7 +65,10 @@ enum {
   SIM_S_NEVER_FITS = 2, /* I+O-1 (+ kv_watermark) > M, or > C without chunked prefill (reading Q35) */
   SIM_S_MAX_STEPS = 3,  /* more than max_steps batches */
   SIM_S_DEADLOCK = 4,   /* B empty, nothing arriving, requests unfinished (defensive) */
-  SIM_S_CAPACITY = 5    /* more than SIM_MAX_WINDOW arrived-but-unfinished requests (only if n > SIM_MAX_WINDOW) */
+  SIM_S_CAPACITY = 5    /* a limit of this implementation: more than SIM_MAX_WINDOW arrived-but-unfinished requests
+                           (only if n > SIM_MAX_WINDOW); or, with M infinite, KV holdings that could exceed 2^31 - 1
+                           (sum over requests of max(I+O-1, the initial reserve) >= 2^31; the holdings are int32);
+                           or more than 2^31 - 1 - n (re)admissions (the admission sequence number, reading Q6) */
 };
 /* call-level errors */
 enum {
@@ -177,21 +180,31 @@ int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wl
  * point to device memory), d_cms[n_cms], d_results[n_cfgs], d_row_off[n_cfgs],
  * d_tim_off[n_cfgs] and the members of d_req are DEVICE pointers.  The host
  * arrays h_cfgs / h_wls_n (n of each workload) describe the same configs and
- * are used only to choose kernel variants and launch order; d_order[n_cfgs]
+ * (n_wls entries) are used to validate every config field that does not need
+ * the workload contents (the checks of sim_validate() below except I, O and T:
+ * enums, knobs, C, M, S, n_cost, workload and cost indices; SIM_EINVAL /
+ * SIM_ECOST), to choose kernel variants and the launch order; d_order[n_cfgs]
  * (device, may be NULL) is a permutation giving the launch order (e.g.
  * longest-first).  Launches asynchronously on `stream` (cudaStream_t, NULL =
  * legacy default stream) and does not synchronize; validation of workload
- * contents is the caller's responsibility (sim_sweep does it).  d_workspace
+ * contents is the caller's responsibility (sim_validate() on the host copies,
+ * which sim_sweep and the Python DeviceSweep do).  d_workspace
  * (device, caller-owned, may be NULL when sim_workspace_bytes() is 0) holds
  * the state of simulations whose workload has n > 4096 requests; its first 4
  * bytes are reset on `stream` before use, so one workspace serves successive
  * calls on one stream.  Returns the number of kernel launches issued (>= 1) or
  * SIM_E* (SIM_EINVAL if the workspace is missing or smaller than needed). */
-int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n,
+int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, int32_t n_wls,
                      const sim_config_t* d_cfgs, const sim_workload_t* d_wls, const sim_cost_model_t* d_cms,
                      int32_t n_cms, const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
                      sim_result_t* d_results, sim_request_out_t d_req, void* d_workspace,
                      int64_t workspace_bytes, void* stream);
+
+/* Host-only validation of a sweep, exactly the checks sim_sweep() makes before it touches the device: every
+ * config field (SIM_EINVAL / SIM_ECOST), every cost model (SIM_ECOST) and every workload's contents (I, O >= 1,
+ * T sorted, T = 0 when n_cost > 1: SIM_EWORKLOAD).  HOST buffers.  Returns 0 or the first error found. */
+int sim_validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
+                 const sim_cost_model_t* cms, int32_t n_cms);
 
 /* ---- per-step schedule trace of one simulation (the schedule log of PAPER.md:714-719) ----
  * One record per step j (a batch B_j; an idle arrival jump is not a step), in step order; the entries of B_j in
@@ -288,6 +301,37 @@ int sim_slo_frontier(const sim_cost_model_t* cms, int32_t n_cms, const sim_slo_q
  * xfer_bw in bytes/s (> 0), M > 0.  Any output pointer may be NULL. */
 int sim_kv_break_even(const sim_cost_model_t* cms, int32_t n_cms, const int64_t* N, int32_t n, double xfer_bw, int64_t M,
                       double* recompute, double* swap, double* interval, int32_t device);
+
+/* Per-operator roofline classification ("What Makes a Batch Compute-Bound?"; Eq. (1)-(3),
+ * PAPER.md:1703-1729).  For one layer of the batch shape shapes[i] under model cms[k], each operator o of
+ * Eq. (3) (SIM_OP_*): its FLOPs and RW (elements; bytes = e * RW, reading Q26), its Eq. (3) time
+ * max(FLOPs / flops, e * RW / bw), its intensity FLOPs / RW (FLOPs per element, the unit of PAPER.md:538:
+ * attention -> 128 for large-c prefills and 2 / (1/128 + 1) ~ 1.98 for decodes on Llama-2-7B) and whether it is
+ * compute-bound (FLOPs / flops > e * RW / bw).  Attention is summed per request with B = 1 (reading Q24).  The
+ * operator times, summed in SIM_OP order (absent attentions skipped) and multiplied by `layers`, are the
+ * theoretical batch time of sim_batch_times() when tp = 1 (tp > 1 adds two All_Reduce terms, not operators of
+ * Eq. (3)).  The linear-mode coefficients are not used (every model carries its dims and GPU constants).
+ * out[(k * n + i) * SIM_N_OPS + o].  HOST buffers, blocking; SIM_EINVAL on a bad shape or n <= 0, SIM_ECOST on
+ * a bad model (flops and bw must be > 0). */
+enum {
+  SIM_OP_QKV = 0,          /* (N x h)(h x (N_Q + 2 N_KV) H) */
+  SIM_OP_O = 1,            /* (N x N_Q H)(N_Q H x h) */
+  SIM_OP_GATE_UP = 2,      /* (N x h)(h x 2f), SwiGLU (reading Q27) */
+  SIM_OP_DOWN = 3,         /* (N x f)(f x h) */
+  SIM_OP_ATTN_PREFILL = 4, /* Eq. (1)-(2) over the n_p prefill entries */
+  SIM_OP_ATTN_DECODE = 5,  /* Eq. (1)-(2) over the n_d decode entries (c = 1) */
+  SIM_N_OPS = 6
+};
+typedef struct {
+  int64_t flops;    /* FLOPs of the operator (one layer) */
+  int64_t rw;       /* elements read or written */
+  double time;      /* Eq. (3) seconds, one layer */
+  double intensity; /* flops / rw (FLOPs per element); 0 when the operator is absent */
+  int32_t bound;    /* 1 compute-bound, 0 memory-bound, -1 absent (no prefill / decode entry) */
+  int32_t pad;
+} sim_op_cost_t; /* 40 bytes */
+int sim_operator_costs(const sim_cost_model_t* cms, int32_t n_cms, const sim_batch_shape_t* shapes, int32_t n,
+                       sim_op_cost_t* out, int32_t device);
 
 /* ---- Exact optimum of the paper's CSP ----
  * A tiny offline workload of n <= SIM_OPT_MAX_N requests.  Every batch j chooses for each unfinished request

@@ -8,6 +8,10 @@ Eq. (1)-(3) / linear model, pinned in tests/test_oracle_cost.py); nothing here s
                    PAPER.md:567-600; tau = the paper's 1 s TPOT threshold, :574).  Reading (Q41):
                    prefills and decodes share one m.  The definition is a scan over m (slo_frontier_scan);
                    slo_frontier bisects, valid because d is non-decreasing in m (pinned by a property test)
+  operator_costs   per operator of Eq. (3) for one layer of a shape: FLOPs, RW elements, time, intensity FLOPs/RW,
+                   compute- or memory-bound ("What Makes a Batch Compute-Bound?", PAPER.md:505-539), from the
+                   oracle's own matmul_cost / attention_cost (Eq. (1)-(2)) summed per request
+                   with B = 1 (reading Q24)
   kv_break_even    recompute = d(one prefill entry c = N, m = 0); swap = N * 2 * layers * NKV * H * e / xfer_bw
                    (K and V over the host link); interval = recompute / N * M, the break-even
                    interval t^N_recom M / N of Eq. (9)
@@ -64,3 +68,41 @@ def kv_break_even(cost, N: int, xfer_bw: float, M: int):
     t = shape_time(cost, 1, N, 0, 0, 0)
     swap = float(N * kv_bytes_per_token(cost)) / float(xfer_bw)
     return t, swap, (t / float(N)) * float(M)
+
+
+OPS = ["qkv", "o", "gate_up", "down", "attn_prefill", "attn_decode"]
+
+
+def _roof(F: int, R: int, cost):
+    """Eq. (3): max(FLOPs / GPU_FLOPS, RW / GPU_bandwidth), RW bytes = e * elements (Q26).
+    -> (time, compute_bound)."""
+    tc = float(F) / cost.flops
+    tm = float(R * cost.e) / cost.bw
+    return max(tc, tm), tc > tm
+
+
+def operator_costs(cost, n_p: int, c: int, m_p: int, n_d: int, m_d: int) -> list:
+    """-> [dict(op, flops, rw, time, intensity, bound)] for one layer, ops in OPS order.  bound: 1 compute-bound,
+    0 memory-bound, -1 absent (no entry of that phase)."""
+    N = n_p * c + n_d  # tokens of the batch (the matmuls' c)
+    h, f, H, NQ, NKV = cost.h, cost.f, cost.H, cost.NQ, cost.NKV
+    mats = [(h, (NQ + 2 * NKV) * H), (NQ * H, h), (h, 2 * f), (f, h)]  # QKV, O, gate+up (SwiGLU, Q27), down
+    out = []
+    for name, (din, dout) in zip(OPS[:4], mats):
+        F, R = _o.matmul_cost(N, din, dout)
+        out.append((name, F, R))
+    for name, (nb, cc, mm) in ((OPS[4], (n_p, c, m_p)), (OPS[5], (n_d, 1, m_d))):
+        if nb == 0:
+            out.append((name, None, None))
+            continue
+        F1, R1 = _o.attention_cost(cc, mm, 1, H, NQ, NKV)  # one request, B = 1 (Q24); identical entries add up
+        out.append((name, nb * F1, nb * R1))
+    res = []
+    for name, F, R in out:
+        if F is None:
+            res.append(dict(op=name, flops=0, rw=0, time=0.0, intensity=0.0, bound=-1))
+            continue
+        t, cb = _roof(F, R, cost)
+        res.append(dict(op=name, flops=F, rw=R, time=t, intensity=(float(F) / float(R)) if R > 0 else 0.0,
+                        bound=1 if cb else 0))
+    return res

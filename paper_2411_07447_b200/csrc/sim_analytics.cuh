@@ -80,4 +80,46 @@ __global__ void kv_break_even_kernel(const sim_cost_model_t* cms, int n_cms, con
   }
 }
 
+// Per-operator roofline classification of one layer ("What Makes a Batch Compute-Bound?"):
+// the operators of Eq. (3) in batch_time's order, each with its FLOPs, RW elements, Eq. (3) time, intensity
+// FLOPs / RW and compute- vs memory-boundness.  Attention is summed per request with B = 1 (Q24).
+__device__ __forceinline__ void op_cost(long long F, long long R, const sim_cost_model_t& cm, sim_op_cost_t& o) {
+  const double tc = ddiv(i2d(F), cm.flops), tm = ddiv(i2d(R * (long long)cm.e), cm.bw);
+  o.flops = F;
+  o.rw = R;
+  o.time = fmax(tc, tm);  // == roof(F, R, cm)
+  o.intensity = R > 0 ? ddiv(i2d(F), i2d(R)) : 0.0;
+  o.bound = tc > tm ? 1 : 0;
+  o.pad = 0;
+}
+
+__global__ void operator_costs_kernel(const sim_cost_model_t* cms, int n_cms, const sim_batch_shape_t* shapes, int n,
+                                      sim_op_cost_t* out) {
+  const long long total = (long long)n * n_cms;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total; x += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(x / n), i = (int)(x % n);
+    const sim_cost_model_t& cm = cms[k];
+    const sim_batch_shape_t b = shapes[i];
+    const Feat f = shape_features(b.n_p, b.c, b.m_p, b.n_d, b.m_d, cm.H);
+    const long long h = cm.h, ff = cm.f, H = cm.H, NQ = cm.NQ, NKV = cm.NKV, N = f.N;
+    const long long qo = (NQ + 2 * NKV) * H, ao = NQ * H;
+    sim_op_cost_t* o = out + x * SIM_N_OPS;
+    op_cost(2 * N * h * qo, h * qo + N * h + N * qo, cm, o[SIM_OP_QKV]);
+    op_cost(2 * N * ao * h, ao * h + N * ao + N * h, cm, o[SIM_OP_O]);
+    op_cost(2 * N * h * (2 * ff), h * (2 * ff) + N * h + N * (2 * ff), cm, o[SIM_OP_GATE_UP]);
+    op_cost(2 * N * ff * h, ff * h + N * ff + N * h, cm, o[SIM_OP_DOWN]);
+    if (f.np > 0) {
+      op_cost(4 * H * NQ * f.pcm, 2 * H * NQ * f.cp + 2 * NQ * f.pcm + 2 * H * NKV * f.pceil[0], cm, o[SIM_OP_ATTN_PREFILL]);
+    } else {
+      o[SIM_OP_ATTN_PREFILL] = sim_op_cost_t{0, 0, 0.0, 0.0, -1, 0};
+    }
+    if (f.nd > 0) {
+      const long long s1m = f.md + f.nd;
+      op_cost(4 * H * NQ * s1m, 2 * H * NQ * f.nd + 2 * NQ * s1m + 2 * H * NKV * s1m, cm, o[SIM_OP_ATTN_DECODE]);
+    } else {
+      o[SIM_OP_ATTN_DECODE] = sim_op_cost_t{0, 0, 0.0, 0.0, -1, 0};
+    }
+  }
+}
+
 }  // namespace simsweep

@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   constexpr int SLB = __builtin_ctz(CAP);  // bits of a slot index
   static_assert((CAP & (CAP - 1)) == 0 && CAP <= 32768, "slots are int16 ring indices");
   constexpr unsigned FM = 0xffffffffu;
+  // the int32 admission counter (Q6) must not wrap: one step admits at most CAP requests
+  constexpr long long SEQ_LIM = 0x7fffffffll - CAP;
   extern __shared__ __align__(16) unsigned char smem[];
   Scal& S = *reinterpret_cast<Scal*>(smem);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -206,19 +208,22 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   }
   // ---- a1: per-simulation validation (Q35) ----
   int bad_long = 0, bad_fit = 0;
+  long long ub = 0;  // M infinite: an upper bound of the int32 holdings U (each request holds <= max(peak, reserve))
   for (int i = tid; i < n; i += NT) {
     long long pk = (long long)wl.I[i] + wl.O[i] - 1;  // peak KV usage
     bad_long |= pk > cfg.S;
     bad_fit |= (finiteM && blk((int)pk) + blk((int)cfg.kv_watermark) > M) || (!chunked && pk > cfg.C);
     bad_fit |= finiteM && cfg.reserve == SIM_RESERVE_CONTEXT && blk(cfg.S) + blk((int)cfg.kv_watermark) > M;  // Q35
+    if (!finiteM && pk <= cfg.S) ub += blk((int)(cfg.reserve == SIM_RESERVE_CONTEXT ? max(pk, (long long)cfg.S) : pk));
   }
   bad_long = __syncthreads_or(bad_long);
   bad_fit = __syncthreads_or(bad_fit);
-  if (bad_long || bad_fit) {
+  const bool bad_cap = !finiteM && block_sum_ll<NT>(ub, S) > 0x7fffffffll;  // (uniform branch: finiteM)
+  if (bad_long || bad_fit || bad_cap) {
     if (tid == 0) {
       sim_result_t r;
       memset(&r, 0, sizeof(r));
-      r.status = bad_long ? SIM_S_TOO_LONG : SIM_S_NEVER_FITS;
+      r.status = bad_long ? SIM_S_TOO_LONG : (bad_fit ? SIM_S_NEVER_FITS : SIM_S_CAPACITY);
       p.results[ci] = r;
     }
     return;
@@ -258,7 +263,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     int nx1;
     if (S.next >= n) {  // everything has arrived (offline after step 1): uniform checks, no barrier
       nx1 = n;
-      exit_status = S.n_done == n ? -1 : (S.steps >= cfg.max_steps ? SIM_S_MAX_STEPS : 0);
+      exit_status = S.n_done == n ? -1 : (S.steps >= cfg.max_steps ? SIM_S_MAX_STEPS : (S.seq > SEQ_LIM ? SIM_S_CAPACITY : 0));
     } else {
       if (tid == 0) {
         int a = S.next, b = n;
@@ -279,6 +284,8 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           st = SIM_S_CAPACITY;
         else if (S.steps >= cfg.max_steps)
           st = SIM_S_MAX_STEPS;
+        else if (S.seq > SEQ_LIM)
+          st = SIM_S_CAPACITY;
         S.status = st;
       }
       __syncthreads();

@@ -174,14 +174,42 @@ int64_t sim_workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int3
 
 }  // extern "C"
 
-static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, const sim_config_t* d_cfgs,
-                        const sim_workload_t* d_wls, const sim_cost_model_t* d_cms, int32_t n_cms,
-                        const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
+// Every config field that can be checked without the workload contents (SIM_EINVAL / SIM_ECOST); wls_n[n_wls] is
+// the size of each workload.  Shared by sim_validate / sim_sweep (host copies) and sim_sweep_device.
+static int validate_configs(const sim_config_t* cfgs, int32_t n_cfgs, const int32_t* wls_n, int32_t n_wls, int32_t n_cms) {
+  if (!cfgs || !wls_n || n_cfgs <= 0 || n_wls <= 0 || n_cms <= 0) return SIM_EINVAL;
+  for (int w = 0; w < n_wls; w++)
+    if (wls_n[w] <= 0) return SIM_EINVAL;
+  for (int i = 0; i < n_cfgs; i++) {
+    const sim_config_t& c = cfgs[i];
+    if (c.order < SIM_ORDER_PREFILL_FIRST || c.order > SIM_ORDER_RANK_O) return SIM_EINVAL;
+    if (c.replacement < SIM_NRF || c.replacement > SIM_PF) return SIM_EINVAL;
+    if (c.reserve < SIM_RESERVE_SEQ || c.reserve > SIM_RESERVE_CONTEXT) return SIM_EINVAL;
+    if ((c.replacement == SIM_PF) != (c.reserve != SIM_RESERVE_SEQ)) return SIM_EINVAL;  // Q39
+    if ((c.knobs & ~(SIM_KNOB_HOL | SIM_KNOB_NRF_ARRIVAL | SIM_KNOB_SRF_VISIT_ADMISSION)) || c.max_seqs < 0 ||
+        c.kv_watermark < 0 || c.kv_watermark >= (1 << 30) || ((c.knobs & SIM_KNOB_NRF_ARRIVAL) && c.replacement != SIM_NRF) ||
+        ((c.knobs & SIM_KNOB_SRF_VISIT_ADMISSION) && c.replacement != SIM_SRF && c.replacement != SIM_SRF_HIST) ||
+        c.kv_block < 0 || c.kv_block > (1 << 16) || (c.kv_block > 1 && c.replacement == SIM_SRF_HIST))
+      return SIM_EINVAL;  // alternative-reading knobs (SURVEY 8(f) row 3)
+    if ((c.hybrid != 0 && c.hybrid != 1) || (c.chunked != 0 && c.chunked != 1)) return SIM_EINVAL;
+    if (c.C < 1 || c.C > (1 << 30) || c.M > (1 << 30) || c.S < 1 || c.S > 262143 || c.max_steps < 1) return SIM_EINVAL;
+    if (c.n_cost < 1 || c.n_cost > SIM_MAX_COST) return SIM_EINVAL;
+    if (c.workload < 0 || c.workload >= n_wls) return SIM_EINVAL;
+    for (int k = 0; k < c.n_cost; k++)
+      if (c.cost[k] < 0 || c.cost[k] >= n_cms) return SIM_ECOST;
+  }
+  return 0;
+}
+
+static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, int32_t n_wls,
+                        const sim_config_t* d_cfgs, const sim_workload_t* d_wls, const sim_cost_model_t* d_cms,
+                        int32_t n_cms, const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
                         sim_result_t* d_results, sim_request_out_t d_req, void* d_workspace, int64_t workspace_bytes_,
                         void* stream, const TraceDev& tr) {
   if (!h_cfgs || !h_wls_n || !d_cfgs || !d_wls || !d_cms || n_cfgs <= 0 || n_cms <= 0 || !d_row_off ||
       !d_tim_off || !d_results || !d_req.t_first || !d_req.t_done || !d_req.n_preempt || !d_req.refill_tokens)
     return SIM_EINVAL;
+  if (int rc = validate_configs(h_cfgs, n_cfgs, h_wls_n, n_wls, n_cms)) return rc;
   bool need[N_VARIANTS] = {false, false, false, false, false, false};
   for (int i = 0; i < n_cfgs; i++)
     need[variant_of(h_wls_n[h_cfgs[i].workload]) + (has_knobs(h_cfgs[i]) ? N_SIZES : 0)] = true;
@@ -230,14 +258,14 @@ static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_
 
 extern "C" {
 
-int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, const sim_config_t* d_cfgs,
-                     const sim_workload_t* d_wls, const sim_cost_model_t* d_cms, int32_t n_cms,
-                     const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
+int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, int32_t n_wls,
+                     const sim_config_t* d_cfgs, const sim_workload_t* d_wls, const sim_cost_model_t* d_cms,
+                     int32_t n_cms, const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
                      sim_result_t* d_results, sim_request_out_t d_req, void* d_workspace, int64_t workspace_bytes_,
                      void* stream) {
   const TraceDev none{nullptr, nullptr, nullptr, 0, 0, 0};
-  return launch_sweep(h_cfgs, n_cfgs, h_wls_n, d_cfgs, d_wls, d_cms, n_cms, d_order, d_row_off, d_tim_off, d_results,
-                      d_req, d_workspace, workspace_bytes_, stream, none);
+  return launch_sweep(h_cfgs, n_cfgs, h_wls_n, n_wls, d_cfgs, d_wls, d_cms, n_cms, d_order, d_row_off, d_tim_off,
+                      d_results, d_req, d_workspace, workspace_bytes_, stream, none);
 }
 
 static int validate_cms(const sim_cost_model_t* cms, int32_t n_cms) {
@@ -256,26 +284,12 @@ static int validate_cms(const sim_cost_model_t* cms, int32_t n_cms) {
 static int validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
                     const sim_cost_model_t* cms, int32_t n_cms) {
   if (!cfgs || !wls || !cms || n_cfgs <= 0 || n_wls <= 0 || n_cms <= 0) return SIM_EINVAL;
+  std::vector<int32_t> wn(n_wls);
+  for (int w = 0; w < n_wls; w++) wn[w] = wls[w].n;
+  if (int rc = validate_configs(cfgs, n_cfgs, wn.data(), n_wls, n_cms)) return rc;
   std::vector<char> multi(n_wls, 0);
-  for (int i = 0; i < n_cfgs; i++) {
-    const sim_config_t& c = cfgs[i];
-    if (c.order < SIM_ORDER_PREFILL_FIRST || c.order > SIM_ORDER_RANK_O) return SIM_EINVAL;
-    if (c.replacement < SIM_NRF || c.replacement > SIM_PF) return SIM_EINVAL;
-    if (c.reserve < SIM_RESERVE_SEQ || c.reserve > SIM_RESERVE_CONTEXT) return SIM_EINVAL;
-    if ((c.replacement == SIM_PF) != (c.reserve != SIM_RESERVE_SEQ)) return SIM_EINVAL;  // Q39
-    if ((c.knobs & ~(SIM_KNOB_HOL | SIM_KNOB_NRF_ARRIVAL | SIM_KNOB_SRF_VISIT_ADMISSION)) || c.max_seqs < 0 ||
-        c.kv_watermark < 0 || c.kv_watermark >= (1 << 30) || ((c.knobs & SIM_KNOB_NRF_ARRIVAL) && c.replacement != SIM_NRF) ||
-        ((c.knobs & SIM_KNOB_SRF_VISIT_ADMISSION) && c.replacement != SIM_SRF && c.replacement != SIM_SRF_HIST) ||
-        c.kv_block < 0 || c.kv_block > (1 << 16) || (c.kv_block > 1 && c.replacement == SIM_SRF_HIST))
-      return SIM_EINVAL;  // alternative-reading knobs (SURVEY 8(f) row 3)
-    if ((c.hybrid != 0 && c.hybrid != 1) || (c.chunked != 0 && c.chunked != 1)) return SIM_EINVAL;
-    if (c.C < 1 || c.C > (1 << 30) || c.M > (1 << 30) || c.S < 1 || c.S > 262143 || c.max_steps < 1) return SIM_EINVAL;
-    if (c.n_cost < 1 || c.n_cost > SIM_MAX_COST) return SIM_EINVAL;
-    if (c.workload < 0 || c.workload >= n_wls) return SIM_EINVAL;
-    for (int k = 0; k < c.n_cost; k++)
-      if (c.cost[k] < 0 || c.cost[k] >= n_cms) return SIM_ECOST;
-    if (c.n_cost > 1) multi[c.workload] = 1;
-  }
+  for (int i = 0; i < n_cfgs; i++)
+    if (cfgs[i].n_cost > 1) multi[cfgs[i].workload] = 1;
   for (int w = 0; w < n_wls; w++) {
     const sim_workload_t& W = wls[w];
     if (W.n <= 0 || !W.I || !W.O || !W.T) return SIM_EINVAL;
@@ -478,7 +492,7 @@ static int host_run(const sim_config_t* cfgs_in, int32_t n_cfgs, const sim_workl
     tr.cap_steps = trace->cap_steps, tr.cap_entries = trace->cap_entries, tr.cap_events = trace->cap_events;
   }
   if (!rc) {
-    int l = launch_sweep(cfgs, n_cfgs, wn.data(), reinterpret_cast<const sim_config_t*>(base + o_cfg),
+    int l = launch_sweep(cfgs, n_cfgs, wn.data(), n_wls, reinterpret_cast<const sim_config_t*>(base + o_cfg),
                              reinterpret_cast<const sim_workload_t*>(base + o_wl),
                              reinterpret_cast<const sim_cost_model_t*>(base + o_cm), n_cms,
                              reinterpret_cast<const int32_t*>(base + o_ord),
@@ -513,6 +527,11 @@ static int host_run(const sim_config_t* cfgs_in, int32_t n_cfgs, const sim_workl
 }
 
 extern "C" {
+
+int sim_validate(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
+                 const sim_cost_model_t* cms, int32_t n_cms) {
+  return validate(cfgs, n_cfgs, wls, n_wls, cms, n_cms);
+}
 
 int sim_sweep(const sim_config_t* cfgs, int32_t n_cfgs, const sim_workload_t* wls, int32_t n_wls,
               const sim_cost_model_t* cms, int32_t n_cms, sim_result_t* results, sim_request_out_t req,
@@ -591,6 +610,26 @@ int sim_slo_frontier(const sim_cost_model_t* cms, int32_t n_cms, const sim_slo_q
   return run_analytics(cms, n_cms, q, n, outs, 1, device,
                        [&](int b, int t, const sim_cost_model_t* dc, const sim_slo_query_t* di, int64_t* dout, size_t) {
                          slo_frontier_kernel<<<b, t>>>(dc, n_cms, di, n, reinterpret_cast<long long*>(dout));
+                       });
+}
+
+int sim_operator_costs(const sim_cost_model_t* cms, int32_t n_cms, const sim_batch_shape_t* shapes, int32_t n,
+                       sim_op_cost_t* out, int32_t device) {
+  if (!shapes || !out || n <= 0) return SIM_EINVAL;
+  if (int rc = validate_cms(cms, n_cms)) return rc;
+  for (int k = 0; k < n_cms; k++)
+    if (!(cms[k].flops > 0) || !(cms[k].bw > 0) || cms[k].h < 1 || cms[k].f < 1 || cms[k].NQ < 1 || cms[k].NKV < 1)
+      return SIM_ECOST;
+  for (int i = 0; i < n; i++)
+    if (!shape_ok(shapes[i].n_p, shapes[i].c, shapes[i].m_p, shapes[i].n_d, shapes[i].m_d)) return SIM_EINVAL;
+  // run_analytics sizes its output as n * n_cms records: one record per (model, shape) holding SIM_N_OPS operators
+  struct Rec {
+    sim_op_cost_t op[SIM_N_OPS];
+  };
+  Rec* recs[1] = {reinterpret_cast<Rec*>(out)};
+  return run_analytics(cms, n_cms, shapes, n, recs, 1, device,
+                       [&](int b, int t, const sim_cost_model_t* dc, const sim_batch_shape_t* di, Rec* dout, size_t) {
+                         operator_costs_kernel<<<b, t>>>(dc, n_cms, di, n, reinterpret_cast<sim_op_cost_t*>(dout));
                        });
 }
 

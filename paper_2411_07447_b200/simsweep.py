@@ -123,10 +123,16 @@ def lib() -> ctypes.CDLL:
         L.sim_sweep.argtypes = [P(SimConfig), ctypes.c_int32, P(SimWorkload), ctypes.c_int32, P(SimCostModel),
                                 ctypes.c_int32, P(SimResult), SimRequestOut, ctypes.c_int32]
         L.sim_sweep_device.restype = ctypes.c_int
-        L.sim_sweep_device.argtypes = [P(SimConfig), ctypes.c_int32, P(ctypes.c_int32), ctypes.c_void_p,
+        L.sim_sweep_device.argtypes = [P(SimConfig), ctypes.c_int32, P(ctypes.c_int32), ctypes.c_int32, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, SimRequestOut,
                                        ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.sim_validate.restype = ctypes.c_int
+        L.sim_validate.argtypes = [P(SimConfig), ctypes.c_int32, P(SimWorkload), ctypes.c_int32, P(SimCostModel),
+                                   ctypes.c_int32]
+        L.sim_operator_costs.restype = ctypes.c_int
+        L.sim_operator_costs.argtypes = [P(SimCostModel), ctypes.c_int32, P(SimBatchShape), ctypes.c_int32,
+                                         ctypes.c_void_p, ctypes.c_int32]
         L.sim_run_traced.restype = ctypes.c_int
         L.sim_run_traced.argtypes = [P(SimConfig), P(SimWorkload), ctypes.c_int32, P(SimCostModel), ctypes.c_int32,
                                      P(SimResult), SimRequestOut, P(SimTrace), ctypes.c_int32]
@@ -155,8 +161,9 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-EXPORTED_SYMBOLS = ["sim_sweep", "sim_sweep_device", "sim_run_traced", "sim_workspace_bytes", "sim_request_rows", "sim_strerror",
-                    "sim_version", "sim_batch_times", "sim_slo_frontier", "sim_kv_break_even", "sim_optimum"]
+EXPORTED_SYMBOLS = ["sim_sweep", "sim_sweep_device", "sim_validate", "sim_run_traced", "sim_workspace_bytes",
+                    "sim_request_rows", "sim_strerror", "sim_version", "sim_batch_times", "sim_slo_frontier",
+                    "sim_kv_break_even", "sim_operator_costs", "sim_optimum"]
 
 
 def strerror(code: int) -> str:
@@ -295,6 +302,13 @@ def _wl_array(wls):
     return warr, keep
 
 
+def sim_validate(cfgs, wls: list[Workload], cms) -> None:
+    """Host-only validation (the checks sim_sweep makes before touching the device); raises SimError."""
+    cfgs = list(cfgs)
+    warr, _keep = _wl_array(wls)
+    _check(lib().sim_validate(_cfg_array(cfgs), len(cfgs), warr, len(wls), _cm_array(cms), len(cms)))
+
+
 def sim_sweep(cfgs, wls: list[Workload], cms, device: int = -1, out=None) -> SweepResult:
     """Host-buffer entry point: validates, copies in, simulates, copies out (blocking).
     `out` = alloc_outputs(...) to reuse (e.g. pinned) output buffers."""
@@ -320,6 +334,7 @@ class DeviceSweep:
         self.cfgs = list(cfgs)
         self.wls = wls
         self.dev = torch.device(device)
+        sim_validate(self.cfgs, wls, cms)  # the workload contents too: sim_sweep_device only checks config fields
         n_of, k_of, row_off, tim_off, rows, trows = _offsets(self.cfgs, wls)
         self.n_of, self.k_of, self.row_off_np, self.tim_off_np = n_of, k_of, row_off, tim_off
         self.h_cfgs = _cfg_array(self.cfgs)
@@ -359,7 +374,7 @@ class DeviceSweep:
         s = stream if stream is not None else self.torch.cuda.current_stream(self.dev)
         req = SimRequestOut(self.t_first.data_ptr(), self.t_done.data_ptr(), self.n_preempt.data_ptr(),
                             self.refill.data_ptr())
-        rc = lib().sim_sweep_device(self.h_cfgs, len(self.cfgs), self.h_wls_n, self.d_cfgs.data_ptr(),
+        rc = lib().sim_sweep_device(self.h_cfgs, len(self.cfgs), self.h_wls_n, len(self.wls), self.d_cfgs.data_ptr(),
                                     self.d_wls.data_ptr(), self.d_cms.data_ptr(), self.n_cms,
                                     self.d_order.data_ptr(), self.d_row_off.data_ptr(), self.d_tim_off.data_ptr(),
                                     self.d_results.data_ptr(), req, ctypes.c_void_p(self.ws.data_ptr()),
@@ -474,6 +489,24 @@ def sim_kv_break_even(cms, N, xfer_bw: float, M: int, device: int = -1):
                                    len(Nn), float(xfer_bw), int(M), outs[0].ctypes.data, outs[1].ctypes.data,
                                    outs[2].ctypes.data, int(device)))
     return tuple(o.reshape(len(cms), len(Nn)) for o in outs)
+
+
+OP_NAMES = ["qkv", "o", "gate_up", "down", "attn_prefill", "attn_decode"]  # SIM_OP_* order
+OP_COST_DTYPE = np.dtype([("flops", "<i8"), ("rw", "<i8"), ("time", "<f8"), ("intensity", "<f8"), ("bound", "<i4"),
+                          ("pad", "<i4")])  # == sim_op_cost_t
+
+
+def sim_operator_costs(cms, shapes, device: int = -1) -> np.ndarray:
+    """Per-operator roofline classification of one layer of every shape (n_p, c, m_p, n_d, m_d)
+    under every model: OP_COST_DTYPE [len(cms), len(shapes), 6] (operators in OP_NAMES order; bound 1 = compute,
+    0 = memory, -1 = absent)."""
+    cms = list(cms)
+    arr = np.ascontiguousarray(np.asarray(shapes, np.int64).reshape(-1, 5))
+    n = arr.shape[0]
+    out = np.zeros(len(cms) * n * len(OP_NAMES), OP_COST_DTYPE)
+    _check(lib().sim_operator_costs(_cm_array(cms), len(cms), arr.ctypes.data_as(ctypes.POINTER(SimBatchShape)), n,
+                                    out.ctypes.data, int(device)))
+    return out.reshape(len(cms), n, len(OP_NAMES))
 
 
 # ------------------------------------------------------------ exact CSP optimum (SURVEY.md 8(f) row 2)

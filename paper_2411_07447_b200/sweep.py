@@ -3,8 +3,10 @@
 Simulations are independent (single-instance serving), so a
 sweep shards with no data-path communication: each rank simulates its shard
 with one ``sim_sweep_device`` launch and the only collective is the final
-gather of fixed-size per-simulation result rows (sim_result_t, 200 B) to rank
-0 (NCCL over NVLink on GPUs; gloo in the CPU tests).
+gather of the outputs to rank 0 (NCCL over NVLink on GPUs; gloo in the CPU
+tests).  The gather moves the per-simulation rows AND the per-request slabs
+(t_first, t_done, n_preempt, refill), so rank 0 ends with exactly what one
+sim_sweep over the whole sweep returns.
 """
 from __future__ import annotations
 
@@ -87,54 +89,184 @@ def partition_lpt(est, n_ranks: int) -> list:
     return shards
 
 
-def gather_results(local: np.ndarray, local_idx, n_total: int, group=None, device=None):
-    """Gather per-simulation result rows (RESULT_DTYPE) of every rank to rank 0, reassembled in
-    global config order.  One all_gather of a fixed-size padded slab (the only collective)."""
+class ShardPlan:
+    """The LPT partition of one sweep over `world` ranks and the layout of every rank's output slab.
+
+    Every rank computes the same plan from the same configs (a pure function of the sweep), so the gather needs
+    no count exchange.  A rank's slab is [result rows | t_first | t_done | n_preempt | refill] of its shard in
+    shard order (the layout sim_sweep gives a sweep of those configs), padded to the largest slab.
+    """
+
+    def __init__(self, cfgs, wls, world: int):
+        self.cfgs, self.wls, self.world = list(cfgs), wls, int(world)
+        self.n_total = len(self.cfgs)
+        self.shards = partition_lpt(estimate(self.cfgs, wls), self.world)
+        self.n_of = np.array([wls[c.workload].n for c in self.cfgs], np.int64)
+        self.k_of = np.array([c.n_cost for c in self.cfgs], np.int64)
+        self.row_off = np.concatenate([[0], np.cumsum(self.n_of)[:-1]]).astype(np.int64)
+        self.tim_off = np.concatenate([[0], np.cumsum(self.n_of * self.k_of)[:-1]]).astype(np.int64)
+        self.rows, self.trows = int(self.n_of.sum()), int((self.n_of * self.k_of).sum())
+        item = simsweep.RESULT_DTYPE.itemsize
+        self.sizes = []  # per rank: (n_cfgs, rows, tim_rows)
+        for sh in self.shards:
+            sh = np.asarray(sh, np.int64)
+            self.sizes.append((len(sh), int(self.n_of[sh].sum()), int((self.n_of[sh] * self.k_of[sh]).sum())))
+        self.slab_bytes = [item * c + 16 * t + 16 * r for (c, r, t) in self.sizes]
+        self.cap = max(max(self.slab_bytes), 8)
+
+    def shard_configs(self, rank: int):
+        return [simsweep.SimConfig.from_buffer_copy(self.cfgs[i]) for i in self.shards[rank]]
+
+    def scatter_index(self, rank: int):
+        """Global row indices of rank's per-request rows (rows, tim_rows) in its shard order."""
+        rix, tix = [], []
+        for i in self.shards[rank]:
+            n, k = int(self.n_of[i]), int(self.k_of[i])
+            rix.append(self.row_off[i] + np.arange(n, dtype=np.int64))
+            tix.append(self.tim_off[i] + np.arange(n * k, dtype=np.int64))
+        cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64)  # noqa: E731
+        return cat(rix), cat(tix)
+
+
+def pack_slab(plan: ShardPlan, rank: int, results_u8, t_first, t_done, n_preempt, refill, out=None):
+    """This rank's outputs (torch tensors on any device) -> one uint8 slab of plan.cap bytes."""
+    import torch
+
+    dev = results_u8.device
+    slab = out if out is not None else torch.zeros(plan.cap, dtype=torch.uint8, device=dev)
+    off = 0
+    for t in (results_u8, t_first, t_done, n_preempt, refill):
+        if t.numel() == 0:  # (an empty shard)
+            continue
+        b = t.contiguous().view(torch.uint8).reshape(-1)
+        slab[off: off + b.numel()].copy_(b)
+        off += b.numel()
+    return slab
+
+
+class Assembler:
+    """Rank 0: the gathered slabs [world x cap] -> the full sweep's outputs in global config order (device ops)."""
+
+    def __init__(self, plan: ShardPlan, device):
+        import torch
+
+        self.plan, self.dev = plan, device
+        self.idx = []
+        for r in range(plan.world):
+            rix, tix = plan.scatter_index(r)
+            self.idx.append((torch.as_tensor(np.asarray(plan.shards[r], np.int64), device=device),
+                             torch.as_tensor(rix, device=device), torch.as_tensor(tix, device=device)))
+        item = simsweep.RESULT_DTYPE.itemsize
+        self.res = torch.zeros((plan.n_total, item), dtype=torch.uint8, device=device)
+        self.tf = torch.zeros(plan.trows, dtype=torch.float64, device=device)
+        self.td = torch.zeros(plan.trows, dtype=torch.float64, device=device)
+        self.npre = torch.zeros(plan.rows, dtype=torch.int64, device=device)
+        self.rf = torch.zeros(plan.rows, dtype=torch.int64, device=device)
+
+    def assemble(self, big):
+        import torch
+
+        item = simsweep.RESULT_DTYPE.itemsize
+        buf = big.reshape(self.plan.world, self.plan.cap)
+        for r, (nc, nr, nt) in enumerate(self.plan.sizes):
+            if nc == 0:
+                continue
+            ci, rix, tix = self.idx[r]
+            b = buf[r]
+            o = 0
+            self.res.index_copy_(0, ci, b[o: o + nc * item].reshape(nc, item))
+            o += nc * item
+            for dst, ix, cnt in ((self.tf, tix, nt), (self.td, tix, nt), (self.npre, rix, nr), (self.rf, rix, nr)):
+                dst.index_copy_(0, ix, b[o: o + 8 * cnt].view(dst.dtype))
+                o += 8 * cnt
+        return self
+
+    def result(self) -> simsweep.SweepResult:
+        p = self.plan
+        res = np.frombuffer(self.res.cpu().numpy().tobytes(), simsweep.RESULT_DTYPE).copy()
+        return simsweep.SweepResult(res, self.tf.cpu().numpy(), self.td.cpu().numpy(), self.npre.cpu().numpy(),
+                                    self.rf.cpu().numpy(), p.row_off, p.tim_off, p.n_of, p.k_of)
+
+
+def gather_slabs(plan: ShardPlan, slab, group=None):
+    """The sweep's only collective: all_gather_into_tensor of every rank's padded output slab (NCCL over NVLink on
+    GPUs, gloo on CPU).  Returns the [world * cap] uint8 tensor (every rank receives it; rank 0 assembles)."""
+    import torch
+    import torch.distributed as dist
+
+    big = torch.empty(plan.world * plan.cap, dtype=torch.uint8, device=slab.device)
+    dist.all_gather_into_tensor(big, slab, group=group)
+    return big
+
+
+def gather_results(local: simsweep.SweepResult, plan: ShardPlan, rank: int, group=None, device=None):
+    """Host-side gather of one rank's SweepResult (numpy) to a full SweepResult on rank 0 (None elsewhere):
+    per-simulation rows AND the per-request slabs (t_first, t_done, n_preempt, refill)."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    if world == 1:
-        out = np.zeros(n_total, simsweep.RESULT_DTYPE)
-        out[np.asarray(local_idx, np.int64)] = local
-        return out
-    item = simsweep.RESULT_DTYPE.itemsize
-    counts = torch.tensor([len(local_idx)], dtype=torch.int64, device=device if device is not None else "cpu")
-    allc = [torch.zeros_like(counts) for _ in range(world)]
-    dist.all_gather(allc, counts, group=group)
-    cap = int(max(int(c.item()) for c in allc))
-    slab = np.zeros(cap * item + 8 * cap, np.uint8)
-    slab[: len(local_idx) * item] = np.frombuffer(local.tobytes(), np.uint8)
-    slab[cap * item: cap * item + 8 * len(local_idx)] = np.frombuffer(
-        np.asarray(local_idx, np.int64).tobytes(), np.uint8)
     dev = device if device is not None else torch.device("cpu")
-    t = torch.from_numpy(slab).to(dev)
-    big = torch.empty(world * t.numel(), dtype=torch.uint8, device=dev)
-    dist.all_gather_into_tensor(big, t, group=group)
-    if dist.get_rank(group) != 0:
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).to(dev)  # noqa: E731
+    slab = pack_slab(plan, rank, t(local.results, np.uint8), t(local.t_first, np.float64), t(local.t_done, np.float64),
+                     t(local.n_preempt, np.int64), t(local.refill, np.int64))
+    big = gather_slabs(plan, slab, group) if world > 1 else slab
+    if rank != 0:
         return None
-    buf = big.cpu().numpy().reshape(world, -1)
-    out = np.zeros(n_total, simsweep.RESULT_DTYPE)
-    for r in range(world):
-        c = int(allc[r].item())
-        rows = np.frombuffer(buf[r, : c * item].tobytes(), simsweep.RESULT_DTYPE)
-        idx = np.frombuffer(buf[r, cap * item: cap * item + 8 * c].tobytes(), np.int64)
-        out[idx] = rows
-    return out
+    return Assembler(plan, dev).assemble(big).result()
+
+
+def _empty_result():
+    z = np.zeros(0, np.int64)
+    return simsweep.SweepResult(np.zeros(0, simsweep.RESULT_DTYPE), np.zeros(0), np.zeros(0), z, z.copy(), z, z, z, z)
+
+
+class ShardedSweep:
+    """One sweep partitioned over the ranks of `group` (LPT), each shard simulated by one sim_sweep_device call on
+    this rank's GPU, the outputs gathered to rank 0 by one all_gather of padded slabs (device tensors, NCCL)."""
+
+    def __init__(self, cfgs, wls, cms, group=None, device="cuda"):
+        import torch
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.dev = torch.device(device)
+        self.plan = ShardPlan(cfgs, wls, self.world)
+        self.mine = self.plan.shards[self.rank]
+        sub = self.plan.shard_configs(self.rank)
+        # a rank whose shard is empty (fewer simulations than ranks) still joins the collective with a zero slab
+        self.ds = simsweep.DeviceSweep(sub, wls, cms, device=self.dev, order=np.arange(len(sub))) if sub else None
+        self.slab = torch.zeros(self.plan.cap, dtype=torch.uint8, device=self.dev)
+        self.asm = Assembler(self.plan, self.dev) if self.rank == 0 else None
+
+    def launch(self, stream=None) -> int:
+        return self.ds.launch(stream) if self.ds is not None else 0
+
+    def gather(self):
+        """Pack this rank's device outputs, all_gather the slabs, assemble on rank 0 (enqueued on the current
+        stream).  Returns the number of collectives issued."""
+        if self.ds is not None:
+            d = self.ds
+            pack_slab(self.plan, self.rank, d.d_results, d.t_first, d.t_done, d.n_preempt, d.refill, out=self.slab)
+        big = gather_slabs(self.plan, self.slab, self.group) if self.world > 1 else self.slab
+        if self.rank == 0:
+            self.asm.assemble(big)
+        return 1 if self.world > 1 else 0
+
+    def local(self) -> simsweep.SweepResult:
+        return self.ds.fetch() if self.ds is not None else _empty_result()
+
+    def result(self):
+        """The full sweep's SweepResult on rank 0 (after gather()), None elsewhere."""
+        return self.asm.result() if self.rank == 0 else None
 
 
 def run_sharded(cfgs, wls, cms, group=None, device="cuda"):
-    """Simulate a sweep over all ranks of `group` (LPT shards), gather results on rank 0.
-    Returns (results on rank 0 / None elsewhere, this rank's shard indices, this rank's SweepResult)."""
-    import torch.distributed as dist
-
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    shards = partition_lpt(estimate(cfgs, wls), world)
-    mine = shards[rank]
-    sub = [simsweep.SimConfig.from_buffer_copy(cfgs[i]) for i in mine]
-    ds = simsweep.DeviceSweep(sub, wls, cms, device=device, order=np.arange(len(sub)))
-    ds.launch()
-    local = ds.fetch()
-    full = gather_results(local.results, mine, len(cfgs), group=group, device=ds.dev)
-    return full, mine, local
+    """Simulate a sweep over all ranks of `group` (LPT shards), gather every output to rank 0.
+    Returns (full SweepResult on rank 0 / None elsewhere, this rank's shard indices, this rank's SweepResult)."""
+    sh = ShardedSweep(cfgs, wls, cms, group=group, device=device)
+    sh.launch()
+    sh.gather()
+    return sh.result(), sh.mine, sh.local()

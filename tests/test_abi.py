@@ -47,6 +47,7 @@ def test_struct_layout_matches_header(tmp_path):
                    'printf("%zu %zu %zu\\n", sizeof(sim_opt_problem_t), offsetof(sim_opt_problem_t, C), sizeof(sim_opt_result_t));'
                    'printf("%zu %zu %zu %zu %zu\\n", sizeof(sim_trace_step_t), offsetof(sim_trace_step_t, start), '
                    'sizeof(sim_trace_entry_t), sizeof(sim_trace_event_t), sizeof(sim_trace_t));'
+                   'printf("%zu %zu\\n", sizeof(sim_op_cost_t), offsetof(sim_op_cost_t, bound));'
                    'return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
@@ -58,9 +59,10 @@ def test_struct_layout_matches_header(tmp_path):
             ctypes.sizeof(simsweep.SimBatchShape), ctypes.sizeof(simsweep.SimSloQuery), simsweep.SimSloQuery.tau.offset,
             ctypes.sizeof(simsweep.SimOptProblem), simsweep.SimOptProblem.C.offset, ctypes.sizeof(simsweep.SimOptResult),
             simsweep.TRACE_STEP_DTYPE.itemsize, simsweep.TRACE_STEP_DTYPE.fields["start"][1],
-            simsweep.TRACE_ENTRY_DTYPE.itemsize, simsweep.TRACE_EVENT_DTYPE.itemsize, ctypes.sizeof(simsweep.SimTrace)]
+            simsweep.TRACE_ENTRY_DTYPE.itemsize, simsweep.TRACE_EVENT_DTYPE.itemsize, ctypes.sizeof(simsweep.SimTrace),
+            simsweep.OP_COST_DTYPE.itemsize, simsweep.OP_COST_DTYPE.fields["bound"][1]]
     assert got == want
-    assert got[0] == 96 and got[-5:] == [48, 32, 16, 8, 72]
+    assert got[0] == 96 and got[-7:] == [48, 32, 16, 8, 72, 40, 32]
 
 
 def test_version_and_strerror(L):
@@ -100,6 +102,8 @@ def test_no_gpu_fails_loudly(L):
         simsweep.sim_kv_break_even([simsweep.unit_cost()], [4], 64e9, 100)
     with pytest.raises(simsweep.SimError, match="no sm_100"):
         simsweep.sim_optimum([([2, 2], [4, 4], 4096, 6)], simsweep.unit_cost())
+    with pytest.raises(simsweep.SimError, match="no sm_100"):
+        simsweep.sim_operator_costs([simsweep.unit_cost()], [(1, 1, 0, 0, 0)])
     with pytest.raises(simsweep.SimError, match="no sm_100"):
         simsweep.sim_run_traced(simsweep.preset_config("vllm", 100), [wl], [simsweep.unit_cost()])
 
@@ -151,5 +155,53 @@ def test_workspace_bytes_host_query(L):
     assert b1 > 32768 * 51 and b3 - 256 == 3 * (b1 - 256)
     assert L.sim_workspace_bytes(None, 1, n) == -1
     req = simsweep.SimRequestOut(1, 1, 1, 1)
-    rc = L.sim_sweep_device(simsweep._cfg_array(big), 3, n, 1, 1, 1, 1, None, 1, 1, 1, req, None, 0, None)
+    rc = L.sim_sweep_device(simsweep._cfg_array(big), 3, n, 2, 1, 1, 1, 1, None, 1, 1, 1, req, None, 0, None)
     assert rc == -1
+
+
+def test_device_entry_validates_configs(L):
+    """sim_sweep_device checks every config field it can without the workload contents (enums, knob
+    bits, C, M, S, n_cost, workload and cost indices) and returns SIM_EINVAL / SIM_ECOST before any device work;
+    a valid call with dummy (non-NULL) device pointers would launch, so only rejected calls are made here."""
+    n = (ctypes.c_int32 * 2)(16, 16)
+    req = simsweep.SimRequestOut(1, 1, 1, 1)
+
+    def call(c, n_wls=2, n_cms=1):
+        return L.sim_sweep_device(simsweep._cfg_array([c]), 1, n, n_wls, 1, 1, 1, n_cms, None, 1, 1, 1, req, None, 0,
+                                  None)
+
+    def mk(**kw):
+        c = simsweep.preset_config("vllm", 1000)
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+
+    for bad in (mk(workload=-1), mk(workload=2), mk(order=5), mk(replacement=4), mk(knobs=8), mk(C=0),
+                mk(C=(1 << 30) + 1), mk(M=(1 << 30) + 1), mk(S=0), mk(n_cost=0), mk(n_cost=5), mk(hybrid=2),
+                mk(replacement=3), mk(kv_block=-1), mk(max_seqs=-1)):
+        assert call(bad) == -1
+    c = mk()
+    c.cost[0] = 1
+    assert call(c) == -3  # cost index out of range (n_cms = 1)
+    assert call(mk(), n_wls=0) == -1
+
+
+def test_sim_validate_host_checks(L):
+    from paper_2411_07447_b200 import workloads
+    wl = workloads.fixed(2, 2, 4)
+    simsweep.sim_validate([simsweep.preset_config("vllm", 100)], [wl], [simsweep.unit_cost()])  # ok: no raise
+    online = workloads.Workload(np.array([1, 1], np.int32), np.array([1, 1], np.int32), np.array([0.0, 1.0]))
+    with pytest.raises(simsweep.SimError, match="invalid workload"):  # n_cost > 1 needs an offline workload
+        simsweep.sim_validate([simsweep.preset_config("vllm", 100, cost=(0, 0))], [online], [simsweep.unit_cost()])
+    with pytest.raises(simsweep.SimError, match="invalid argument"):
+        simsweep.sim_validate([simsweep.preset_config("vllm", 100, workload=-1)], [wl], [simsweep.unit_cost()])
+
+
+def test_operator_costs_rejects_bad_input(L):
+    cm = simsweep.load_cost_models()["llama3-8b_a100_theoretical"]
+    with pytest.raises(simsweep.SimError, match="invalid argument"):
+        simsweep.sim_operator_costs([cm], [(0, 1, 0, 0, 0)])
+    bad = simsweep.unit_cost()
+    bad.bw = 0.0
+    with pytest.raises(simsweep.SimError, match="cost"):
+        simsweep.sim_operator_costs([bad], [(1, 1, 0, 0, 0)])

@@ -83,3 +83,22 @@ def test_invalid_shapes_rejected():
         simsweep.sim_slo_frontier(cm, [(1, 1, 1, 10, 0.0)])
     with pytest.raises(simsweep.SimError, match="invalid argument"):
         simsweep.sim_kv_break_even(cm, [0], 64e9, 100_000)
+
+
+def test_operator_costs_exact():
+    """sim_operator_costs vs oracle/analytics.operator_costs: FLOPs, RW and boundness exact,
+    times and intensities 0 ULP, on the shape grid x all 12 models."""
+    shapes = shapes_grid(seed=3, n=300)
+    g = simsweep.sim_operator_costs([PCMS[k] for k in NAMES], shapes)
+    assert g.shape == (len(NAMES), len(shapes), len(simsweep.OP_NAMES))
+    for a, name in enumerate(NAMES):
+        for i, s in enumerate(shapes):
+            ref = an.operator_costs(OCMS[name], *s)
+            for o_, r in enumerate(ref):
+                x = g[a, i, o_]
+                assert (int(x["flops"]), int(x["rw"]), int(x["bound"])) == (r["flops"], r["rw"], r["bound"]), (name, s, o_)
+                assert float(x["time"]) == r["time"] and float(x["intensity"]) == r["intensity"], (name, s, o_)
+    # the paper's limits straight from the GPU: 128 / ~1.98 on Llama-2-7B (PAPER.md:538)
+    cm = PCMS["llama2-7b_a100_theoretical"]
+    lim = simsweep.sim_operator_costs([cm], [(256, 4096, 10_000_000, 0, 0), (0, 1, 0, 256, 10_000_000)])[0]
+    assert abs(lim[0, 4]["intensity"] - 128.0) < 0.02 and abs(lim[1, 5]["intensity"] - 2 / (1 / 128 + 1)) < 1e-3

@@ -108,3 +108,71 @@ def test_break_even_interval_decreases_with_N():
     cm = CMS["llama3-8b_h100_theoretical"]
     iv = [an.kv_break_even(cm, N, PCIE5_X16, 100_000)[2] for N in (1, 2, 4, 8, 16, 32, 64, 128, 256)]
     assert all(a > b for a, b in zip(iv, iv[1:]))
+
+
+# ---------------------------------------------------------------- per-operator roofline classification
+# "What Makes a Batch Compute-Bound?", Eq. (3) per operator.
+
+def _tiny_cost(flops=1.0, bw=1.0):
+    c = o.OracleCost()
+    c.mode, c.layers, c.h, c.f, c.H, c.NQ, c.NKV, c.e, c.tp = 1, 1, 2, 3, 1, 2, 1, 2, 1
+    c.flops, c.bw, c.link_bw = flops, bw, 1.0
+    return c
+
+
+def test_operator_costs_tiny_hand_sums():
+    # tiny dims h=2, f=3, H=1, N_Q=2, N_KV=1, e=2 B, FLOPS = BW = 1; one prefill (c=2, m=0), N = 2 (the hand sums
+    # of test_oracle_cost.py::test_theoretical_hand_sum_prefill):
+    #  QKV  F 32, RW 20 el = 40 B -> time 40, intensity 1.6, memory-bound (32 < 40)
+    #  O    F 16, RW 12 el -> 24, 4/3        G+U F 48, RW 28 el -> 56, 12/7     Down F 24, RW 16 el -> 32, 1.5
+    #  prefill attn F 32, RW 32 el -> 64, 1.0; no decode entry -> absent
+    ops = an.operator_costs(_tiny_cost(), 1, 2, 0, 0, 0)
+    assert [(x["op"], x["flops"], x["rw"], x["time"], x["bound"]) for x in ops] == [
+        ("qkv", 32, 20, 40.0, 0), ("o", 16, 12, 24.0, 0), ("gate_up", 48, 28, 56.0, 0), ("down", 24, 16, 32.0, 0),
+        ("attn_prefill", 32, 32, 64.0, 0), ("attn_decode", 0, 0, 0.0, -1)]
+    assert [x["intensity"] for x in ops[:5]] == [32 / 20, 16 / 12, 48 / 28, 24 / 16, 1.0]
+    # the same batch on a GPU with 100x the bandwidth: every operator now takes FLOPs / FLOPS -> compute-bound
+    fast = an.operator_costs(_tiny_cost(bw=100.0), 1, 2, 0, 0, 0)
+    assert [(x["time"], x["bound"]) for x in fast[:5]] == [(32.0, 1), (16.0, 1), (48.0, 1), (24.0, 1), (32.0, 1)]
+    # one decode (c = 1, m = 3), N = 1: attention F = 4*1*4*1*2 = 32, RW = 2*1*1*2 + 2*1*4*2 + 2*1*4*1*1 = 28
+    dec = an.operator_costs(_tiny_cost(), 0, 1, 0, 1, 3)
+    assert dec[4]["bound"] == -1 and (dec[5]["flops"], dec[5]["rw"], dec[5]["time"]) == (32, 28, 56.0)
+
+
+def test_attention_intensity_limits_paper():
+    # as c, m and B grow the attention intensity converges to 2 / (1/H + ceil(c/H) N_KV / (c N_Q));
+    # Llama-2-7B (H = 128, N_Q = N_KV = 32): 128 for large-c prefills, 2 / (1/128 + 1) ~ 1.98 for decodes.
+    cm = CMS["llama2-7b_a100_theoretical"]
+    assert (cm.H, cm.NQ, cm.NKV) == (128, 32, 32)
+    pre = an.operator_costs(cm, 256, 4096, 10_000_000, 0, 0)[4]["intensity"]
+    dec = an.operator_costs(cm, 0, 1, 0, 256, 10_000_000)[5]["intensity"]
+    assert abs(pre - 128.0) / 128.0 < 1e-4
+    assert abs(dec - 2.0 / (1.0 / 128.0 + 1.0)) < 1e-4 and abs(dec - 2.0) < 0.02
+
+
+def test_remark_attention_memory_bound_matmuls_can_be_compute_bound():
+    # Remark: "Attentions are memory-bound. Only matmuls can be compute-bound, when c is large
+    # enough to surpass the cost of loading fixed-size model weights."  On every A100 / H100 model of the paper.
+    names = [k for k in CMS if k.endswith("theoretical")]
+    shapes = [(1, 1, 0, 0, 0), (8, 4096, 0, 0, 0), (64, 4096, 100_000, 0, 0), (0, 1, 0, 256, 4096),
+              (1, 512, 1000, 1024, 100_000), (128, 2048, 2048, 128, 2048)]
+    for nm in names:
+        for s in shapes:
+            ops = an.operator_costs(CMS[nm], *s)
+            assert all(x["bound"] in (0, -1) for x in ops[4:]), (nm, s)  # attention: memory-bound (or absent)
+        small = an.operator_costs(CMS[nm], 1, 1, 0, 0, 0)
+        big = an.operator_costs(CMS[nm], 8, 4096, 0, 0, 0)  # N = 32768 tokens
+        assert all(x["bound"] == 0 for x in small[:4]), nm   # c = 1: weight loading dominates
+        assert all(x["bound"] == 1 for x in big[:4]), nm     # large c: FLOPs dominate
+
+
+def test_operator_times_sum_to_the_batch_time():
+    # Eq. (3) summed over the operators in batch_time's order, times the layers, IS the theoretical batch time
+    # (tp = 1: no All_Reduce term) -- bit for bit, the same additions in the same order (Q36)
+    for nm in [k for k in CMS if k.endswith("theoretical") and CMS[k].tp == 1]:
+        for s in [(1, 1, 0, 0, 0), (3, 129, 5, 7, 4000), (0, 1, 0, 64, 100_000), (128, 4096, 0, 0, 0)]:
+            t = 0.0
+            for x in an.operator_costs(CMS[nm], *s):
+                if x["bound"] >= 0:
+                    t = t + x["time"]
+            assert float(CMS[nm].layers) * t == an.shape_time(CMS[nm], *s), (nm, s)

@@ -56,57 +56,107 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _toy_sweep(n_cfgs):
+    """n_cfgs configs over 5 workloads of different sizes, K = 1 or 2 cost models (ragged slabs)."""
+    wls = [workloads.fixed(1, 1, n) for n in (3, 1, 7, 2, 5)]
+    cfgs = [simsweep.preset_config("vllm", 100, workload=i % 5, cost=(0,) * (1 + i % 2)) for i in range(n_cfgs)]
+    return cfgs, wls
+
+
+def _fingerprint(plan, rank):
+    """The outputs rank `rank` would produce for its shard, each value a function of its GLOBAL position."""
+    sh = plan.shards[rank]
+    nc, nr, nt = plan.sizes[rank]
+    res = np.zeros(nc, simsweep.RESULT_DTYPE)
+    res["steps"] = np.asarray(sh, np.int64) * 7 + 3
+    res["makespan"][:, 0] = np.asarray(sh) * 0.5
+    rix, tix = plan.scatter_index(rank)
+    local = simsweep.SweepResult(res, tix * 1.25, tix * 2.5 + 1, rix * 3, rix * 5 + 2, None, None, None, None)
+    assert local.t_first.shape == (nt,) and local.n_preempt.shape == (nr,)
+    return local
+
+
 def _gather_worker(rank, world, port, n_total, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    est = np.arange(n_total, 0, -1, dtype=np.float64) ** 1.5
-    shards = sweep.partition_lpt(est, world)
-    mine = shards[rank]
-    local = np.zeros(len(mine), simsweep.RESULT_DTYPE)
-    local["steps"] = np.asarray(mine) * 7 + 3  # a per-config fingerprint
-    local["status"] = 0
-    local["makespan"][:, 0] = np.asarray(mine) * 0.5
-    full = sweep.gather_results(local, mine, n_total)
+    cfgs, wls = _toy_sweep(n_total)
+    plan = sweep.ShardPlan(cfgs, wls, world)
+    full = sweep.gather_results(_fingerprint(plan, rank), plan, rank)
     if rank == 0:
-        np.save(out_path, full)
+        np.savez(out_path, res=full.results, tf=full.t_first, td=full.t_done, np_=full.n_preempt, rf=full.refill,
+                 ro=full.row_off, to=full.tim_off)
     else:
         assert full is None
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_gather_gloo_world2(tmp_path):
-    n_total = 137  # ragged: shards of unequal size
-    out = str(tmp_path / "full.npy")
-    mp.spawn(_gather_worker, args=(2, _free_port(), n_total, out), nprocs=2, join=True)
-    full = np.load(out, allow_pickle=False)
+@pytest.mark.parametrize("n_total,world", [(137, 2), (1, 2), (3, 4)])
+def test_gather_gloo(tmp_path, n_total, world):
+    """Ragged shards, and more ranks than simulations (empty shards still join the collective)."""
+    out = str(tmp_path / "full.npz")
+    mp.spawn(_gather_worker, args=(world, _free_port(), n_total, out), nprocs=world, join=True)
+    z = np.load(out, allow_pickle=False)
+    full = z["res"]
     assert full.dtype == simsweep.RESULT_DTYPE and full.shape == (n_total,)
     assert (full["steps"] == np.arange(n_total) * 7 + 3).all()
     assert np.array_equal(full["makespan"][:, 0], np.arange(n_total) * 0.5)
+    cfgs, wls = _toy_sweep(n_total)
+    n_of = np.array([wls[c.workload].n for c in cfgs])
+    k_of = np.array([c.n_cost for c in cfgs])
+    rows, trows = int(n_of.sum()), int((n_of * k_of).sum())
+    # every per-request row landed at its global row (the layout of one unsharded sim_sweep)
+    assert np.array_equal(z["tf"], np.arange(trows) * 1.25) and np.array_equal(z["td"], np.arange(trows) * 2.5 + 1)
+    assert np.array_equal(z["np_"], np.arange(rows) * 3) and np.array_equal(z["rf"], np.arange(rows) * 5 + 2)
+    assert np.array_equal(z["ro"], np.concatenate([[0], np.cumsum(n_of)[:-1]]))
+
+
+def test_shard_plan_layout():
+    cfgs, wls = _toy_sweep(40)
+    for world in (1, 3, 64):
+        plan = sweep.ShardPlan(cfgs, wls, world)
+        assert sorted(i for sh in plan.shards for i in sh) == list(range(40))
+        rows = np.concatenate([plan.scatter_index(r)[0] for r in range(world)])
+        trows = np.concatenate([plan.scatter_index(r)[1] for r in range(world)])
+        assert sorted(rows.tolist()) == list(range(plan.rows)) and sorted(trows.tolist()) == list(range(plan.trows))
+        assert plan.cap % 8 == 0 and plan.cap >= max(plan.slab_bytes)
 
 
 @pytest.mark.gpu
 def test_sharded_equals_unsharded():
-    """Independent simulations: splitting a sweep into LPT shards (one launch each, as N ranks would)
-    and reassembling gives exactly the unsharded results (SURVEY 8(e) byte-identity check)."""
+    """Independent simulations: splitting a sweep into LPT shards (one launch each, as N ranks would), packing each
+    shard's device outputs into its slab and assembling the slabs gives exactly the unsharded outputs -- result rows
+    and every per-request slab byte for byte (SURVEY 8(e) byte-identity check)."""
+    import torch
+
     cfgs, wls, cms, labels = sweep.grid_sweep(values=[1, 16, 256, 1024])
     whole = simsweep.DeviceSweep(cfgs, wls, cms)
     whole.launch()
     ref = whole.fetch()
-    for world in (2, 3, 8):
-        shards = sweep.partition_lpt(sweep.estimate(cfgs, wls), world)
-        full = np.zeros(len(cfgs), simsweep.RESULT_DTYPE)
-        for sh in shards:
-            if not sh:
-                continue
-            sub = [simsweep.SimConfig.from_buffer_copy(cfgs[i]) for i in sh]
-            ds = simsweep.DeviceSweep(sub, wls, cms)
-            ds.launch()
-            r = ds.fetch()
-            full[np.asarray(sh)] = r.results
-            for j, i in enumerate(sh):
-                a = r.request_times(j)
-                b = ref.request_times(i)
-                assert np.array_equal(a[1], b[1]) and np.array_equal(a[0], b[0])
-        assert full.tobytes() == ref.results.tobytes(), world
+    for world in (2, 3, 8, 200):  # 200 > 48 simulations: empty shards
+        plan = sweep.ShardPlan(cfgs, wls, world)
+        slabs = []
+        for r in range(world):
+            sub = plan.shard_configs(r)
+            slab = torch.zeros(plan.cap, dtype=torch.uint8, device="cuda")
+            if sub:
+                ds = simsweep.DeviceSweep(sub, wls, cms, order=np.arange(len(sub)))
+                ds.launch()
+                sweep.pack_slab(plan, r, ds.d_results, ds.t_first, ds.t_done, ds.n_preempt, ds.refill, out=slab)
+            slabs.append(slab)
+        full = sweep.Assembler(plan, torch.device("cuda")).assemble(torch.cat(slabs)).result()
+        assert full.results.tobytes() == ref.results.tobytes(), world
+        for a, b in ((full.t_first, ref.t_first), (full.t_done, ref.t_done), (full.n_preempt, ref.n_preempt),
+                     (full.refill, ref.refill)):
+            assert a.tobytes() == b.tobytes(), world
+
+
+@pytest.mark.gpu
+def test_run_sharded_single_rank():
+    """run_sharded without a process group (world 1) returns the unsharded outputs."""
+    cfgs, wls, cms, labels = sweep.grid_sweep(values=[2, 64], preset_names=["vllm", "sarathi"])
+    full, mine, local = sweep.run_sharded(cfgs, wls, cms)
+    ref = simsweep.sim_sweep(cfgs, wls, cms)
+    assert sorted(mine) == list(range(len(cfgs)))
+    assert full.results.tobytes() == ref.results.tobytes() and full.t_done.tobytes() == ref.t_done.tobytes()
