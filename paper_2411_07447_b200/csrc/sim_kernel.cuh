@@ -41,7 +41,7 @@ struct TraceDev {
 };
 
 struct KParams {
-  unsigned char* ws;  // large-window variant: [WS_HEADER | arenas], the counter at ws[0]
+  unsigned char* ws;  // large-window variants: [WS_HEADER (arena counters) | arenas]
   const sim_config_t* cfgs;
   const sim_workload_t* wls;
   const sim_cost_model_t* cms;
@@ -52,6 +52,9 @@ struct KParams {
   sim_request_out_t req;
   int32_t n_cfgs;
   int32_t variant;
+  int32_t lean;        // route the eligible configs to the lean one-warp kernel (kernel_variant)
+  int32_t arena_base;  // GM variants: this launch's first arena (the two GM variants may run concurrently)
+  int32_t ctr_off;     // GM variants: byte offset of this launch's arena counter in the workspace header
   TraceDev tr;
 };
 
@@ -339,6 +342,6 @@ struct Smem {
   static constexpr size_t arr_bytes = (off_union + 8 * CAP + 255) & ~size_t(255);
   static constexpr size_t bytes = scal + arr_bytes;  // all in shared memory
 };
-constexpr size_t WS_HEADER = 256;  // workspace header: the arena counter
+constexpr size_t WS_HEADER = 256;  // workspace header: the arena counters (one per GM variant, 64 B apart)
 
 }  // namespace simsweep

@@ -1,0 +1,903 @@
+// sim_lean.cuh -- the lean step kernel: ONE WARP per simulation (included by simsweep.cu).
+//
+// The same method and readings as sim_step.cuh (Algorithm 1; Q1-Q40), for the
+// configurations that dominate the north-star sweep (lean_ok in simsweep.cu): the vLLM / Sarathi presets
+// (prefill-first without chunking, or decode-first), NRF / SRF / PF, no alternative-reading knob, no SRF+Hist,
+// no schedule trace, n <= CAP requests.  Everything a step decides (tok, U, seq, list lengths, counters) lives
+// in registers, uniform across the warp; lane k < K holds the clock of cost model k; per-request state is a
+// structure of arrays in shared memory.  A step is a few warp passes with no block barrier and no
+// shared-memory broadcast: the per-step latency IS the sweep's critical path.
+//
+// One step (one batch B_j):
+//   a2    arrivals: the next arrival time stays in a register; a ballot pass admits every T <= clock (Q21)
+//   a3-a8 GetNextBatch, the exact mechanisms of the block kernel on one warp:
+//         * the running decodes in closed form (decode group): head i (the i-th decode in retention order, at
+//           run position p_i) is admitted iff i <= C - tok and F + U0 - PS(p_i) >= i (F = M - U, U0 = the run
+//           list's holdings, PS = prefix sum of holdings over run positions <= p_i; monotone in i, so the walk
+//           stops at the first failing head); the minimal tail suffix [q*, n) with F + U0 - PS(q* - 1) >= a is
+//           evicted; if the KV stopped the walk, head a+1 evicts everything behind it and self-preempts
+//           (Q8)
+//         * the waiting group and the running prefills (they never preempt, Q5): 32 candidates per pass,
+//           ballot + prefix scan, the first cumulative failure dropped, a cropped chunk ends the group
+//   a9    exact integer features by warp reductions; lane k < K evaluates cost model k (no FMA, Q36)
+//   a10   Process: the batch is the run list's decodes before p_{a+1}, the flagged running prefills and this
+//         step's admissions -- nothing is copied into a batch list
+//   runs  steady decode runs are charged in closed form (features affine in the step index); the clock chain
+//         stays one sequential fp64 add per step (Q36)
+//   a3'   the run list for the next step: the evicted suffix is cut, completions are compacted out, admissions
+//         are appended (NRF / PF: admission order) or, for SRF, this step's prefill entries (the only keys that
+//         moved) are merged back by (m desc, seq) (Q3, Q7)
+#pragma once
+
+namespace simsweep {
+
+constexpr uint8_t F_INB_L = 8;    // a running prefill admitted into this step's batch
+constexpr uint8_t F_MOVE_L = 64;  // SRF: a prefill entry of this step's batch that stays running (its key moved)
+
+struct LHead {
+  sim_cost_model_t cm[SIM_MAX_COST];
+};
+
+template <int CAP>
+struct LLayout {
+  static constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+  static constexpr size_t rec = a16(sizeof(LHead));  // int4 {I, g, m, reserved}
+  static constexpr size_t O = rec + 16 * CAP;        // int32
+  static constexpr size_t seq = O + 4 * CAP;         // int32 admission sequence number (Q6)
+  static constexpr size_t c = seq + 4 * CAP;         // int32 c of the running prefills of this batch  \ u64 sort keys
+  static constexpr size_t ev = c + 4 * CAP;          // int32 first-token / completion events          / (SRF merge)
+  static constexpr size_t run = ev + 4 * CAP;        // int16 run list (retention order)
+  static constexpr size_t run2 = run + 2 * CAP;      // int16 second run list (merge target)
+  static constexpr size_t nw = run2 + 2 * CAP;       // int16 admitted from R_w this step, in admission order
+  static constexpr size_t vic = nw + 2 * CAP;        // int16 preempted this step, then the SRF movers
+  static constexpr size_t fl = vic + 2 * CAP;        // uint8 status and flags
+  static constexpr size_t bytes = a16(fl + CAP);     // 41 B per slot
+};
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// SRF retention key (ascending = retained longer): m descending, then admission order (Q3, Q7); the slot rides in
+// the low bits so that sorting keys sorts slots
+template <int SLB>
+__device__ __forceinline__ unsigned long long srf_key(int m, int seq, int slot) {
+  return ((unsigned long long)(0x3FFFF - m) << 43) | ((unsigned long long)(unsigned)seq << SLB) | (unsigned)slot;
+}
+
+template <int CAP>
+__global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
+  using L = LLayout<CAP>;
+  constexpr unsigned FM = 0xffffffffu;
+  constexpr int SLB = __builtin_ctz(CAP);
+  static_assert(SLB <= 12, "slot bits of the SRF key");
+  constexpr long long SEQ_LIM = 0x7fffffffll - CAP;  // the int32 admission counter must not wrap
+  extern __shared__ __align__(16) unsigned char smem[];
+  LHead& H = *reinterpret_cast<LHead*>(smem);
+  const int lane = threadIdx.x;
+  const unsigned lt = (1u << lane) - 1u;
+  const int ci = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
+  if (kernel_variant(p.cfgs[ci], p.wls[p.cfgs[ci].workload].n, p.lean) != p.variant) return;
+  int4* s_rec = reinterpret_cast<int4*>(smem + L::rec);
+  int32_t* s_O = reinterpret_cast<int32_t*>(smem + L::O);
+  int32_t* s_seq = reinterpret_cast<int32_t*>(smem + L::seq);
+  int32_t* s_c = reinterpret_cast<int32_t*>(smem + L::c);
+  int32_t* s_ev = reinterpret_cast<int32_t*>(smem + L::ev);
+  double* s_dbuf = reinterpret_cast<double*>(smem + L::ev);                    // steady run: CAP/2 batch times
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem + L::c);  // SRF merge: CAP keys
+  int16_t* s_run = reinterpret_cast<int16_t*>(smem + L::run);
+  int16_t* s_run2 = reinterpret_cast<int16_t*>(smem + L::run2);
+  int16_t* s_new = reinterpret_cast<int16_t*>(smem + L::nw);
+  int16_t* s_vic = reinterpret_cast<int16_t*>(smem + L::vic);
+  uint8_t* s_fl = smem + L::fl;
+
+  const sim_config_t cfg = p.cfgs[ci];
+  const sim_workload_t wl = p.wls[cfg.workload];
+  const int n = wl.n, K = cfg.n_cost;
+  const bool finiteM = cfg.M >= 0, hybrid = cfg.hybrid != 0, chunked = cfg.chunked != 0;
+  const int M = finiteM ? (int)cfg.M : 0, C = (int)cfg.C;  // host-validated <= 2^30
+  const bool pfirst = cfg.order == SIM_ORDER_PREFILL_FIRST;  // {R_w, R_r} (never chunked here), else {R_r^d, R_r^p, R_w}
+  const bool srf = cfg.replacement == SIM_SRF;
+  const int rmode = cfg.reserve;
+  const bool kv1 = rmode == SIM_RESERVE_SEQ;  // a decode needs one KV (else its PEAK / CONTEXT reserve covers it, Q39)
+  const long long row0 = p.row_off[ci], tim0 = p.tim_off[ci];
+  double* tf = p.req.t_first + tim0;
+  double* td = p.req.t_done + tim0;
+  unsigned long long* npre = reinterpret_cast<unsigned long long*>(p.req.n_preempt + row0);
+  unsigned long long* refill = reinterpret_cast<unsigned long long*>(p.req.refill_tokens + row0);
+  for (int i = lane; i < n; i += 32) npre[i] = 0, refill[i] = 0;
+  for (int x = lane; x < K * n; x += 32) tf[x] = 0.0, td[x] = 0.0;
+
+  // ---- a1: per-simulation validation (Q35) and the int32 holdings bound (M infinite) ----
+  {
+    int bad_long = 0, bad_fit = 0;
+    long long ub = 0;
+    for (int i = lane; i < n; i += 32) {
+      const long long pk = (long long)wl.I[i] + wl.O[i] - 1;  // peak KV usage
+      bad_long |= pk > cfg.S;
+      bad_fit |= (finiteM && pk > M) || (!chunked && pk > cfg.C);
+      bad_fit |= finiteM && rmode == SIM_RESERVE_CONTEXT && cfg.S > M;
+      if (!finiteM && pk <= cfg.S) ub += rmode == SIM_RESERVE_CONTEXT ? max(pk, (long long)cfg.S) : pk;
+    }
+    bad_long = __any_sync(FM, bad_long);
+    bad_fit = __any_sync(FM, bad_fit);
+    const bool bad_cap = !finiteM && warp_sum_ll(ub) > 0x7fffffffll;
+    if (bad_long || bad_fit || bad_cap) {
+      if (lane == 0) {
+        sim_result_t r;
+        memset(&r, 0, sizeof(r));
+        r.status = bad_long ? SIM_S_TOO_LONG : (bad_fit ? SIM_S_NEVER_FITS : SIM_S_CAPACITY);
+        p.results[ci] = r;
+      }
+      return;
+    }
+  }
+  if (lane < K) H.cm[lane] = p.cms[cfg.cost[lane]];
+  bool anyTheo = false;
+  int Hk[SIM_MAX_COST] = {1, 1, 1, 1};  // attention head dim per model (the ceil(c/H) feature, Eq. (2))
+#pragma unroll
+  for (int k = 0; k < SIM_MAX_COST; k++)
+    if (k < K) {
+      const sim_cost_model_t* cm = p.cms + cfg.cost[k];
+      anyTheo |= cm->mode == 1;
+      Hk[k] = cm->H;
+    }
+  __syncwarp();
+
+  double clk = 0.0;  // lane k < K: the clock of cost model k
+  int U = 0, seq = 0, next = 0, lo = 0, n_done = 0, nrun = 0, n_rd = 0, nW = 0, minSW = 0x7fffffff, wfirst = 0;
+  int wstale = 0;
+  bool w_dirty = true;
+  double Tnext = wl.T[0];  // arrival time of request `next`
+  long long steps = 0, preempt = 0, entries = 0, processed = 0, sumU = 0, pentries = 0, idle = 0, visits = 0;
+  int exit_status = 0;
+
+  for (;;) {
+    // ---- (1) a2: GetNewRequests (Alg. 1 line 3): all T <= clock, inclusive (Q21) ----
+    int nx1 = next;
+    if (next < n && Tnext <= __shfl_sync(FM, clk, 0)) {
+      const double clk0 = __shfl_sync(FM, clk, 0);
+      for (;;) {
+        const int idx = nx1 + lane;
+        const bool arr = idx < n && wl.T[idx] <= clk0;
+        const unsigned b = __ballot_sync(FM, arr);  // T is sorted: the arrivals are a prefix
+        if (arr) {
+          s_rec[idx] = make_int4(wl.I[idx], 0, 0, 0);
+          s_O[idx] = wl.O[idx];
+          s_seq[idx] = 0;
+          s_fl[idx] = ST_WAIT;
+        }
+        nx1 += __popc(b);
+        if (b != FM) break;
+      }
+      wfirst = min(wfirst, next);  // the new arrivals wait
+      w_dirty = true;
+      if (nx1 < n) Tnext = wl.T[nx1];
+      __syncwarp();
+    }
+    if (n_done == n) {
+      exit_status = -1;
+      break;
+    }
+    if (steps >= cfg.max_steps) {
+      exit_status = SIM_S_MAX_STEPS;
+      break;
+    }
+    if (seq > SEQ_LIM) {
+      exit_status = SIM_S_CAPACITY;
+      break;
+    }
+    const int Lw = nx1 - lo;  // window offsets [0, Lw): slot = lo + offset (n <= CAP: no ring)
+    const int w0 = max(wfirst - lo, 0);
+    if (w_dirty) {  // |R_w| and its smallest s (the skip test), exact
+      int cnt = 0, mn = 0x7fffffff;
+      for (int q = w0 + lane; q < Lw; q += 32) {
+        const int sl = lo + q;
+        if ((s_fl[sl] & ST_MASK) == ST_WAIT) {
+          const int4 r = s_rec[sl];
+          cnt++;
+          mn = min(mn, r.x + r.y);
+        }
+      }
+      nW = (int)__reduce_add_sync(FM, (unsigned)cnt);
+      minSW = (int)__reduce_min_sync(FM, (unsigned)mn);
+      w_dirty = false;
+      wstale = 0;
+    }
+    const int nrun0 = nrun, U0 = U;  // U0: holdings of the run list (only running requests hold KVs)
+    const long long nP = (long long)nW + nrun;
+    visits += nP;  // |P| (Alg. 1 line 9)
+
+    // ---- (2) a3-a8: GetNextBatch (steps 2-4) ----
+    int tok = 0, n_new = 0, bph = -1, n_vic = 0;
+    int pa1 = 0;       // the decodes at run positions < pa1 are in B
+    int cut = nrun;    // run positions >= cut were evicted this step
+    int rp_first = nrun;  // no running prefill before this run position
+    int wnext = -1;
+    auto rnew = [&](const int4& rc, int sl) -> int {  // the reserve taken at (re)admission (Table 2, Q13, Q39)
+      return rmode == SIM_RESERVE_SEQ ? rc.x + rc.y : (rmode == SIM_RESERVE_PEAK ? rc.x + s_O[sl] - 1 : cfg.S);
+    };
+
+    // Candidates that never preempt (Q5): the waiting group in index order (src 1: window offsets [b0, b1)) or the
+    // running prefills in retention order (src 2: run positions [b0, b1); their KV delta is 0 since reserved >= s).
+    auto warp_np = [&](int src, int b0, int b1) {
+      const bool overWin = src == 1;
+      const bool scand = overWin && !kv1;  // KV deltas differ from c under PEAK / CONTEXT: scan them too
+      bool wcont = overWin;                // every waiting request at offsets [b0, i0) was admitted
+      if (overWin) wnext = b0;
+      for (int i0 = b0; i0 < b1; i0 += 32) {
+        if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining candidate fails
+        if (overWin && ((finiteM && U + minSW > M) || (!chunked && minSW > C - tok))) return;
+        const int i = i0 + lane;
+        int sl = -1;
+        if (i < b1) {
+          const int s2 = overWin ? lo + i : s_run[i];
+          const uint8_t f2 = s_fl[s2];
+          if (overWin ? (f2 & (ST_MASK | F_PRE)) == ST_WAIT : (f2 & (ST_MASK | F_PRE | F_FILLED)) == ST_RUN) sl = s2;
+        }
+        if (!__any_sync(FM, sl >= 0)) {
+          if (wcont) wnext = min(i0 + 32, b1);
+          continue;
+        }
+        const int4 rc = s_rec[sl < 0 ? 0 : sl];
+        const int s = rc.x + rc.y, avail = s - rc.z;
+        const int dkv = overWin ? rnew(rc, sl < 0 ? 0 : sl) : 0;  // the initial reserve >= s >= c (Q13)
+        bool alive = sl >= 0, admitted = false;
+        for (;;) {
+          const int rt = C - tok;
+          const bool fit = alive && rt >= 1 && (chunked || avail <= rt) && (!finiteM || U + dkv <= M);
+          const unsigned fm = __ballot_sync(FM, fit);
+          if (!fm) break;
+          const int cc = fit ? avail : 0, dk = fit ? dkv : 0;
+          int xc = cc, xd = dk;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int yc = __shfl_up_sync(FM, xc, o);
+            if (lane >= o) xc += yc;
+            if (scand) {
+              const int yd = __shfl_up_sync(FM, xd, o);
+              if (lane >= o) xd += yd;
+            }
+          }
+          const int ec = xc - cc, ek = __popc(fm & lt);
+          const int ed = overWin ? (scand ? xd - dk : ec) : 0;  // SEQ: a waiting admission reserves exactly c = s
+          bool brk = false, crop = false;
+          if (fit) {
+            const int prt = rt - ec;
+            if (chunked)
+              crop = prt < avail;  // cropped (c = prt >= 1) or exhausted (prt <= 0)
+            else
+              brk = avail > prt;
+            if (finiteM) brk |= U + ed + dkv > M;
+            if (crop && prt <= 0) brk = true;
+          }
+          const unsigned bm = __ballot_sync(FM, brk), cm = __ballot_sync(FM, crop && !brk);
+          const int b = bm ? __ffs(bm) - 1 : 32, cl = cm ? __ffs(cm) - 1 : 32;
+          const int stop = min(b, cl);
+          const bool adm = fit && lane < stop, adc = fit && lane == cl && cl < b;
+          if (adm || adc) {
+            s_c[sl] = adm ? avail : rt - ec;
+            if (overWin) {
+              s_seq[sl] = seq + ek + 1;
+              s_rec[sl] = make_int4(rc.x, rc.y, 0, dkv);
+              s_fl[sl] = ST_RUN | (s_fl[sl] & F_FIRST);
+              s_new[n_new + ek] = (int16_t)sl;
+            } else {
+              s_fl[sl] |= F_INB_L;
+            }
+            alive = false;
+            admitted = true;
+          }
+          const bool cropped = cl < b && cl < 32;
+          const int nadm = __popc(fm & (stop >= 32 ? FM : ((1u << stop) - 1u)));
+          const int lastl = stop > 0 ? min(stop, 32) - 1 : 0;
+          const int addc = stop > 0 ? __shfl_sync(FM, xc, lastl) : 0;
+          const int addd = (scand && stop > 0) ? __shfl_sync(FM, xd, lastl) : addc;
+          int cropc = 0, crops = 0;
+          if (cropped) {
+            cropc = __shfl_sync(FM, rt - ec, cl);
+            crops = __shfl_sync(FM, dkv, cl);
+          }
+          const int nall = nadm + (cropped ? 1 : 0);
+          tok += addc + cropc;
+          if (overWin) {
+            U += addd + crops;
+            seq += nall, n_new += nall;
+          }
+          if (nall > 0 && bph < 0) bph = PH_PRE;
+          if (cropped) break;  // the token budget is exhausted: every later candidate is rejected
+          if (b < 32 && lane == b) alive = false;  // rejected (no state change)
+          if (b >= 32) break;
+        }
+        if (wcont) {  // advance the waiting bound past this chunk unless a waiting request is left in it
+          const unsigned lf = __ballot_sync(FM, sl >= 0 && !admitted);
+          if (lf) {
+            wnext = i0 + __ffs(lf) - 1;
+            wcont = false;
+          } else {
+            wnext = min(i0 + 32, b1);
+          }
+        }
+        if (chunked && tok >= C) return;
+      }
+    };
+
+    // The running decodes in closed form (see the file header).  Heads = the F_FILLED entries of the run list in
+    // retention order; the victim pool is the run list's tail (all running, none in B yet).
+    auto decode_group = [&]() {
+      const bool fM = finiteM && kv1;  // heads need one KV each (else none: admitted up to the token budget)
+      const int F = fM ? M - U : 0x3fffffff;
+      const int T = C - tok;
+      int a = n_rd;                      // heads admitted
+      bool kvstop = false;               // the KV test (not the token budget) stopped the walk at pa1
+      pa1 = nrun;
+      if (F < n_rd || T < n_rd) {        // some head fails a test: walk the heads while they pass
+        int ps = 0, hs = 0;
+        for (int q0 = 0; q0 < nrun; q0 += 32) {
+          const int q = q0 + lane;
+          int held = 0, head = 0;
+          if (q < nrun) {
+            const int sl = s_run[q];
+            const int4 rc = s_rec[sl];
+            held = max(rc.w, rc.z);
+            head = (s_fl[sl] & F_FILLED) ? 1 : 0;
+          }
+          int xs = held, xh = head;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int ys = __shfl_up_sync(FM, xs, o), yh = __shfl_up_sync(FM, xh, o);
+            if (lane >= o) xs += ys, xh += yh;
+          }
+          const int PS = ps + xs, i = hs + xh;
+          // head i fails the token test (i > T, checked first: Q11) or the KV test (F + U0 - PS(p_i) < i)
+          const bool tfail = head && i > T, kfail = head && fM && F + (U0 - PS) < i;
+          const unsigned fb = __ballot_sync(FM, tfail || kfail);
+          if (fb) {
+            const int f0 = __ffs(fb) - 1;
+            pa1 = q0 + f0;
+            kvstop = __shfl_sync(FM, (int)tfail, f0) == 0;
+            a = __shfl_sync(FM, i, f0) - 1;
+            break;
+          }
+          ps = __shfl_sync(FM, PS, 31);
+          hs = __shfl_sync(FM, i, 31);
+        }
+      }
+      // the evicted suffix: the minimal [q*, nrun) with F + RS(q*) >= a, RS(q) = U0 - PS(q - 1) (lazy tail
+      // victims); if the KV stopped the walk at head a+1 (run position pa1) and it lies before q*, it evicts
+      // everything behind it and self-preempts (Q8): the suffix starts at pa1
+      int qs = nrun;
+      if (fM && F < a) {  // q* = 1 + max{j : PS(j) <= F + U0 - a} (PS strictly increasing, held >= 1; PS(-1) = 0)
+        const int X = F + U0 - a;
+        int cnt = 0, ps = 0;
+        for (int q0 = 0; q0 < nrun; q0 += 32) {
+          const int q = q0 + lane;
+          int held = 0;
+          if (q < nrun) {
+            const int4 rc = s_rec[s_run[q]];
+            held = max(rc.w, rc.z);
+          }
+          int xs = held;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int ys = __shfl_up_sync(FM, xs, o);
+            if (lane >= o) xs += ys;
+          }
+          const unsigned okm = __ballot_sync(FM, q < nrun && ps + xs <= X);
+          cnt += __popc(okm);
+          if (okm != FM) break;
+          ps = __shfl_sync(FM, ps + xs, 31);
+        }
+        qs = min(cnt, nrun);  // PS(q* - 1) <= X < PS(q*): q* = #{j : PS(j) <= X}
+      }
+      if (kvstop && pa1 < qs) qs = pa1;
+      // apply: evict run positions [qs, nrun) (refill semantics P:1570)
+      int fr = 0, evd = 0;
+      for (int q = qs + lane; q < nrun; q += 32) {
+        const int sl = s_run[q];
+        const int4 rc = s_rec[sl];
+        const uint8_t f = s_fl[sl];
+        fr += max(rc.w, rc.z);
+        evd += (f & F_FILLED) ? 1 : 0;
+        atomicAdd(&npre[sl], 1ull);
+        atomicAdd(&refill[sl], (unsigned long long)rc.z);
+        s_rec[sl] = make_int4(rc.x, rc.y, 0, 0);
+        s_fl[sl] = ST_WAIT | F_PRE | (f & F_FIRST);
+        s_vic[q - qs] = (int16_t)sl;
+      }
+      fr = (int)__reduce_add_sync(FM, (unsigned)fr);
+      evd = (int)__reduce_add_sync(FM, (unsigned)evd);
+      n_vic = nrun - qs;
+      n_rd -= evd;
+      cut = qs;
+      tok += a;
+      U += (kv1 ? a : 0) - fr;
+      if (a > 0 && bph < 0) bph = PH_DEC;
+      if (pa1 > qs) pa1 = qs;
+    };
+
+    if (pfirst) {  // vLLM {R_w, R_r}: every running request is a decode (no chunking)
+      if (nW > 0) warp_np(1, w0, Lw);
+      if (nrun > 0 && (hybrid || bph != PH_PRE)) decode_group();  // else every decode fails step 2
+      else pa1 = 0;
+    } else {  // Sarathi {R_r^d, R_r^p, R_w}
+      if (n_rd > 0) decode_group();
+      else pa1 = 0;
+      if (nrun - n_vic > n_rd) {  // running prefills survive: the first one's run position
+        for (int q0 = 0; q0 < cut; q0 += 32) {
+          const int q = q0 + lane;
+          const unsigned pm = __ballot_sync(FM, q < cut && !(s_fl[s_run[q]] & F_FILLED));
+          if (pm) {
+            rp_first = q0 + __ffs(pm) - 1;
+            break;
+          }
+        }
+        if (rp_first < cut) warp_np(2, rp_first, cut);
+      }
+      if (nW > 0) warp_np(1, w0, Lw);
+    }
+    if (wnext >= 0) wfirst = lo + wnext;
+    __syncwarp();
+
+    if (tok == 0) {  // B = {}: idle jump to the next arrival, not a step (Q21)
+      if (n_vic == 0 && nx1 < n) {
+        if (lane == 0) clk = fmax(clk, wl.T[nx1]);
+        idle++;
+        next = nx1;
+        continue;
+      }
+      exit_status = SIM_S_DEADLOCK;
+      break;
+    }
+
+    // ---- (3) a9 + a10: Process(B) and the exact integer features in one pass ----
+    // the batch: run positions [0, seg) (decodes before pa1, flagged running prefills), then the admissions
+    const int segA = pfirst ? pa1 : cut;
+    unsigned N = 0, np_ = 0, cp = 0, mp = 0, nd = 0, md = 0, freed = 0, ndone = 0, mdn = 0, nfa = 0, ndd = 0;
+    int minrem = 0x7fffffff, n_ev = 0;
+    bool moved = false;  // SRF: some retention key changed relative to the others (movers to merge back)
+    long long c2 = 0, mc = 0, pcm = 0, pce[SIM_MAX_COST] = {0, 0, 0, 0};
+    for (int e0 = 0; e0 < segA + n_new; e0 += 32) {
+      const int e = e0 + lane;
+      int sl = -1;
+      bool inb = false;
+      if (e < segA) {
+        sl = s_run[e];
+        const uint8_t f = s_fl[sl];
+        inb = (f & F_FILLED) ? e < pa1 : (f & F_INB_L) != 0;
+        // SRF: a running prefill left out of B but before pa1 is overtaken by the decodes after it (m + 1): it
+        // moves too (the block kernel re-sorts whenever nd != |R_r|)
+        if (srf && !inb && !(f & F_FILLED) && e < pa1) {
+          s_fl[sl] = f | F_MOVE_L;
+          moved = true;
+        }
+      } else if (e < segA + n_new) {
+        sl = s_new[e - segA];
+        inb = true;
+      }
+      unsigned evc = 0;
+      if (inb) {
+        uint8_t fl = s_fl[sl];
+        const int4 rc = s_rec[sl];
+        const bool dec = (fl & F_FILLED) != 0;
+        const int c = dec ? 1 : s_c[sl], O = s_O[sl];
+        const int m0 = rc.z, s = rc.x + rc.y, m = m0 + c;
+        int g = rc.y;
+        N += c;
+        if (!dec) {  // prefill entry (incl. refills and chunks)
+          np_++;
+          cp += c;
+          mp += m0;
+          c2 += (long long)c * c;
+          mc += (long long)m0 * c;
+          if (anyTheo) {
+            pcm += (long long)c * (c + m0);
+#pragma unroll
+            for (int k = 0; k < SIM_MAX_COST; k++)
+              if (k < K) pce[k] += (long long)((c + Hk[k] - 1) / Hk[k]) * (c + m0);
+          }
+        } else {  // decode entry (c = 1)
+          nd++;
+          md += m0;
+        }
+        fl &= ~F_INB_L;
+        bool done = false;
+        if (c == s - m0) {  // Eq. (6): all available tokens processed -> one token (Q18)
+          g++;
+          fl |= F_FILLED;
+          if (!(fl & F_FIRST)) fl |= F_FIRST, evc |= 1;
+          if (g == O) {
+            done = true;
+            fl = (fl & ~ST_MASK) | ST_DONE;
+            evc |= 2;
+            freed += max(rc.w, m);
+            ndone++;
+            ndd += dec ? 1 : 0;
+          } else if (!dec) {
+            nfa++;  // a (re)fill completed: a new running decode
+          }
+        }
+        if (!done) {
+          minrem = min(minrem, O - g);
+          mdn += m;
+          if (srf && !dec && e < segA) fl |= F_MOVE_L, moved = true;  // its key moved (admissions merge anyway)
+        }
+        s_rec[sl] = make_int4(rc.x, g, m, rc.w);
+        s_fl[sl] = fl;
+      }
+      const unsigned eb = __ballot_sync(FM, evc != 0);
+      if (evc) s_ev[n_ev + __popc(eb & lt)] = sl | (int)(evc << 16);
+      n_ev += __popc(eb);
+    }
+    N = __reduce_add_sync(FM, N), np_ = __reduce_add_sync(FM, np_), cp = __reduce_add_sync(FM, cp);
+    mp = __reduce_add_sync(FM, mp), nd = __reduce_add_sync(FM, nd), md = __reduce_add_sync(FM, md);
+    freed = __reduce_add_sync(FM, freed), ndone = __reduce_add_sync(FM, ndone), mdn = __reduce_add_sync(FM, mdn);
+    nfa = __reduce_add_sync(FM, nfa), ndd = __reduce_add_sync(FM, ndd);
+    moved = __any_sync(FM, moved);
+    minrem = (int)__reduce_min_sync(FM, (unsigned)minrem);
+    if (np_ > 0) {
+      c2 = warp_sum_ll(c2);
+      mc = warp_sum_ll(mc);
+      if (anyTheo) {
+        pcm = warp_sum_ll(pcm);
+#pragma unroll
+        for (int k = 0; k < SIM_MAX_COST; k++) pce[k] = warp_sum_ll(pce[k]);
+      }
+    }
+    // a9: lane k < K charges cost model k; clock += d_j (one fp64 add, Q36)
+    if (lane < K) {
+      Feat f;
+      f.N = N, f.np = np_, f.cp = cp, f.mp = mp, f.nd = nd, f.md = md, f.c2 = c2, f.mc = mc, f.pcm = pcm;
+      f.pceil[0] = lane == 0 ? pce[0] : (lane == 1 ? pce[1] : (lane == 2 ? pce[2] : pce[3]));  // this lane's model
+      f.pceil[1] = f.pceil[2] = f.pceil[3] = 0;
+      clk = dadd(clk, batch_time(H.cm[lane], f, 0));
+    }
+    steps++;
+    sumU += U;
+    entries += np_ + nd;
+    processed += N;
+    pentries += np_;
+    n_done += (int)ndone;
+    preempt += n_vic;
+    n_rd += (int)nfa - (int)ndd;
+    const int Uafter = U - (int)freed;
+    U = Uafter;
+
+    // event times (first token, completion) under every cost model
+    {
+      double c0 = __shfl_sync(FM, clk, 0), c1 = __shfl_sync(FM, clk, 1), c2_ = __shfl_sync(FM, clk, 2),
+             c3 = __shfl_sync(FM, clk, 3);
+      __syncwarp();
+      for (int e = lane; e < n_ev; e += 32) {
+        const int code = s_ev[e], sl = code & 0xffff;
+        double* dst[2] = {tf + sl, td + sl};
+#pragma unroll
+        for (int w = 0; w < 2; w++)
+          if (code & ((1 << w) << 16)) {
+            dst[w][0] = c0;
+            if (K > 1) dst[w][n] = c1;
+            if (K > 2) dst[w][2 * (long long)n] = c2_;
+            if (K > 3) dst[w][3 * (long long)n] = c3;
+          }
+      }
+    }
+    // this step's victims wait from the next step on: clear Q9's mark; R_w gains them (exact count; the smallest
+    // s stays a lower bound after admissions, recounted every 32 admission steps)
+    {
+      int vmin = 0x7fffffff, vidx = 0x7fffffff;
+      for (int v = lane; v < n_vic; v += 32) {
+        const int sl = s_vic[v];
+        s_fl[sl] &= ~F_PRE;
+        const int4 rc = s_rec[sl];
+        vmin = min(vmin, rc.x + rc.y);
+        vidx = min(vidx, sl);
+      }
+      vmin = (int)__reduce_min_sync(FM, (unsigned)vmin);
+      vidx = (int)__reduce_min_sync(FM, (unsigned)vidx);
+      wfirst = min(wfirst, vidx);
+      nW = nW - n_new + n_vic;
+      minSW = min(minSW, vmin);
+      if (n_new > 0) wstale++;
+      if (wstale >= 32) w_dirty = true;
+    }
+
+    // ---- (4) steady decode run: step j had only decodes and no admission, preemption or completion; step j+1
+    // repeats it exactly (waiting rejections persist: KV is monotone in U, tokens and phases unchanged) until a
+    // completion, the KV limit (U + k nd <= M) or an arrival.  After an eviction step the same holds when every
+    // running request was a decode of B and every waiting candidate fails the KV test already.
+    {
+      bool steady = ndone == 0 && np_ == 0 && nd > 0;
+      if (steady && n_vic > 0)
+        steady = (int)nd == nrun0 - n_vic && (nW == 0 || (finiteM && (long long)Uafter + minSW > M));
+      long long Lr = 0;
+      if (steady) {
+        Lr = minrem;
+        if (finiteM && kv1) Lr = min(Lr, (long long)(M - Uafter) / (long long)nd);
+        Lr = min(Lr, cfg.max_steps - steps);
+      }
+      if (Lr > 0) {
+        const long long ndl = nd, MD = mdn, Ur = Uafter, du = kv1 ? ndl : 0;  // KV growth per run step
+        constexpr int DB = 32;
+        long long E = 0;
+        while (E < Lr) {
+          const int chunk = (int)min((long long)DB, Lr - E);
+          // lane t: the batch times of run step E + t + 1 under every model (affine features)
+          if (lane < chunk) {
+            Feat f;
+            f.N = ndl, f.np = 0, f.c2 = 0, f.mc = 0, f.cp = 0, f.mp = 0, f.pcm = 0, f.nd = ndl;
+            f.md = MD + (E + lane) * ndl;
+            for (int k = 0; k < SIM_MAX_COST; k++) f.pceil[k] = 0;
+            for (int k = 0; k < K; k++) s_dbuf[k * DB + lane] = batch_time(H.cm[k], f, 0);
+          }
+          __syncwarp();
+          int ex = chunk;
+          if (lane < K) {  // the clock chain stays sequential: one fp64 add per step (Q36)
+            const double* db = s_dbuf + lane * DB;
+            if (nx1 < n) {  // online (K == 1): stop before a step that would start at/after an arrival (Q21)
+              for (int t = 0; t < chunk; t++) {
+                if (Tnext <= clk) {
+                  ex = t;
+                  break;
+                }
+                clk = dadd(clk, db[t]);
+              }
+            } else {
+              int t = 0;
+              for (; t + 8 <= chunk; t += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) v[u] = db[t + u];
+#pragma unroll
+                for (int u = 0; u < 8; u++) clk = dadd(clk, v[u]);
+              }
+              for (; t < chunk; t++) clk = dadd(clk, db[t]);
+            }
+          }
+          ex = __shfl_sync(FM, ex, 0);
+          __syncwarp();
+          E += ex;
+          if (ex < chunk) break;
+        }
+        if (E > 0) {  // every batch entry of the steady step is a decode: the run positions [0, pa1)
+          const double c0 = __shfl_sync(FM, clk, 0), c1 = __shfl_sync(FM, clk, 1), c2_ = __shfl_sync(FM, clk, 2),
+                       c3 = __shfl_sync(FM, clk, 3);
+          int fr2 = 0, nd2 = 0;
+          for (int q = lane; q < pa1; q += 32) {
+            const int sl = s_run[q];
+            if (!(s_fl[sl] & F_FILLED)) continue;  // (decode-first: a running prefill left out of the batch)
+            const int4 rc = s_rec[sl];
+            const int m = rc.z + (int)E, g = rc.y + (int)E, O = s_O[sl];
+            s_rec[sl] = make_int4(rc.x, g, m, rc.w);
+            if (g == O) {  // completes at the last run step
+              s_fl[sl] = (s_fl[sl] & ~ST_MASK) | ST_DONE;
+              td[sl] = c0;
+              if (K > 1) td[n + sl] = c1;
+              if (K > 2) td[2 * (long long)n + sl] = c2_;
+              if (K > 3) td[3 * (long long)n + sl] = c3;
+              fr2 += max(rc.w, m);
+              nd2++;
+            }
+          }
+          fr2 = (int)__reduce_add_sync(FM, (unsigned)fr2);
+          nd2 = (int)__reduce_add_sync(FM, (unsigned)nd2);
+          steps += E;
+          sumU += E * Ur + du * (E * (E + 1) / 2);
+          entries += E * ndl;
+          processed += E * ndl;
+          visits += E * nP;
+          U = (int)(Ur + E * du) - fr2;
+          n_done += nd2;
+          n_rd -= nd2;
+          ndone += nd2;
+        }
+      }
+    }
+
+    // ---- (5) the run list for the next step (retention order) ----
+    {
+      int cnt = cut;  // the evicted suffix is cut off
+      int nmov = 0;   // SRF: this step's prefill entries that stay running (their keys moved), in s_vic
+      if (ndone > 0 || moved) {  // stable in-place compaction: drop completions (and take out the SRF movers)
+        int w = 0;
+        for (int q0 = 0; q0 < cnt; q0 += 32) {
+          const int q = q0 + lane;
+          int sl = 0;
+          uint8_t f = 0;
+          if (q < cnt) {
+            sl = s_run[q];
+            f = s_fl[sl];
+          }
+          const bool live = q < cnt && (f & ST_MASK) == ST_RUN;
+          const bool mov = live && (f & F_MOVE_L);
+          const unsigned km = __ballot_sync(FM, live && !mov), mm = __ballot_sync(FM, mov);
+          __syncwarp();
+          if (live && !mov) s_run[w + __popc(km & lt)] = (int16_t)sl;
+          if (mov) {
+            s_vic[nmov + __popc(mm & lt)] = (int16_t)sl;
+            s_fl[sl] = f & ~F_MOVE_L;
+          }
+          w += __popc(km);
+          nmov += __popc(mm);
+        }
+        cnt = w;
+      }
+      // this step's admissions that stay running: appended in admission order (NRF / PF retention = admission
+      // order, Q6, Q39), or SRF movers
+      for (int e0 = 0; e0 < n_new; e0 += 32) {
+        const int e = e0 + lane;
+        const int sl = e < n_new ? s_new[e] : 0;
+        const bool live = e < n_new && (s_fl[sl] & ST_MASK) == ST_RUN;
+        const unsigned km = __ballot_sync(FM, live);
+        if (live) {
+          if (srf)
+            s_vic[nmov + __popc(km & lt)] = (int16_t)sl;
+          else
+            s_run[cnt + __popc(km & lt)] = (int16_t)sl;
+        }
+        if (srf)
+          nmov += __popc(km);
+        else
+          cnt += __popc(km);
+      }
+      __syncwarp();
+      if (nmov > 0) {  // SRF: merge the movers back into the (still sorted) kept list by (m desc, seq)
+        const int nk = cnt;
+        bool appended = false;
+        if (nmov <= 32) {
+          unsigned long long mk = ~0ull;
+          if (lane < nmov) {
+            const int sl = s_vic[lane];
+            mk = srf_key<SLB>(s_rec[sl].z, s_seq[sl], sl);
+          }
+          // bitonic sort of the (<= 32) mover keys across the warp
+#pragma unroll
+          for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+#pragma unroll
+            for (int j = k2 >> 1; j > 0; j >>= 1) {
+              const unsigned long long o = __shfl_xor_sync(FM, mk, j);
+              const bool up = (lane & k2) == 0, lower = (lane & j) == 0;
+              mk = (lower == up) ? (mk < o ? mk : o) : (mk > o ? mk : o);
+            }
+          }
+          unsigned long long tail = 0;
+          if (nk > 0) {
+            const int sl = s_run[nk - 1];
+            tail = srf_key<SLB>(s_rec[sl].z, s_seq[sl], sl);
+          }
+          const unsigned long long mk0 = __shfl_sync(FM, mk, 0);
+          if (nk == 0 || mk0 > tail) {  // every mover goes after the kept tail: append in key order
+            if (lane < nmov) s_run[nk + lane] = (int16_t)(mk & (CAP - 1));
+            appended = true;
+          } else {  // ins_t = #{kept j : key_j < key_t} by binary search, then shift the kept entries
+            int ins = nk;
+            if (lane < nmov) {
+              int lo2 = 0, hi2 = nk;
+              while (lo2 < hi2) {
+                const int mid = (lo2 + hi2) >> 1;
+                const int sl = s_run[mid];
+                if (srf_key<SLB>(s_rec[sl].z, s_seq[sl], sl) < mk)
+                  lo2 = mid + 1;
+                else
+                  hi2 = mid;
+              }
+              ins = lo2;
+            }
+            for (int q0 = 0; q0 < nk; q0 += 32) {
+              const int q = q0 + lane;
+              int sh = 0;
+              for (int t = 0; t < nmov; t++) sh += __shfl_sync(FM, ins, t) <= q ? 1 : 0;
+              if (q < nk) s_run2[q + sh] = s_run[q];
+            }
+            if (lane < nmov) s_run2[ins + lane] = (int16_t)(mk & (CAP - 1));
+            __syncwarp();
+            int16_t* t = s_run;
+            s_run = s_run2;
+            s_run2 = t;
+            appended = true;
+          }
+        }
+        if (!appended) {  // many movers (e.g. a large first admission): sort the whole list by key (bitonic)
+          const int tot = nk + nmov;
+          for (int q = lane; q < nk; q += 32) {
+            const int sl = s_run[q];
+            s_key[q] = srf_key<SLB>(s_rec[sl].z, s_seq[sl], sl);
+          }
+          for (int t = lane; t < nmov; t += 32) {
+            const int sl = s_vic[t];
+            s_key[nk + t] = srf_key<SLB>(s_rec[sl].z, s_seq[sl], sl);
+          }
+          int P2 = 1;
+          while (P2 < tot) P2 <<= 1;
+          for (int q = tot + lane; q < P2; q += 32) s_key[q] = ~0ull;
+          __syncwarp();
+          for (int k2 = 2; k2 <= P2; k2 <<= 1) {
+            for (int j = k2 >> 1; j > 0; j >>= 1) {
+              for (int i = lane; i < P2; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                  const unsigned long long x = s_key[i], y = s_key[ixj];
+                  if ((x > y) == ((i & k2) == 0)) s_key[i] = y, s_key[ixj] = x;
+                }
+              }
+              __syncwarp();
+            }
+          }
+          for (int q = lane; q < tot; q += 32) s_run[q] = (int16_t)(s_key[q] & (CAP - 1));
+        }
+        cnt = nk + nmov;
+      }
+      nrun = cnt;
+      next = nx1;
+      // the oldest unfinished request bounds the window
+      while (lo < nx1) {
+        const int q = lo + lane;
+        const unsigned dm = __ballot_sync(FM, q < nx1 && (s_fl[q] & ST_MASK) == ST_DONE);
+        const int run_len = __ffs(~dm) - 1;  // done prefix of this chunk
+        if (dm == FM) {
+          lo += 32;
+        } else {
+          lo += run_len;
+          break;
+        }
+      }
+      lo = min(lo, nx1);
+      __syncwarp();
+    }
+  }
+
+  // ---- a11: metrics ----
+  const int st = exit_status == -1 ? SIM_S_OK : exit_status;
+  __syncwarp();
+  if (st != SIM_S_OK) {  // failed simulations: zero-filled rows
+    for (int i = lane; i < n; i += 32) npre[i] = 0, refill[i] = 0;
+    for (int x = lane; x < K * n; x += 32) tf[x] = 0.0, td[x] = 0.0;
+    if (lane == 0) {
+      sim_result_t r;
+      memset(&r, 0, sizeof(r));
+      r.status = st;
+      p.results[ci] = r;
+    }
+    return;
+  }
+  __syncwarp();
+  if (lane < K) {  // sequential sums in request order (identical to the oracle)
+    const int k = lane;
+    double mx = 0.0, sl = 0.0, st1 = 0.0, stp = 0.0;
+    long long ntp = 0;
+    const double* tfk = tf + (long long)k * n;
+    const double* tdk = td + (long long)k * n;
+    for (int i = 0; i < n; i++) {
+      const double a = tfk[i], b = tdk[i], T = wl.T[i];
+      if (i == 0 || b > mx) mx = b;
+      sl = dadd(sl, b - T);
+      st1 = dadd(st1, a - T);
+      if (wl.O[i] > 1) {
+        stp = dadd(stp, ddiv(b - a, i2d(wl.O[i] - 1)));
+        ntp++;
+      }
+    }
+    sim_result_t& r = p.results[ci];
+    r.makespan[k] = mx - wl.T[0];
+    r.mean_latency[k] = ddiv(sl, i2d(n));
+    r.mean_ttft[k] = ddiv(st1, i2d(n));
+    r.mean_tpot[k] = ntp > 0 ? ddiv(stp, i2d(ntp)) : 0.0;
+  }
+  if (lane == 0) {
+    sim_result_t& r = p.results[ci];
+    r.status = SIM_S_OK;
+    r.pad = 0;
+    r.steps = steps;
+    r.preemptions = preempt;
+    r.batch_entries = entries;
+    r.processed_tokens = processed;
+    r.sum_U = sumU;
+    r.prefill_entries = pentries;
+    r.idle_jumps = idle;
+    r.visits = visits;
+    for (int k = K; k < SIM_MAX_COST; k++) r.makespan[k] = r.mean_latency[k] = r.mean_ttft[k] = r.mean_tpot[k] = 0.0;
+  }
+}
+
+}  // namespace simsweep

@@ -131,10 +131,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   Scal& S = *reinterpret_cast<Scal*>(smem);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int ci = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
-  if (variant_of(p.wls[p.cfgs[ci].workload].n) + (has_knobs(p.cfgs[ci]) ? N_SIZES : 0) != p.variant) return;
+  if (kernel_variant(p.cfgs[ci], p.wls[p.cfgs[ci].workload].n, p.lean) != p.variant) return;
   unsigned char* arr = smem + L::scal;
   if constexpr (GM) {  // claim a per-CTA arena of the workspace
-    if (tid == 0) S.arena = (int)atomicAdd(reinterpret_cast<unsigned*>(p.ws), 1u);
+    if (tid == 0) S.arena = p.arena_base + (int)atomicAdd(reinterpret_cast<unsigned*>(p.ws + p.ctr_off), 1u);
     __syncthreads();
     arr = p.ws + WS_HEADER + (size_t)S.arena * L::arr_bytes;
   }

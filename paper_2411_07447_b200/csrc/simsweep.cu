@@ -2,6 +2,7 @@
 // the C-ABI of include/simsweep.h.  See sim_kernel.cuh for the per-step plan.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -60,7 +61,19 @@ constexpr int32_t SIM_KNOB_TRACE_INTERNAL = 1 << 30;  // set by sim_run_traced o
 __host__ __device__ inline bool has_knobs(const sim_config_t& c) {
   return c.knobs || c.max_seqs || c.kv_watermark || c.kv_block > 1;
 }
-constexpr int N_VARIANTS = 2 * N_SIZES;
+constexpr int N_GENERAL = 2 * N_SIZES;
+// the lean one-warp kernel (sim_lean.cuh) for the configurations that dominate the north-star sweep: the vLLM /
+// Sarathi presets (prefill-first without chunking, or decode-first), NRF / SRF / PF, no knob, no SRF+Hist, no trace
+constexpr int V_LEAN = N_GENERAL;  // + 0: n <= 1024, + 1: n <= 4096 (state in shared memory)
+constexpr int N_VARIANTS = N_GENERAL + 2;
+__host__ __device__ inline bool lean_ok(const sim_config_t& c, int n) {
+  return !has_knobs(c) && c.replacement != SIM_SRF_HIST && n <= 4096 &&
+         ((c.order == SIM_ORDER_PREFILL_FIRST && !c.chunked) || c.order == SIM_ORDER_DECODE_FIRST);
+}
+__host__ __device__ inline int kernel_variant(const sim_config_t& c, int n, int lean) {
+  if (lean && lean_ok(c, n)) return V_LEAN + (n <= 1024 ? 0 : 1);
+  return variant_of(n) + (has_knobs(c) ? N_SIZES : 0);
+}
 
 #ifndef SIM_NT_SMALL
 #define SIM_NT_SMALL 256  // threads per CTA of the W <= 1024 variant
@@ -84,6 +97,7 @@ __device__ __forceinline__ long long block_sum_ll(long long v, Scal& S) {
 }  // namespace simsweep
 
 #include "sim_step.cuh"
+#include "sim_lean.cuh"
 #include "sim_analytics.cuh"
 #include "sim_optimum.cuh"
 
@@ -102,11 +116,22 @@ Variant make_variant() {
   using L = Smem<NT, CAP>;
   return Variant{NT, CAP, GM ? L::scal : L::bytes, GM ? L::arr_bytes : 0, sim_kernel<NT, CAP, IPT_, GM, KN>};
 }
+template <int CAP>
+Variant make_lean() {
+  return Variant{32, CAP, LLayout<CAP>::bytes, 0, sim_lean_kernel<CAP>};
+}
 
 static Variant g_variants[N_VARIANTS] = {
     make_variant<SIM_NT_SMALL, 1024, SIM_IPT_SMALL, false, false>(), make_variant<512, 4096, 4, false, false>(),
     make_variant<512, SIM_MAX_WINDOW, 4, true, false>(),           make_variant<SIM_NT_SMALL, 1024, SIM_IPT_SMALL, false, true>(),
-    make_variant<512, 4096, 4, false, true>(),                     make_variant<512, SIM_MAX_WINDOW, 4, true, true>()};
+    make_variant<512, 4096, 4, false, true>(),                     make_variant<512, SIM_MAX_WINDOW, 4, true, true>(),
+    make_lean<1024>(),                                             make_lean<4096>()};
+
+// SIMSWEEP_LEAN=0 in the environment routes every config to the block kernel (parity tests run both kernels)
+static int lean_enabled() {
+  const char* e = getenv("SIMSWEEP_LEAN");
+  return !(e && e[0] == '0');
+}
 
 static int64_t workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int32_t* wls_n) {
   int64_t big = 0;
@@ -116,6 +141,13 @@ static int64_t workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const i
 
 static int check_cuda(cudaError_t e) { return e == cudaSuccess ? 0 : SIM_ECUDA; }
 static unsigned g_attr_set[64];  // kernel attributes already set, per device and variant
+struct AuxStreams {              // per device: one stream per variant, a fork event and one join event each
+  bool ready = false;
+  cudaStream_t s[N_VARIANTS];
+  cudaEvent_t done[N_VARIANTS];
+  cudaEvent_t fork;
+};
+static AuxStreams g_aux[64];
 
 }  // namespace simsweep
 
@@ -176,7 +208,8 @@ int64_t sim_workspace_bytes(const sim_config_t* cfgs, int32_t n_cfgs, const int3
 
 // Every config field that can be checked without the workload contents (SIM_EINVAL / SIM_ECOST); wls_n[n_wls] is
 // the size of each workload.  Shared by sim_validate / sim_sweep (host copies) and sim_sweep_device.
-static int validate_configs(const sim_config_t* cfgs, int32_t n_cfgs, const int32_t* wls_n, int32_t n_wls, int32_t n_cms) {
+static int validate_configs(const sim_config_t* cfgs, int32_t n_cfgs, const int32_t* wls_n, int32_t n_wls, int32_t n_cms,
+                            int32_t internal_knobs = 0) {
   if (!cfgs || !wls_n || n_cfgs <= 0 || n_wls <= 0 || n_cms <= 0) return SIM_EINVAL;
   for (int w = 0; w < n_wls; w++)
     if (wls_n[w] <= 0) return SIM_EINVAL;
@@ -186,7 +219,7 @@ static int validate_configs(const sim_config_t* cfgs, int32_t n_cfgs, const int3
     if (c.replacement < SIM_NRF || c.replacement > SIM_PF) return SIM_EINVAL;
     if (c.reserve < SIM_RESERVE_SEQ || c.reserve > SIM_RESERVE_CONTEXT) return SIM_EINVAL;
     if ((c.replacement == SIM_PF) != (c.reserve != SIM_RESERVE_SEQ)) return SIM_EINVAL;  // Q39
-    if ((c.knobs & ~(SIM_KNOB_HOL | SIM_KNOB_NRF_ARRIVAL | SIM_KNOB_SRF_VISIT_ADMISSION)) || c.max_seqs < 0 ||
+    if ((c.knobs & ~(SIM_KNOB_HOL | SIM_KNOB_NRF_ARRIVAL | SIM_KNOB_SRF_VISIT_ADMISSION | internal_knobs)) || c.max_seqs < 0 ||
         c.kv_watermark < 0 || c.kv_watermark >= (1 << 30) || ((c.knobs & SIM_KNOB_NRF_ARRIVAL) && c.replacement != SIM_NRF) ||
         ((c.knobs & SIM_KNOB_SRF_VISIT_ADMISSION) && c.replacement != SIM_SRF && c.replacement != SIM_SRF_HIST) ||
         c.kv_block < 0 || c.kv_block > (1 << 16) || (c.kv_block > 1 && c.replacement == SIM_SRF_HIST))
@@ -209,10 +242,11 @@ static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_
   if (!h_cfgs || !h_wls_n || !d_cfgs || !d_wls || !d_cms || n_cfgs <= 0 || n_cms <= 0 || !d_row_off ||
       !d_tim_off || !d_results || !d_req.t_first || !d_req.t_done || !d_req.n_preempt || !d_req.refill_tokens)
     return SIM_EINVAL;
-  if (int rc = validate_configs(h_cfgs, n_cfgs, h_wls_n, n_wls, n_cms)) return rc;
-  bool need[N_VARIANTS] = {false, false, false, false, false, false};
-  for (int i = 0; i < n_cfgs; i++)
-    need[variant_of(h_wls_n[h_cfgs[i].workload]) + (has_knobs(h_cfgs[i]) ? N_SIZES : 0)] = true;
+  // (sim_run_traced's internal routing bit is set after its own validation, never by a caller)
+  if (int rc = validate_configs(h_cfgs, n_cfgs, h_wls_n, n_wls, n_cms, tr.steps ? SIM_KNOB_TRACE_INTERNAL : 0)) return rc;
+  const int lean = lean_enabled();
+  int cnt[N_VARIANTS] = {0};
+  for (int i = 0; i < n_cfgs; i++) cnt[kernel_variant(h_cfgs[i], h_wls_n[h_cfgs[i].workload], lean)]++;
   const int64_t wsb = workspace_bytes(h_cfgs, n_cfgs, h_wls_n);
   if (wsb > 0 && (!d_workspace || workspace_bytes_ < wsb)) return SIM_EINVAL;
   KParams kp;
@@ -227,16 +261,35 @@ static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_
   kp.req = d_req;
   kp.n_cfgs = n_cfgs;
   kp.tr = tr;
+  kp.lean = lean;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return SIM_ECUDA;
+  cudaStream_t main = (cudaStream_t)stream;
+  int nneed = 0;
+  for (int v = 0; v < N_VARIANTS; v++) nneed += cnt[v] > 0;
+  if (wsb > 0 && cudaMemsetAsync(d_workspace, 0, WS_HEADER, main) != cudaSuccess) return SIM_ECUDA;
+  // several variants run concurrently on forked streams (joined back into `stream` with events), so a sweep that
+  // mixes kernels is as long as its longest variant, not their sum
+  AuxStreams& ax = g_aux[dev];
+  if (nneed > 1) {
+    if (!ax.ready) {
+      for (int v = 0; v < N_VARIANTS; v++)
+        if (cudaStreamCreateWithFlags(&ax.s[v], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ax.done[v], cudaEventDisableTiming) != cudaSuccess)
+          return SIM_ECUDA;
+      if (cudaEventCreateWithFlags(&ax.fork, cudaEventDisableTiming) != cudaSuccess) return SIM_ECUDA;
+      ax.ready = true;
+    }
+    if (cudaEventRecord(ax.fork, main) != cudaSuccess) return SIM_ECUDA;
+  }
   int launches = 0;
   // the large-window variants first: their simulations are the longest
-  static const int launch_order[N_VARIANTS] = {2, 2 + N_SIZES, 1, 1 + N_SIZES, 0, N_SIZES};
+  static const int launch_order[N_VARIANTS] = {2, 2 + N_SIZES, V_LEAN + 1, 1, 1 + N_SIZES, V_LEAN, 0, N_SIZES};
   for (int vi = 0; vi < N_VARIANTS; vi++) {
     const int v = launch_order[vi];
-    if (!need[v]) continue;
+    if (!cnt[v]) continue;
     const Variant& V = g_variants[v];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !(g_attr_set[dev] >> v & 1)) {
+    if (!(g_attr_set[dev] >> v & 1)) {
       if (cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V.smem) !=
           cudaSuccess)
         return SIM_ECUDA;
@@ -245,11 +298,15 @@ static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_
       cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout, V.arena ? 10 : 100);
       g_attr_set[dev] |= 1u << v;
     }
-    if (V.arena && cudaMemsetAsync(d_workspace, 0, 4, (cudaStream_t)stream) != cudaSuccess) return SIM_ECUDA;
     kp.variant = v;
+    kp.arena_base = v == 2 + N_SIZES ? cnt[2] : 0;  // the two GM variants share the workspace: disjoint arenas
+    kp.ctr_off = v == 2 + N_SIZES ? 64 : 0;
+    cudaStream_t s = nneed > 1 ? ax.s[v] : main;
+    if (nneed > 1 && cudaStreamWaitEvent(s, ax.fork, 0) != cudaSuccess) return SIM_ECUDA;
     void* args[] = {&kp};
-    if (cudaLaunchKernel((const void*)V.fn, dim3(n_cfgs), dim3(V.nt), args, V.smem, (cudaStream_t)stream) !=
-        cudaSuccess)
+    if (cudaLaunchKernel((const void*)V.fn, dim3(n_cfgs), dim3(V.nt), args, V.smem, s) != cudaSuccess)
+      return SIM_ECUDA;
+    if (nneed > 1 && (cudaEventRecord(ax.done[v], s) != cudaSuccess || cudaStreamWaitEvent(main, ax.done[v], 0) != cudaSuccess))
       return SIM_ECUDA;
     launches++;
   }
