@@ -1,38 +1,45 @@
-// sim_lean.cuh -- the lean step kernel: ONE WARP per simulation (included by simsweep.cu).
+// sim_lean.cuh -- the lean step kernel: ONE WARP per simulation, decodes advanced lazily (included by simsweep.cu).
 //
 // The same method and readings as sim_step.cuh (Algorithm 1; Q1-Q40), for the
 // configurations that dominate the north-star sweep (lean_ok in simsweep.cu): the vLLM / Sarathi presets
 // (prefill-first without chunking, or decode-first), NRF / SRF / PF, no alternative-reading knob, no SRF+Hist,
 // no schedule trace, n <= CAP requests.  Everything a step decides (tok, U, seq, list lengths, counters) lives
 // in registers, uniform across the warp; lane k < K holds the clock of cost model k; per-request state is a
-// structure of arrays in shared memory.  A step is a few warp passes with no block barrier and no
-// shared-memory broadcast: the per-step latency IS the sweep's critical path.
+// structure of arrays in shared memory.
+//
+// Decode epochs.  Every running decode that is in a batch advances by exactly one token (c = 1, m += 1, g += 1,
+// Eq. (6)), and in almost every step either all surviving decodes are in B or none is.  So a running decode
+// stores its m and g relative to a decode epoch D (rec = {I, g - D, m - D, reserved}), and a step that admits the
+// decodes advances all of them with D += 1.  The decodes a step leaves out (only the token budget can, Q11) are
+// compensated (their offsets lowered by one).  The batch features of the decodes come from running sums
+// (n_d = the admitted heads, sum m = sum(m - D) + n_d D, Table 3), and the next completion is the smallest
+// completion epoch O - (g - D) over the running decodes.  A step therefore costs O(its events) -- the admitted
+// prefills, the evicted tail, completions -- not O(|R_r|).
 //
 // One step (one batch B_j):
 //   a2    arrivals: the next arrival time stays in a register; a ballot pass admits every T <= clock (Q21)
-//   a3-a8 GetNextBatch, the exact mechanisms of the block kernel on one warp:
-//         * the running decodes in closed form (decode group): head i (the i-th decode in retention order, at
-//           run position p_i) is admitted iff i <= C - tok and F + U0 - PS(p_i) >= i (F = M - U, U0 = the run
-//           list's holdings, PS = prefix sum of holdings over run positions <= p_i; monotone in i, so the walk
-//           stops at the first failing head); the minimal tail suffix [q*, n) with F + U0 - PS(q* - 1) >= a is
-//           evicted; if the KV stopped the walk, head a+1 evicts everything behind it and self-preempts
-//           (Q8)
+//   a3-a8 GetNextBatch:
+//         * the running decodes in closed form (decode group): head i (the i-th decode in retention order, at run
+//           position p_i) is admitted iff i <= C - tok and F + RS(p_i + 1) >= i (F = M - U, RS = the holdings
+//           behind p_i); the predicate is monotone in i, so a walk from the run list's TAIL finds the last
+//           admitted head a; the minimal tail suffix [q*, n) with F + RS(q*) >= a is evicted; if the KV stopped
+//           the walk, head a+1 evicts everything behind it and self-preempts (Q8)
 //         * the waiting group and the running prefills (they never preempt, Q5): 32 candidates per pass,
 //           ballot + prefix scan, the first cumulative failure dropped, a cropped chunk ends the group
-//   a9    exact integer features by warp reductions; lane k < K evaluates cost model k (no FMA, Q36)
-//   a10   Process: the batch is the run list's decodes before p_{a+1}, the flagged running prefills and this
-//         step's admissions -- nothing is copied into a batch list
-//   runs  steady decode runs are charged in closed form (features affine in the step index); the clock chain
-//         stays one sequential fp64 add per step (Q36)
+//   a9    exact integer features (prefill entries explicitly, decodes from the running sums); lane k < K
+//         evaluates cost model k (no FMA, Q36)
+//   a10   Process: the prefill entries explicitly, the decodes by D += 1; completions at their completion epoch
+//   runs  steady decode runs charged in closed form (features affine in the step index) up to the next completion
+//         epoch, the KV limit or an arrival; the clock chain stays one sequential fp64 add per step (Q36)
 //   a3'   the run list for the next step: the evicted suffix is cut, completions are compacted out, admissions
-//         are appended (NRF / PF: admission order) or, for SRF, this step's prefill entries (the only keys that
-//         moved) are merged back by (m desc, seq) (Q3, Q7)
+//         are appended (NRF / PF: admission order) or, for SRF, the entries whose keys moved are merged back by
+//         (m desc, seq) (Q3, Q7)
 #pragma once
 
 namespace simsweep {
 
 constexpr uint8_t F_INB_L = 8;    // a running prefill admitted into this step's batch
-constexpr uint8_t F_MOVE_L = 64;  // SRF: a prefill entry of this step's batch that stays running (its key moved)
+constexpr uint8_t F_MOVE_L = 64;  // SRF: an entry whose retention key moved relative to the others
 
 struct LHead {
   sim_cost_model_t cm[SIM_MAX_COST];
@@ -41,13 +48,13 @@ struct LHead {
 template <int CAP>
 struct LLayout {
   static constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
-  static constexpr size_t rec = a16(sizeof(LHead));  // int4 {I, g, m, reserved}
+  static constexpr size_t rec = a16(sizeof(LHead));  // int4 {I, g | g - D, m | m - D, reserved}
   static constexpr size_t O = rec + 16 * CAP;        // int32
   static constexpr size_t seq = O + 4 * CAP;         // int32 admission sequence number (Q6)
-  static constexpr size_t c = seq + 4 * CAP;         // int32 c of the running prefills of this batch  \ u64 sort keys
-  static constexpr size_t ev = c + 4 * CAP;          // int32 first-token / completion events          / (SRF merge)
+  static constexpr size_t c = seq + 4 * CAP;         // int32 c of this batch's prefill entries  \ u64 sort keys
+  static constexpr size_t ev = c + 4 * CAP;          // int32 first-token / completion events   / (SRF merge)
   static constexpr size_t run = ev + 4 * CAP;        // int16 run list (retention order)
-  static constexpr size_t run2 = run + 2 * CAP;      // int16 second run list (merge target)
+  static constexpr size_t run2 = run + 2 * CAP;      // int16 this batch's running prefills; the merge target
   static constexpr size_t nw = run2 + 2 * CAP;       // int16 admitted from R_w this step, in admission order
   static constexpr size_t vic = nw + 2 * CAP;        // int16 preempted this step, then the SRF movers
   static constexpr size_t fl = vic + 2 * CAP;        // uint8 status and flags
@@ -74,6 +81,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
   constexpr int SLB = __builtin_ctz(CAP);
   static_assert(SLB <= 12, "slot bits of the SRF key");
   constexpr long long SEQ_LIM = 0x7fffffffll - CAP;  // the int32 admission counter must not wrap
+  constexpr int BIG = 0x3fffffff;
   extern __shared__ __align__(16) unsigned char smem[];
   LHead& H = *reinterpret_cast<LHead*>(smem);
   const int lane = threadIdx.x;
@@ -85,7 +93,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
   int32_t* s_seq = reinterpret_cast<int32_t*>(smem + L::seq);
   int32_t* s_c = reinterpret_cast<int32_t*>(smem + L::c);
   int32_t* s_ev = reinterpret_cast<int32_t*>(smem + L::ev);
-  double* s_dbuf = reinterpret_cast<double*>(smem + L::ev);                    // steady run: CAP/2 batch times
+  double* s_dbuf = reinterpret_cast<double*>(smem + L::ev);                        // steady run: batch times
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem + L::c);  // SRF merge: CAP keys
   int16_t* s_run = reinterpret_cast<int16_t*>(smem + L::run);
   int16_t* s_run2 = reinterpret_cast<int16_t*>(smem + L::run2);
@@ -100,7 +108,8 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
   const int M = finiteM ? (int)cfg.M : 0, C = (int)cfg.C;  // host-validated <= 2^30
   const bool pfirst = cfg.order == SIM_ORDER_PREFILL_FIRST;  // {R_w, R_r} (never chunked here), else {R_r^d, R_r^p, R_w}
   const bool srf = cfg.replacement == SIM_SRF;
-  const int rmode = cfg.reserve;
+  const int rmode = cfg.reserve, Sctx = cfg.S;
+  const long long max_steps = cfg.max_steps;
   const bool kv1 = rmode == SIM_RESERVE_SEQ;  // a decode needs one KV (else its PEAK / CONTEXT reserve covers it, Q39)
   const long long row0 = p.row_off[ci], tim0 = p.tim_off[ci];
   double* tf = p.req.t_first + tim0;
@@ -116,10 +125,10 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     long long ub = 0;
     for (int i = lane; i < n; i += 32) {
       const long long pk = (long long)wl.I[i] + wl.O[i] - 1;  // peak KV usage
-      bad_long |= pk > cfg.S;
-      bad_fit |= (finiteM && pk > M) || (!chunked && pk > cfg.C);
-      bad_fit |= finiteM && rmode == SIM_RESERVE_CONTEXT && cfg.S > M;
-      if (!finiteM && pk <= cfg.S) ub += rmode == SIM_RESERVE_CONTEXT ? max(pk, (long long)cfg.S) : pk;
+      bad_long |= pk > Sctx;
+      bad_fit |= (finiteM && pk > M) || (!chunked && pk > C);
+      bad_fit |= finiteM && rmode == SIM_RESERVE_CONTEXT && Sctx > M;
+      if (!finiteM && pk <= Sctx) ub += rmode == SIM_RESERVE_CONTEXT ? max(pk, (long long)Sctx) : pk;
     }
     bad_long = __any_sync(FM, bad_long);
     bad_fit = __any_sync(FM, bad_fit);
@@ -134,7 +143,6 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       return;
     }
   }
-  if (lane < K) H.cm[lane] = p.cms[cfg.cost[lane]];
   bool anyTheo = false;
   int Hk[SIM_MAX_COST] = {1, 1, 1, 1};  // attention head dim per model (the ceil(c/H) feature, Eq. (2))
 #pragma unroll
@@ -143,16 +151,25 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       const sim_cost_model_t* cm = p.cms + cfg.cost[k];
       anyTheo |= cm->mode == 1;
       Hk[k] = cm->H;
+      if (lane == k) H.cm[k] = *cm;
     }
   __syncwarp();
 
   double clk = 0.0;  // lane k < K: the clock of cost model k
-  int U = 0, seq = 0, next = 0, lo = 0, n_done = 0, nrun = 0, n_rd = 0, nW = 0, minSW = 0x7fffffff, wfirst = 0;
+  int U = 0, seq = 0, next = 0, lo = 0, n_done = 0, nrun = 0, nW = 0, minSW = 0x7fffffff, wfirst = 0;
   int wstale = 0;
   bool w_dirty = true;
+  // decode epochs: a running decode holds rec.y = g - D, rec.z = m - D; n_rd of them, SMO = the sum of their m - D,
+  // Dmin = their smallest completion epoch O - (g - D) (BIG if none; exact unless dmin_dirty)
+  int D = 0, n_rd = 0, Dmin = BIG;
+  long long SMO = 0;
+  bool dmin_dirty = false;
   double Tnext = wl.T[0];  // arrival time of request `next`
   long long steps = 0, preempt = 0, entries = 0, processed = 0, sumU = 0, pentries = 0, idle = 0, visits = 0;
   int exit_status = 0;
+
+  auto is_dec = [&](uint8_t f) { return (f & (ST_MASK | F_FILLED)) == (ST_RUN | F_FILLED); };
+  auto m_of = [&](const int4& rc, uint8_t f) { return is_dec(f) ? rc.z + D : rc.z; };  // the current m of a slot
 
   for (;;) {
     // ---- (1) a2: GetNewRequests (Alg. 1 line 3): all T <= clock, inclusive (Q21) ----
@@ -181,7 +198,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       exit_status = -1;
       break;
     }
-    if (steps >= cfg.max_steps) {
+    if (steps >= max_steps) {
       exit_status = SIM_S_MAX_STEPS;
       break;
     }
@@ -206,22 +223,23 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       w_dirty = false;
       wstale = 0;
     }
-    const int nrun0 = nrun, U0 = U;  // U0: holdings of the run list (only running requests hold KVs)
+    const int nrun0 = nrun;
     const long long nP = (long long)nW + nrun;
     visits += nP;  // |P| (Alg. 1 line 9)
 
     // ---- (2) a3-a8: GetNextBatch (steps 2-4) ----
-    int tok = 0, n_new = 0, bph = -1, n_vic = 0;
-    int pa1 = 0;       // the decodes at run positions < pa1 are in B
-    int cut = nrun;    // run positions >= cut were evicted this step
-    int rp_first = nrun;  // no running prefill before this run position
+    int tok = 0, n_new = 0, n_pb = 0, bph = -1, n_vic = 0;
+    int a = 0;          // decodes admitted: the heads at run positions < pa1
+    int pa1 = 0;        // run position of head a+1 (or the end of the list)
+    int cut = nrun;     // run positions >= cut were evicted this step
     int wnext = -1;
     auto rnew = [&](const int4& rc, int sl) -> int {  // the reserve taken at (re)admission (Table 2, Q13, Q39)
-      return rmode == SIM_RESERVE_SEQ ? rc.x + rc.y : (rmode == SIM_RESERVE_PEAK ? rc.x + s_O[sl] - 1 : cfg.S);
+      return rmode == SIM_RESERVE_SEQ ? rc.x + rc.y : (rmode == SIM_RESERVE_PEAK ? rc.x + s_O[sl] - 1 : Sctx);
     };
 
     // Candidates that never preempt (Q5): the waiting group in index order (src 1: window offsets [b0, b1)) or the
-    // running prefills in retention order (src 2: run positions [b0, b1); their KV delta is 0 since reserved >= s).
+    // running prefills in retention order (src 2: run positions [b0, b1); their KV delta is 0 since reserved >= s;
+    // the admitted ones are listed in s_run2 for Process).
     auto warp_np = [&](int src, int b0, int b1) {
       const bool overWin = src == 1;
       const bool scand = overWin && !kv1;  // KV deltas differ from c under PEAK / CONTEXT: scan them too
@@ -286,6 +304,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
               s_new[n_new + ek] = (int16_t)sl;
             } else {
               s_fl[sl] |= F_INB_L;
+              s_run2[n_pb + ek] = (int16_t)sl;
             }
             alive = false;
             admitted = true;
@@ -305,6 +324,8 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
           if (overWin) {
             U += addd + crops;
             seq += nall, n_new += nall;
+          } else {
+            n_pb += nall;
           }
           if (nall > 0 && bph < 0) bph = PH_PRE;
           if (cropped) break;  // the token budget is exhausted: every later candidate is rejected
@@ -324,25 +345,44 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       }
     };
 
-    // The running decodes in closed form (see the file header).  Heads = the F_FILLED entries of the run list in
-    // retention order; the victim pool is the run list's tail (all running, none in B yet).
+    // the run position of the cnt-th decode (1-based) of the run list, or nrun
+    auto nth_head = [&](int cnt) -> int {
+      for (int q0 = 0; q0 < nrun; q0 += 32) {
+        const int q = q0 + lane;
+        const unsigned hb = __ballot_sync(FM, q < nrun && is_dec(s_fl[s_run[q < nrun ? q : 0]]));
+        const int h = __popc(hb);
+        if (h >= cnt) return q0 + (int)__fns(hb, 0, cnt);
+        cnt -= h;
+      }
+      return nrun;
+    };
+
+    // The running decodes in closed form (see the file header); the victim pool is the run list's tail.
     auto decode_group = [&]() {
       const bool fM = finiteM && kv1;  // heads need one KV each (else none: admitted up to the token budget)
-      const int F = fM ? M - U : 0x3fffffff;
+      const int F = fM ? M - U : BIG;
       const int T = C - tok;
-      int a = n_rd;                      // heads admitted
-      bool kvstop = false;               // the KV test (not the token budget) stopped the walk at pa1
-      pa1 = nrun;
-      if (F < n_rd || T < n_rd) {        // some head fails a test: walk the heads while they pass
-        int ps = 0, hs = 0;
-        for (int q0 = 0; q0 < nrun; q0 += 32) {
-          const int q = q0 + lane;
+      const int k = n_rd;
+      int qs = nrun;
+      if (F >= k && T >= k) {  // every head passes both tests: nothing is evicted
+        a = k, pa1 = nrun;
+      } else if (F >= k) {  // only the token budget binds (Q11: no preemption): heads 1..T
+        a = T;
+        pa1 = pfirst ? T : nth_head(T + 1);  // prefill-first: every running request is a decode
+      } else {
+        // walk from the tail: lane j <-> run position top - j; RSx = the holdings behind the chunk, HSi = its heads
+        // behind it; head i (i = k - #heads behind p_i) passes iff i <= T and F + RS(p_i + 1) >= i
+        int RSx = 0, HSi = 0, lastfail = nrun;
+        bool lastfail_t = false, found = false, kvstop = false;
+        a = 0;
+        for (int top = nrun - 1; top >= 0; top -= 32) {
+          const int q = top - lane;
           int held = 0, head = 0;
-          if (q < nrun) {
+          if (q >= 0) {
             const int sl = s_run[q];
             const int4 rc = s_rec[sl];
-            held = max(rc.w, rc.z);
-            head = (s_fl[sl] & F_FILLED) ? 1 : 0;
+            head = is_dec(s_fl[sl]) ? 1 : 0;
+            held = max(rc.w, head ? rc.z + D : rc.z);
           }
           int xs = held, xh = head;
 #pragma unroll
@@ -350,92 +390,112 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
             const int ys = __shfl_up_sync(FM, xs, o), yh = __shfl_up_sync(FM, xh, o);
             if (lane >= o) xs += ys, xh += yh;
           }
-          const int PS = ps + xs, i = hs + xh;
-          // head i fails the token test (i > T, checked first: Q11) or the KV test (F + U0 - PS(p_i) < i)
-          const bool tfail = head && i > T, kfail = head && fM && F + (U0 - PS) < i;
-          const unsigned fb = __ballot_sync(FM, tfail || kfail);
-          if (fb) {
-            const int f0 = __ffs(fb) - 1;
-            pa1 = q0 + f0;
-            kvstop = __shfl_sync(FM, (int)tfail, f0) == 0;
-            a = __shfl_sync(FM, i, f0) - 1;
+          const int rsx = RSx + xs - held, i = k - (HSi + xh) + 1;
+          const bool tfail = i > T, kfail = F + rsx < i;
+          const unsigned hb = __ballot_sync(FM, head);
+          const unsigned pb = __ballot_sync(FM, head && !tfail && !kfail);
+          if (pb) {  // the tail-most passing head is head a; head a+1 is the nearest failing head behind it
+            const int La = __ffs(pb) - 1;
+            a = __shfl_sync(FM, i, La);
+            const unsigned behind = hb & ((1u << La) - 1u);
+            if (behind) {
+              const int Lf = 31 - __clz(behind);
+              pa1 = top - Lf;
+              kvstop = __shfl_sync(FM, (int)tfail, Lf) == 0;
+            } else {
+              pa1 = lastfail;
+              kvstop = lastfail < nrun && !lastfail_t;
+            }
+            if (top == nrun - 1 && F < a) {  // q* from the same registers: the tail-most q with F + RS(q) >= a
+              const unsigned qb = __ballot_sync(FM, q >= 0 && F + RSx + xs >= a);
+              if (qb) qs = top - (__ffs(qb) - 1);
+            }
+            found = true;
             break;
           }
-          ps = __shfl_sync(FM, PS, 31);
-          hs = __shfl_sync(FM, i, 31);
-        }
-      }
-      // the evicted suffix: the minimal [q*, nrun) with F + RS(q*) >= a, RS(q) = U0 - PS(q - 1) (lazy tail
-      // victims); if the KV stopped the walk at head a+1 (run position pa1) and it lies before q*, it evicts
-      // everything behind it and self-preempts (Q8): the suffix starts at pa1
-      int qs = nrun;
-      if (fM && F < a) {  // q* = 1 + max{j : PS(j) <= F + U0 - a} (PS strictly increasing, held >= 1; PS(-1) = 0)
-        const int X = F + U0 - a;
-        int cnt = 0, ps = 0;
-        for (int q0 = 0; q0 < nrun; q0 += 32) {
-          const int q = q0 + lane;
-          int held = 0;
-          if (q < nrun) {
-            const int4 rc = s_rec[s_run[q]];
-            held = max(rc.w, rc.z);
+          if (hb) {  // every head of this chunk fails; its front-most one has the lowest rank so far
+            const int Lf = 31 - __clz(hb);
+            lastfail = top - Lf;
+            lastfail_t = __shfl_sync(FM, (int)tfail, Lf) != 0;
           }
-          int xs = held;
+          RSx += __shfl_sync(FM, xs, 31);
+          HSi += __shfl_sync(FM, xh, 31);
+        }
+        if (!found) {  // even head 1 fails
+          a = 0;
+          pa1 = lastfail;
+          kvstop = lastfail < nrun && !lastfail_t;
+        }
+        if (F < a && qs == nrun) {  // q* = the tail-most q with F + RS(q) >= a (walk the tail again)
+          int rs = 0;
+          for (int top = nrun - 1; top >= 0; top -= 32) {
+            const int q = top - lane;
+            int held = 0;
+            if (q >= 0) {
+              const int sl = s_run[q];
+              const int4 rc = s_rec[sl];
+              held = max(rc.w, is_dec(s_fl[sl]) ? rc.z + D : rc.z);
+            }
+            int xs = held;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int ys = __shfl_up_sync(FM, xs, o);
-            if (lane >= o) xs += ys;
+            for (int o = 1; o < 32; o <<= 1) {
+              const int ys = __shfl_up_sync(FM, xs, o);
+              if (lane >= o) xs += ys;
+            }
+            const unsigned qb = __ballot_sync(FM, q >= 0 && F + rs + xs >= a);
+            if (qb) {
+              qs = top - (__ffs(qb) - 1);
+              break;
+            }
+            rs += __shfl_sync(FM, xs, 31);
           }
-          const unsigned okm = __ballot_sync(FM, q < nrun && ps + xs <= X);
-          cnt += __popc(okm);
-          if (okm != FM) break;
-          ps = __shfl_sync(FM, ps + xs, 31);
         }
-        qs = min(cnt, nrun);  // PS(q* - 1) <= X < PS(q*): q* = #{j : PS(j) <= X}
+        // if the KV stopped the walk at head a+1 and it lies before q*, it evicts everything behind it and
+        // self-preempts (Q8): the suffix starts at pa1
+        if (kvstop && pa1 < qs) qs = pa1;
       }
-      if (kvstop && pa1 < qs) qs = pa1;
       // apply: evict run positions [qs, nrun) (refill semantics P:1570)
       int fr = 0, evd = 0;
+      long long smo_ev = 0;
+      bool hitmin = false;
       for (int q = qs + lane; q < nrun; q += 32) {
         const int sl = s_run[q];
         const int4 rc = s_rec[sl];
         const uint8_t f = s_fl[sl];
-        fr += max(rc.w, rc.z);
-        evd += (f & F_FILLED) ? 1 : 0;
+        const bool dec = is_dec(f);
+        const int m = dec ? rc.z + D : rc.z, g = dec ? rc.y + D : rc.y;
+        fr += max(rc.w, m);
+        if (dec) {
+          evd++;
+          smo_ev += rc.z;
+          hitmin |= s_O[sl] - rc.y == Dmin;
+        }
         atomicAdd(&npre[sl], 1ull);
-        atomicAdd(&refill[sl], (unsigned long long)rc.z);
-        s_rec[sl] = make_int4(rc.x, rc.y, 0, 0);
+        atomicAdd(&refill[sl], (unsigned long long)m);
+        s_rec[sl] = make_int4(rc.x, g, 0, 0);
         s_fl[sl] = ST_WAIT | F_PRE | (f & F_FIRST);
         s_vic[q - qs] = (int16_t)sl;
       }
       fr = (int)__reduce_add_sync(FM, (unsigned)fr);
       evd = (int)__reduce_add_sync(FM, (unsigned)evd);
+      smo_ev = warp_sum_ll(smo_ev);
+      dmin_dirty |= __any_sync(FM, hitmin);
       n_vic = nrun - qs;
       n_rd -= evd;
+      SMO -= smo_ev;
       cut = qs;
+      if (pa1 > qs) pa1 = qs;
       tok += a;
       U += (kv1 ? a : 0) - fr;
       if (a > 0 && bph < 0) bph = PH_DEC;
-      if (pa1 > qs) pa1 = qs;
     };
 
     if (pfirst) {  // vLLM {R_w, R_r}: every running request is a decode (no chunking)
       if (nW > 0) warp_np(1, w0, Lw);
-      if (nrun > 0 && (hybrid || bph != PH_PRE)) decode_group();  // else every decode fails step 2
-      else pa1 = 0;
+      if (n_rd > 0 && (hybrid || bph != PH_PRE)) decode_group();  // else every decode fails step 2
     } else {  // Sarathi {R_r^d, R_r^p, R_w}
       if (n_rd > 0) decode_group();
-      else pa1 = 0;
-      if (nrun - n_vic > n_rd) {  // running prefills survive: the first one's run position
-        for (int q0 = 0; q0 < cut; q0 += 32) {
-          const int q = q0 + lane;
-          const unsigned pm = __ballot_sync(FM, q < cut && !(s_fl[s_run[q]] & F_FILLED));
-          if (pm) {
-            rp_first = q0 + __ffs(pm) - 1;
-            break;
-          }
-        }
-        if (rp_first < cut) warp_np(2, rp_first, cut);
-      }
+      if (cut > n_rd) warp_np(2, 0, cut);  // running prefills survive (the run list holds cut entries)
       if (nW > 0) warp_np(1, w0, Lw);
     }
     if (wnext >= 0) wfirst = lo + wnext;
@@ -452,41 +512,58 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       break;
     }
 
-    // ---- (3) a9 + a10: Process(B) and the exact integer features in one pass ----
-    // the batch: run positions [0, seg) (decodes before pa1, flagged running prefills), then the admissions
-    const int segA = pfirst ? pa1 : cut;
-    unsigned N = 0, np_ = 0, cp = 0, mp = 0, nd = 0, md = 0, freed = 0, ndone = 0, mdn = 0, nfa = 0, ndd = 0;
-    int minrem = 0x7fffffff, n_ev = 0;
-    bool moved = false;  // SRF: some retention key changed relative to the others (movers to merge back)
-    long long c2 = 0, mc = 0, pcm = 0, pce[SIM_MAX_COST] = {0, 0, 0, 0};
-    for (int e0 = 0; e0 < segA + n_new; e0 += 32) {
-      const int e = e0 + lane;
-      int sl = -1;
-      bool inb = false;
-      if (e < segA) {
-        sl = s_run[e];
-        const uint8_t f = s_fl[sl];
-        inb = (f & F_FILLED) ? e < pa1 : (f & F_INB_L) != 0;
-        // SRF: a running prefill left out of B but before pa1 is overtaken by the decodes after it (m + 1): it
-        // moves too (the block kernel re-sorts whenever nd != |R_r|)
-        if (srf && !inb && !(f & F_FILLED) && e < pa1) {
-          s_fl[sl] = f | F_MOVE_L;
-          moved = true;
-        }
-      } else if (e < segA + n_new) {
-        sl = s_new[e - segA];
-        inb = true;
-      }
-      unsigned evc = 0;
-      if (inb) {
-        uint8_t fl = s_fl[sl];
+    // ---- (3) a9 + a10: the admitted decodes advance by one epoch; Process the prefill entries explicitly ----
+    // the decodes of B: the a heads before pa1, n_d = a, sum m = sum(m - D) + a D over them (Table 3 features)
+    long long smo_out = 0;  // sum of m - D over the decodes left out of B (positions [pa1, cut): token budget)
+    if (a > 0 && cut > pa1) {  // they do not advance: offsets lowered by one
+      long long so = 0;
+      for (int q = pa1 + lane; q < cut; q += 32) {
+        const int sl = s_run[q];
+        if (!is_dec(s_fl[sl])) continue;
         const int4 rc = s_rec[sl];
-        const bool dec = (fl & F_FILLED) != 0;
-        const int c = dec ? 1 : s_c[sl], O = s_O[sl];
-        const int m0 = rc.z, s = rc.x + rc.y, m = m0 + c;
-        int g = rc.y;
-        N += c;
-        if (!dec) {  // prefill entry (incl. refills and chunks)
+        so += rc.z;
+        s_rec[sl] = make_int4(rc.x, rc.y - 1, rc.z - 1, rc.w);
+      }
+      smo_out = warp_sum_ll(so);
+      dmin_dirty = true;
+    }
+    const int nd = a;
+    const long long md = a > 0 ? (SMO - smo_out) + (long long)a * D : 0;
+    if (a > 0) {
+      SMO -= n_rd - a;  // the left-out decodes' offsets were lowered by one
+      D++;
+    }
+    unsigned N = 0, np_ = 0, cp = 0, mp = 0, freed = 0, ndone = 0, nfa = 0;
+    int n_ev = 0, dm_new = BIG;
+    bool moved = false;  // SRF: some retention key changed relative to the others (movers to merge back)
+    long long c2 = 0, mc = 0, pcm = 0, pce[SIM_MAX_COST] = {0, 0, 0, 0}, smo_new = 0;
+    // SRF: a running prefill left out of B but before pa1 is overtaken by the decodes after it (m + 1): it moves
+    // too (the block kernel re-sorts whenever nd != |R_r|)
+    if (srf && !pfirst && a > 0 && pa1 > a) {
+      bool mv = false;
+      for (int q = lane; q < pa1; q += 32) {
+        const int sl = s_run[q];
+        const uint8_t f = s_fl[sl];
+        if ((f & (ST_MASK | F_FILLED | F_INB_L)) == ST_RUN) s_fl[sl] = f | F_MOVE_L, mv = true;
+      }
+      moved |= __any_sync(FM, mv);
+    }
+    // the prefill entries: this batch's running prefills (s_run2) and admissions (s_new)
+    for (int sg = 0; sg < 2; sg++) {
+      const int16_t* list = sg == 0 ? s_run2 : s_new;
+      const int len = sg == 0 ? n_pb : n_new;
+      for (int e0 = 0; e0 < len; e0 += 32) {
+        const int e = e0 + lane;
+        unsigned evc = 0;
+        int sl = 0;
+        if (e < len) {
+          sl = list[e];
+          uint8_t fl = s_fl[sl];
+          const int4 rc = s_rec[sl];
+          const int O = s_O[sl];
+          const int c = s_c[sl], m0 = rc.z, s = rc.x + rc.y, m = m0 + c;
+          int g = rc.y;
+          N += c;
           np_++;
           cp += c;
           mp += m0;
@@ -498,45 +575,41 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
             for (int k = 0; k < SIM_MAX_COST; k++)
               if (k < K) pce[k] += (long long)((c + Hk[k] - 1) / Hk[k]) * (c + m0);
           }
-        } else {  // decode entry (c = 1)
-          nd++;
-          md += m0;
-        }
-        fl &= ~F_INB_L;
-        bool done = false;
-        if (c == s - m0) {  // Eq. (6): all available tokens processed -> one token (Q18)
-          g++;
-          fl |= F_FILLED;
-          if (!(fl & F_FIRST)) fl |= F_FIRST, evc |= 1;
-          if (g == O) {
-            done = true;
-            fl = (fl & ~ST_MASK) | ST_DONE;
-            evc |= 2;
-            freed += max(rc.w, m);
-            ndone++;
-            ndd += dec ? 1 : 0;
-          } else if (!dec) {
-            nfa++;  // a (re)fill completed: a new running decode
+          fl &= ~F_INB_L;
+          int4 out = make_int4(rc.x, g, m, rc.w);
+          if (c == s - m0) {  // Eq. (6): all available tokens processed -> one token (Q18)
+            g++;
+            fl |= F_FILLED;
+            if (!(fl & F_FIRST)) fl |= F_FIRST, evc |= 1;
+            if (g == O) {
+              fl = (fl & ~ST_MASK) | ST_DONE;
+              evc |= 2;
+              freed += max(rc.w, m);
+              ndone++;
+              out = make_int4(rc.x, g, m, rc.w);
+            } else {  // the (re)fill completed: a running decode from now on, in epoch form
+              nfa++;
+              out = make_int4(rc.x, g - D, m - D, rc.w);
+              smo_new += m - D;
+              dm_new = min(dm_new, O - (g - D));
+              if (srf && sg == 0) fl |= F_MOVE_L, moved = true;
+            }
+          } else if (srf && sg == 0) {
+            fl |= F_MOVE_L, moved = true;  // a chunk: its key moved (the admissions are merged anyway)
           }
+          s_rec[sl] = out;
+          s_fl[sl] = fl;
         }
-        if (!done) {
-          minrem = min(minrem, O - g);
-          mdn += m;
-          if (srf && !dec && e < segA) fl |= F_MOVE_L, moved = true;  // its key moved (admissions merge anyway)
-        }
-        s_rec[sl] = make_int4(rc.x, g, m, rc.w);
-        s_fl[sl] = fl;
+        const unsigned eb = __ballot_sync(FM, evc != 0);
+        if (evc) s_ev[n_ev + __popc(eb & lt)] = sl | (int)(evc << 16);
+        n_ev += __popc(eb);
       }
-      const unsigned eb = __ballot_sync(FM, evc != 0);
-      if (evc) s_ev[n_ev + __popc(eb & lt)] = sl | (int)(evc << 16);
-      n_ev += __popc(eb);
     }
-    N = __reduce_add_sync(FM, N), np_ = __reduce_add_sync(FM, np_), cp = __reduce_add_sync(FM, cp);
-    mp = __reduce_add_sync(FM, mp), nd = __reduce_add_sync(FM, nd), md = __reduce_add_sync(FM, md);
-    freed = __reduce_add_sync(FM, freed), ndone = __reduce_add_sync(FM, ndone), mdn = __reduce_add_sync(FM, mdn);
-    nfa = __reduce_add_sync(FM, nfa), ndd = __reduce_add_sync(FM, ndd);
+    nfa = __reduce_add_sync(FM, nfa);
+    N = __reduce_add_sync(FM, N) + (unsigned)a;
+    np_ = __reduce_add_sync(FM, np_), cp = __reduce_add_sync(FM, cp), mp = __reduce_add_sync(FM, mp);
+    freed = __reduce_add_sync(FM, freed), ndone = __reduce_add_sync(FM, ndone);
     moved = __any_sync(FM, moved);
-    minrem = (int)__reduce_min_sync(FM, (unsigned)minrem);
     if (np_ > 0) {
       c2 = warp_sum_ll(c2);
       mc = warp_sum_ll(mc);
@@ -545,6 +618,51 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
 #pragma unroll
         for (int k = 0; k < SIM_MAX_COST; k++) pce[k] = warp_sum_ll(pce[k]);
       }
+    }
+    // decode completions: the admitted decodes reaching g = O at this epoch (completion epoch O - (g - D) == D);
+    // the new decodes of this step are not in the run list yet and complete later (their epoch > D)
+    if (a > 0 && (dmin_dirty || Dmin <= D)) {
+      int dm = BIG, nd2 = 0, fr2 = 0;
+      long long so = 0;
+      for (int q0 = 0; q0 < cut; q0 += 32) {
+        const int q = q0 + lane;
+        unsigned evc = 0;
+        int sl = 0;
+        if (q < cut) {
+          sl = s_run[q];
+          const uint8_t f = s_fl[sl];
+          if (is_dec(f) && !(f & F_INB_L)) {
+            const int4 rc = s_rec[sl];
+            const int O = s_O[sl], ce = O - rc.y;
+            if (ce == D) {
+              s_fl[sl] = (f & ~ST_MASK) | ST_DONE;
+              s_rec[sl] = make_int4(rc.x, O, rc.z + D, rc.w);
+              fr2 += max(rc.w, rc.z + D);
+              so += rc.z;
+              nd2++;
+              evc = 2;
+            } else {
+              dm = min(dm, ce);
+            }
+          }
+        }
+        const unsigned eb = __ballot_sync(FM, evc != 0);
+        if (evc) s_ev[n_ev + __popc(eb & lt)] = sl | (int)(evc << 16);
+        n_ev += __popc(eb);
+      }
+      const int ndd = (int)__reduce_add_sync(FM, (unsigned)nd2);
+      freed += (unsigned)__reduce_add_sync(FM, (unsigned)fr2);
+      SMO -= warp_sum_ll(so);
+      Dmin = (int)__reduce_min_sync(FM, (unsigned)dm);  // (the run-list prefills turned decodes are in it)
+      dmin_dirty = false;
+      n_rd -= ndd;
+      ndone += ndd;
+    }
+    // the new decodes join the epoch sums
+    if (nfa > 0) {
+      SMO += warp_sum_ll(smo_new);
+      Dmin = min(Dmin, (int)__reduce_min_sync(FM, (unsigned)dm_new));
+      n_rd += (int)nfa;
     }
     // a9: lane k < K charges cost model k; clock += d_j (one fp64 add, Q36)
     if (lane < K) {
@@ -561,14 +679,12 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     pentries += np_;
     n_done += (int)ndone;
     preempt += n_vic;
-    n_rd += (int)nfa - (int)ndd;
-    const int Uafter = U - (int)freed;
-    U = Uafter;
+    U -= (int)freed;
 
     // event times (first token, completion) under every cost model
     {
-      double c0 = __shfl_sync(FM, clk, 0), c1 = __shfl_sync(FM, clk, 1), c2_ = __shfl_sync(FM, clk, 2),
-             c3 = __shfl_sync(FM, clk, 3);
+      const double c0 = __shfl_sync(FM, clk, 0), c1 = __shfl_sync(FM, clk, 1), c2_ = __shfl_sync(FM, clk, 2),
+                   c3 = __shfl_sync(FM, clk, 3);
       __syncwarp();
       for (int e = lane; e < n_ev; e += 32) {
         const int code = s_ev[e], sl = code & 0xffff;
@@ -585,7 +701,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     }
     // this step's victims wait from the next step on: clear Q9's mark; R_w gains them (exact count; the smallest
     // s stays a lower bound after admissions, recounted every 32 admission steps)
-    {
+    if (n_vic > 0 || n_new > 0) {
       int vmin = 0x7fffffff, vidx = 0x7fffffff;
       for (int v = lane; v < n_vic; v += 32) {
         const int sl = s_vic[v];
@@ -604,21 +720,29 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     }
 
     // ---- (4) steady decode run: step j had only decodes and no admission, preemption or completion; step j+1
-    // repeats it exactly (waiting rejections persist: KV is monotone in U, tokens and phases unchanged) until a
-    // completion, the KV limit (U + k nd <= M) or an arrival.  After an eviction step the same holds when every
-    // running request was a decode of B and every waiting candidate fails the KV test already.
+    // repeats it exactly (waiting rejections persist: KV is monotone in U, tokens and phases unchanged) until the
+    // next completion epoch, the KV limit (U + k nd <= M) or an arrival.  After an eviction step the same holds
+    // when every running request was a decode of B and every waiting candidate fails the KV test already.
     {
       bool steady = ndone == 0 && np_ == 0 && nd > 0;
-      if (steady && n_vic > 0)
-        steady = (int)nd == nrun0 - n_vic && (nW == 0 || (finiteM && (long long)Uafter + minSW > M));
+      if (steady && n_vic > 0) steady = nd == nrun0 - n_vic && (nW == 0 || (finiteM && (long long)U + minSW > M));
       long long Lr = 0;
       if (steady) {
-        Lr = minrem;
-        if (finiteM && kv1) Lr = min(Lr, (long long)(M - Uafter) / (long long)nd);
-        Lr = min(Lr, cfg.max_steps - steps);
+        if (dmin_dirty) {  // (a left-out decode may have held the smallest completion epoch)
+          int dm = BIG;
+          for (int q = lane; q < cut; q += 32) {
+            const int sl = s_run[q];
+            if (is_dec(s_fl[sl])) dm = min(dm, s_O[sl] - s_rec[sl].y);
+          }
+          Dmin = (int)__reduce_min_sync(FM, (unsigned)dm);
+          dmin_dirty = false;
+        }
+        Lr = (long long)Dmin - D;  // steps until the next completion epoch (reached at the run's last step)
+        if (finiteM && kv1) Lr = min(Lr, (long long)(M - U) / (long long)nd);
+        Lr = min(Lr, max_steps - steps);
       }
       if (Lr > 0) {
-        const long long ndl = nd, MD = mdn, Ur = Uafter, du = kv1 ? ndl : 0;  // KV growth per run step
+        const long long ndl = nd, MD = md + ndl, Ur = U, du = kv1 ? ndl : 0;  // KV growth per run step
         constexpr int DB = 32;
         long long E = 0;
         while (E < Lr) {
@@ -660,37 +784,59 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
           E += ex;
           if (ex < chunk) break;
         }
-        if (E > 0) {  // every batch entry of the steady step is a decode: the run positions [0, pa1)
-          const double c0 = __shfl_sync(FM, clk, 0), c1 = __shfl_sync(FM, clk, 1), c2_ = __shfl_sync(FM, clk, 2),
-                       c3 = __shfl_sync(FM, clk, 3);
-          int fr2 = 0, nd2 = 0;
-          for (int q = lane; q < pa1; q += 32) {
-            const int sl = s_run[q];
-            if (!(s_fl[sl] & F_FILLED)) continue;  // (decode-first: a running prefill left out of the batch)
-            const int4 rc = s_rec[sl];
-            const int m = rc.z + (int)E, g = rc.y + (int)E, O = s_O[sl];
-            s_rec[sl] = make_int4(rc.x, g, m, rc.w);
-            if (g == O) {  // completes at the last run step
-              s_fl[sl] = (s_fl[sl] & ~ST_MASK) | ST_DONE;
-              td[sl] = c0;
-              if (K > 1) td[n + sl] = c1;
-              if (K > 2) td[2 * (long long)n + sl] = c2_;
-              if (K > 3) td[3 * (long long)n + sl] = c3;
-              fr2 += max(rc.w, m);
-              nd2++;
+        if (E > 0) {
+          const int nout = n_rd - nd;  // decodes left out of B (token budget) do not advance during the run
+          if (nout > 0) {
+            for (int q = pa1 + lane; q < cut; q += 32) {
+              const int sl = s_run[q];
+              if (!is_dec(s_fl[sl])) continue;
+              const int4 rc = s_rec[sl];
+              s_rec[sl] = make_int4(rc.x, rc.y - (int)E, rc.z - (int)E, rc.w);
             }
+            SMO -= (long long)nout * E;
+            dmin_dirty = true;
           }
-          fr2 = (int)__reduce_add_sync(FM, (unsigned)fr2);
-          nd2 = (int)__reduce_add_sync(FM, (unsigned)nd2);
+          D += (int)E;
           steps += E;
           sumU += E * Ur + du * (E * (E + 1) / 2);
           entries += E * ndl;
           processed += E * ndl;
           visits += E * nP;
-          U = (int)(Ur + E * du) - fr2;
-          n_done += nd2;
-          n_rd -= nd2;
-          ndone += nd2;
+          U = (int)(Ur + E * du);
+          if (Dmin <= D) {  // completions at the run's last step (their time: the clocks after the run)
+            const double c0 = __shfl_sync(FM, clk, 0), c1 = __shfl_sync(FM, clk, 1), c2_ = __shfl_sync(FM, clk, 2),
+                         c3 = __shfl_sync(FM, clk, 3);
+            int dm = BIG, nd2 = 0, fr2 = 0;
+            long long so = 0;
+            for (int q = lane; q < cut; q += 32) {
+              const int sl = s_run[q];
+              const uint8_t f = s_fl[sl];
+              if (!is_dec(f)) continue;
+              const int4 rc = s_rec[sl];
+              const int O = s_O[sl], ce = O - rc.y;
+              if (ce == D) {
+                s_fl[sl] = (f & ~ST_MASK) | ST_DONE;
+                s_rec[sl] = make_int4(rc.x, O, rc.z + D, rc.w);
+                fr2 += max(rc.w, rc.z + D);
+                so += rc.z;
+                nd2++;
+                td[sl] = c0;
+                if (K > 1) td[n + sl] = c1;
+                if (K > 2) td[2 * (long long)n + sl] = c2_;
+                if (K > 3) td[3 * (long long)n + sl] = c3;
+              } else {
+                dm = min(dm, ce);
+              }
+            }
+            nd2 = (int)__reduce_add_sync(FM, (unsigned)nd2);
+            U -= (int)__reduce_add_sync(FM, (unsigned)fr2);
+            SMO -= warp_sum_ll(so);
+            Dmin = (int)__reduce_min_sync(FM, (unsigned)dm);
+            dmin_dirty = false;
+            n_rd -= nd2;
+            n_done += nd2;
+            ndone += nd2;
+          }
         }
       }
     }
@@ -698,7 +844,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     // ---- (5) the run list for the next step (retention order) ----
     {
       int cnt = cut;  // the evicted suffix is cut off
-      int nmov = 0;   // SRF: this step's prefill entries that stay running (their keys moved), in s_vic
+      int nmov = 0;   // SRF: entries whose keys moved, taken out into s_vic
       if (ndone > 0 || moved) {  // stable in-place compaction: drop completions (and take out the SRF movers)
         int w = 0;
         for (int q0 = 0; q0 < cnt; q0 += 32) {
@@ -712,7 +858,6 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
           const bool live = q < cnt && (f & ST_MASK) == ST_RUN;
           const bool mov = live && (f & F_MOVE_L);
           const unsigned km = __ballot_sync(FM, live && !mov), mm = __ballot_sync(FM, mov);
-          __syncwarp();
           if (live && !mov) s_run[w + __popc(km & lt)] = (int16_t)sl;
           if (mov) {
             s_vic[nmov + __popc(mm & lt)] = (int16_t)sl;
@@ -744,40 +889,33 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       __syncwarp();
       if (nmov > 0) {  // SRF: merge the movers back into the (still sorted) kept list by (m desc, seq)
         const int nk = cnt;
-        bool appended = false;
+        auto key_of = [&](int sl) { return srf_key<SLB>(m_of(s_rec[sl], s_fl[sl]), s_seq[sl], sl); };
+        bool merged = false;
         if (nmov <= 32) {
           unsigned long long mk = ~0ull;
-          if (lane < nmov) {
-            const int sl = s_vic[lane];
-            mk = srf_key<SLB>(s_rec[sl].z, s_seq[sl], sl);
-          }
-          // bitonic sort of the (<= 32) mover keys across the warp
+          if (lane < nmov) mk = key_of(s_vic[lane]);
+          if (nmov > 1) {  // bitonic sort of the (<= 32) mover keys across the warp
 #pragma unroll
-          for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+            for (int k2 = 2; k2 <= 32; k2 <<= 1) {
 #pragma unroll
-            for (int j = k2 >> 1; j > 0; j >>= 1) {
-              const unsigned long long o = __shfl_xor_sync(FM, mk, j);
-              const bool up = (lane & k2) == 0, lower = (lane & j) == 0;
-              mk = (lower == up) ? (mk < o ? mk : o) : (mk > o ? mk : o);
+              for (int j = k2 >> 1; j > 0; j >>= 1) {
+                const unsigned long long o = __shfl_xor_sync(FM, mk, j);
+                const bool up = (lane & k2) == 0, lower = (lane & j) == 0;
+                mk = (lower == up) ? (mk < o ? mk : o) : (mk > o ? mk : o);
+              }
             }
           }
-          unsigned long long tail = 0;
-          if (nk > 0) {
-            const int sl = s_run[nk - 1];
-            tail = srf_key<SLB>(s_rec[sl].z, s_seq[sl], sl);
-          }
+          const unsigned long long tail = nk > 0 ? key_of(s_run[nk - 1]) : 0ull;
           const unsigned long long mk0 = __shfl_sync(FM, mk, 0);
           if (nk == 0 || mk0 > tail) {  // every mover goes after the kept tail: append in key order
             if (lane < nmov) s_run[nk + lane] = (int16_t)(mk & (CAP - 1));
-            appended = true;
           } else {  // ins_t = #{kept j : key_j < key_t} by binary search, then shift the kept entries
             int ins = nk;
             if (lane < nmov) {
               int lo2 = 0, hi2 = nk;
               while (lo2 < hi2) {
                 const int mid = (lo2 + hi2) >> 1;
-                const int sl = s_run[mid];
-                if (srf_key<SLB>(s_rec[sl].z, s_seq[sl], sl) < mk)
+                if (key_of(s_run[mid]) < mk)
                   lo2 = mid + 1;
                 else
                   hi2 = mid;
@@ -795,19 +933,13 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
             int16_t* t = s_run;
             s_run = s_run2;
             s_run2 = t;
-            appended = true;
           }
+          merged = true;
         }
-        if (!appended) {  // many movers (e.g. a large first admission): sort the whole list by key (bitonic)
+        if (!merged) {  // many movers (e.g. a large first admission): sort the whole list by key (bitonic)
           const int tot = nk + nmov;
-          for (int q = lane; q < nk; q += 32) {
-            const int sl = s_run[q];
-            s_key[q] = srf_key<SLB>(s_rec[sl].z, s_seq[sl], sl);
-          }
-          for (int t = lane; t < nmov; t += 32) {
-            const int sl = s_vic[t];
-            s_key[nk + t] = srf_key<SLB>(s_rec[sl].z, s_seq[sl], sl);
-          }
+          for (int q = lane; q < nk; q += 32) s_key[q] = key_of(s_run[q]);
+          for (int t = lane; t < nmov; t += 32) s_key[nk + t] = key_of(s_vic[t]);
           int P2 = 1;
           while (P2 < tot) P2 <<= 1;
           for (int q = tot + lane; q < P2; q += 32) s_key[q] = ~0ull;
@@ -834,11 +966,10 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       while (lo < nx1) {
         const int q = lo + lane;
         const unsigned dm = __ballot_sync(FM, q < nx1 && (s_fl[q] & ST_MASK) == ST_DONE);
-        const int run_len = __ffs(~dm) - 1;  // done prefix of this chunk
         if (dm == FM) {
           lo += 32;
         } else {
-          lo += run_len;
+          lo += __ffs(~dm) - 1;  // the done prefix of this chunk
           break;
         }
       }
@@ -861,7 +992,6 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     }
     return;
   }
-  __syncwarp();
   if (lane < K) {  // sequential sums in request order (identical to the oracle)
     const int k = lane;
     double mx = 0.0, sl = 0.0, st1 = 0.0, stp = 0.0;
