@@ -67,6 +67,13 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
   return v;
 }
 
+// warp sum of non-negative per-lane values below 2^51 in two REDUX: the low 24 bits and the rest apart
+__device__ __forceinline__ long long warp_sum_u51(unsigned long long v) {
+  const unsigned lo = __reduce_add_sync(0xffffffffu, (unsigned)(v & 0xffffffu));
+  const unsigned hi = __reduce_add_sync(0xffffffffu, (unsigned)(v >> 24));
+  return ((long long)hi << 24) + (long long)lo;
+}
+
 // SRF retention key (ascending = retained longer): m descending, then admission order (Q3, Q7); the slot rides in
 // the low bits so that sorting keys sorts slots
 template <int SLB>
@@ -156,14 +163,20 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
   __syncwarp();
 
   double clk = 0.0;  // lane k < K: the clock of cost model k
-  int U = 0, seq = 0, next = 0, lo = 0, n_done = 0, nrun = 0, nW = 0, minSW = 0x7fffffff, wfirst = 0;
-  int wstale = 0;
-  bool w_dirty = true;
+  int U = 0, seq = 0, next = 0, n_done = 0, nrun = 0, nW = 0;
+  // the waiting group R_w as a bitmap: word w (32 slots) belongs to lane w % 32, row w / 32; per word the smallest
+  // s and (PEAK reserve) the smallest initial reserve of its waiting requests (BIG if none) -- a chunk can hold an
+  // admissible candidate only if these pass the step's token and KV limits
+  constexpr int R = CAP / 1024;
+  unsigned wm[R];
+  int wmS[R], wmD[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) wm[r] = 0u, wmS[r] = BIG, wmD[r] = BIG;
   // decode epochs: a running decode holds rec.y = g - D, rec.z = m - D; n_rd of them, SMO = the sum of their m - D,
-  // Dmin = their smallest completion epoch O - (g - D) (BIG if none; exact unless dmin_dirty)
+  // Dmin = a lower bound of their smallest completion epoch O - (g - D) (exact after every completion scan;
+  // evictions and left-out decodes only raise the true minimum)
   int D = 0, n_rd = 0, Dmin = BIG;
   long long SMO = 0;
-  bool dmin_dirty = false;
   double Tnext = wl.T[0];  // arrival time of request `next`
   long long steps = 0, preempt = 0, entries = 0, processed = 0, sumU = 0, pentries = 0, idle = 0, visits = 0;
   int exit_status = 0;
@@ -189,10 +202,21 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         nx1 += __popc(b);
         if (b != FM) break;
       }
-      wfirst = min(wfirst, next);  // the new arrivals wait
-      w_dirty = true;
       if (nx1 < n) Tnext = wl.T[nx1];
       __syncwarp();
+      for (int w = next >> 5; w <= (nx1 - 1) >> 5; w++) {  // the new arrivals join R_w
+        const int sl = w * 32 + lane;
+        const bool in = sl >= next && sl < nx1;
+        const unsigned bits = __ballot_sync(FM, in);
+        const int ms = (int)__reduce_min_sync(FM, in ? (unsigned)s_rec[sl].x : (unsigned)BIG);
+        const int md_ = rmode == SIM_RESERVE_PEAK
+                            ? (int)__reduce_min_sync(FM, in ? (unsigned)(s_rec[sl].x + s_O[sl] - 1) : (unsigned)BIG)
+                            : BIG;
+#pragma unroll
+        for (int r = 0; r < R; r++)
+          if (r == (w >> 5) && lane == (w & 31)) wm[r] |= bits, wmS[r] = min(wmS[r], ms), wmD[r] = min(wmD[r], md_);
+      }
+      nW += nx1 - next;
     }
     if (n_done == n) {
       exit_status = -1;
@@ -206,23 +230,6 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       exit_status = SIM_S_CAPACITY;
       break;
     }
-    const int Lw = nx1 - lo;  // window offsets [0, Lw): slot = lo + offset (n <= CAP: no ring)
-    const int w0 = max(wfirst - lo, 0);
-    if (w_dirty) {  // |R_w| and its smallest s (the skip test), exact
-      int cnt = 0, mn = 0x7fffffff;
-      for (int q = w0 + lane; q < Lw; q += 32) {
-        const int sl = lo + q;
-        if ((s_fl[sl] & ST_MASK) == ST_WAIT) {
-          const int4 r = s_rec[sl];
-          cnt++;
-          mn = min(mn, r.x + r.y);
-        }
-      }
-      nW = (int)__reduce_add_sync(FM, (unsigned)cnt);
-      minSW = (int)__reduce_min_sync(FM, (unsigned)mn);
-      w_dirty = false;
-      wstale = 0;
-    }
     const int nrun0 = nrun;
     const long long nP = (long long)nW + nrun;
     visits += nP;  // |P| (Alg. 1 line 9)
@@ -232,116 +239,134 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     int a = 0;          // decodes admitted: the heads at run positions < pa1
     int pa1 = 0;        // run position of head a+1 (or the end of the list)
     int cut = nrun;     // run positions >= cut were evicted this step
-    int wnext = -1;
     auto rnew = [&](const int4& rc, int sl) -> int {  // the reserve taken at (re)admission (Table 2, Q13, Q39)
       return rmode == SIM_RESERVE_SEQ ? rc.x + rc.y : (rmode == SIM_RESERVE_PEAK ? rc.x + s_O[sl] - 1 : Sctx);
     };
 
-    // Candidates that never preempt (Q5): the waiting group in index order (src 1: window offsets [b0, b1)) or the
-    // running prefills in retention order (src 2: run positions [b0, b1); their KV delta is 0 since reserved >= s;
-    // the admitted ones are listed in s_run2 for Process).
-    auto warp_np = [&](int src, int b0, int b1) {
-      const bool overWin = src == 1;
-      const bool scand = overWin && !kv1;  // KV deltas differ from c under PEAK / CONTEXT: scan them too
-      bool wcont = overWin;                // every waiting request at offsets [b0, i0) was admitted
-      if (overWin) wnext = b0;
-      for (int i0 = b0; i0 < b1; i0 += 32) {
-        if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining candidate fails
-        if (overWin && ((finiteM && U + minSW > M) || (!chunked && minSW > C - tok))) return;
-        const int i = i0 + lane;
-        int sl = -1;
-        if (i < b1) {
-          const int s2 = overWin ? lo + i : s_run[i];
-          const uint8_t f2 = s_fl[s2];
-          if (overWin ? (f2 & (ST_MASK | F_PRE)) == ST_WAIT : (f2 & (ST_MASK | F_PRE | F_FILLED)) == ST_RUN) sl = s2;
-        }
-        if (!__any_sync(FM, sl >= 0)) {
-          if (wcont) wnext = min(i0 + 32, b1);
-          continue;
-        }
-        const int4 rc = s_rec[sl < 0 ? 0 : sl];
-        const int s = rc.x + rc.y, avail = s - rc.z;
-        const int dkv = overWin ? rnew(rc, sl < 0 ? 0 : sl) : 0;  // the initial reserve >= s >= c (Q13)
-        bool alive = sl >= 0, admitted = false;
-        for (;;) {
-          const int rt = C - tok;
-          const bool fit = alive && rt >= 1 && (chunked || avail <= rt) && (!finiteM || U + dkv <= M);
-          const unsigned fm = __ballot_sync(FM, fit);
-          if (!fm) break;
-          const int cc = fit ? avail : 0, dk = fit ? dkv : 0;
-          int xc = cc, xd = dk;
+    // Candidates that never preempt (Q5), 32 per pass: ballot the lanes that fit alone, prefix-scan their tokens
+    // (and KV deltas), admit those before the first cumulative failure, drop that failure, repeat; a cropped chunk
+    // (chunked prefill) exhausts the token budget.  One chunk: lanes with `alive` hold a candidate; waiting = R_w
+    // (its initial reserve dkv is the KV delta, Q13), else running prefills (KV delta 0: reserved >= s >= m + c).
+    // Returns the lanes admitted.
+    auto admit_chunk = [&](bool waiting, int sl, const int4& rc, int avail, int dkv, bool alive) -> unsigned {
+      const bool scand = waiting && !kv1;  // KV deltas differ from c under PEAK / CONTEXT: scan them too
+      bool admitted = false;
+      for (;;) {
+        const int rt = C - tok;
+        const bool fit = alive && rt >= 1 && (chunked || avail <= rt) && (!finiteM || U + dkv <= M);
+        const unsigned fm = __ballot_sync(FM, fit);
+        if (!fm) break;
+        const int cc = fit ? avail : 0, dk = fit ? dkv : 0;
+        int xc = cc, xd = dk;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int yc = __shfl_up_sync(FM, xc, o);
-            if (lane >= o) xc += yc;
-            if (scand) {
-              const int yd = __shfl_up_sync(FM, xd, o);
-              if (lane >= o) xd += yd;
-            }
-          }
-          const int ec = xc - cc, ek = __popc(fm & lt);
-          const int ed = overWin ? (scand ? xd - dk : ec) : 0;  // SEQ: a waiting admission reserves exactly c = s
-          bool brk = false, crop = false;
-          if (fit) {
-            const int prt = rt - ec;
-            if (chunked)
-              crop = prt < avail;  // cropped (c = prt >= 1) or exhausted (prt <= 0)
-            else
-              brk = avail > prt;
-            if (finiteM) brk |= U + ed + dkv > M;
-            if (crop && prt <= 0) brk = true;
-          }
-          const unsigned bm = __ballot_sync(FM, brk), cm = __ballot_sync(FM, crop && !brk);
-          const int b = bm ? __ffs(bm) - 1 : 32, cl = cm ? __ffs(cm) - 1 : 32;
-          const int stop = min(b, cl);
-          const bool adm = fit && lane < stop, adc = fit && lane == cl && cl < b;
-          if (adm || adc) {
-            s_c[sl] = adm ? avail : rt - ec;
-            if (overWin) {
-              s_seq[sl] = seq + ek + 1;
-              s_rec[sl] = make_int4(rc.x, rc.y, 0, dkv);
-              s_fl[sl] = ST_RUN | (s_fl[sl] & F_FIRST);
-              s_new[n_new + ek] = (int16_t)sl;
-            } else {
-              s_fl[sl] |= F_INB_L;
-              s_run2[n_pb + ek] = (int16_t)sl;
-            }
-            alive = false;
-            admitted = true;
-          }
-          const bool cropped = cl < b && cl < 32;
-          const int nadm = __popc(fm & (stop >= 32 ? FM : ((1u << stop) - 1u)));
-          const int lastl = stop > 0 ? min(stop, 32) - 1 : 0;
-          const int addc = stop > 0 ? __shfl_sync(FM, xc, lastl) : 0;
-          const int addd = (scand && stop > 0) ? __shfl_sync(FM, xd, lastl) : addc;
-          int cropc = 0, crops = 0;
-          if (cropped) {
-            cropc = __shfl_sync(FM, rt - ec, cl);
-            crops = __shfl_sync(FM, dkv, cl);
-          }
-          const int nall = nadm + (cropped ? 1 : 0);
-          tok += addc + cropc;
-          if (overWin) {
-            U += addd + crops;
-            seq += nall, n_new += nall;
-          } else {
-            n_pb += nall;
-          }
-          if (nall > 0 && bph < 0) bph = PH_PRE;
-          if (cropped) break;  // the token budget is exhausted: every later candidate is rejected
-          if (b < 32 && lane == b) alive = false;  // rejected (no state change)
-          if (b >= 32) break;
-        }
-        if (wcont) {  // advance the waiting bound past this chunk unless a waiting request is left in it
-          const unsigned lf = __ballot_sync(FM, sl >= 0 && !admitted);
-          if (lf) {
-            wnext = i0 + __ffs(lf) - 1;
-            wcont = false;
-          } else {
-            wnext = min(i0 + 32, b1);
+        for (int o = 1; o < 32; o <<= 1) {
+          const int yc = __shfl_up_sync(FM, xc, o);
+          if (lane >= o) xc += yc;
+          if (scand) {
+            const int yd = __shfl_up_sync(FM, xd, o);
+            if (lane >= o) xd += yd;
           }
         }
-        if (chunked && tok >= C) return;
+        const int ec = xc - cc, ek = __popc(fm & lt);
+        const int ed = waiting ? (scand ? xd - dk : ec) : 0;  // SEQ: a waiting admission reserves exactly c = s
+        bool brk = false, crop = false;
+        if (fit) {
+          const int prt = rt - ec;
+          if (chunked)
+            crop = prt < avail;  // cropped (c = prt >= 1) or exhausted (prt <= 0)
+          else
+            brk = avail > prt;
+          if (finiteM) brk |= U + ed + dkv > M;
+          if (crop && prt <= 0) brk = true;
+        }
+        const unsigned bm = __ballot_sync(FM, brk), cm = __ballot_sync(FM, crop && !brk);
+        const int b = bm ? __ffs(bm) - 1 : 32, cl = cm ? __ffs(cm) - 1 : 32;
+        const int stop = min(b, cl);
+        const bool adm = fit && lane < stop, adc = fit && lane == cl && cl < b;
+        if (adm || adc) {
+          s_c[sl] = adm ? avail : rt - ec;
+          if (waiting) {
+            s_seq[sl] = seq + ek + 1;
+            s_rec[sl] = make_int4(rc.x, rc.y, 0, dkv);
+            s_fl[sl] = ST_RUN | (s_fl[sl] & F_FIRST);
+            s_new[n_new + ek] = (int16_t)sl;
+          } else {
+            s_fl[sl] |= F_INB_L;
+            s_run2[n_pb + ek] = (int16_t)sl;
+          }
+          alive = false;
+          admitted = true;
+        }
+        const bool cropped = cl < b && cl < 32;
+        const int nadm = __popc(fm & (stop >= 32 ? FM : ((1u << stop) - 1u)));
+        const int lastl = stop > 0 ? min(stop, 32) - 1 : 0;
+        const int addc = stop > 0 ? __shfl_sync(FM, xc, lastl) : 0;
+        const int addd = (scand && stop > 0) ? __shfl_sync(FM, xd, lastl) : addc;
+        int cropc = 0, crops = 0;
+        if (cropped) {
+          cropc = __shfl_sync(FM, rt - ec, cl);
+          crops = __shfl_sync(FM, dkv, cl);
+        }
+        const int nall = nadm + (cropped ? 1 : 0);
+        tok += addc + cropc;
+        if (waiting) {
+          U += addd + crops;
+          seq += nall, n_new += nall;
+        } else {
+          n_pb += nall;
+        }
+        if (nall > 0 && bph < 0) bph = PH_PRE;
+        if (cropped) break;  // the token budget is exhausted: every later candidate is rejected
+        if (b < 32 && lane == b) alive = false;  // rejected (no state change)
+        if (b >= 32) break;
+      }
+      return __ballot_sync(FM, admitted);
+    };
+
+    // the running prefills at run positions [0, b1), in retention order (decode-first: R_r^p)
+    auto run_prefills = [&](int b1) {
+      for (int i0 = 0; i0 < b1; i0 += 32) {
+        if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining candidate fails
+        const int i = i0 + lane;
+        int sl = 0;
+        bool cand = false;
+        if (i < b1) {
+          sl = s_run[i];
+          cand = (s_fl[sl] & (ST_MASK | F_PRE | F_FILLED)) == ST_RUN;
+        }
+        if (!__any_sync(FM, cand)) continue;
+        const int4 rc = cand ? s_rec[sl] : make_int4(0, 0, 0, 0);
+        admit_chunk(false, sl, rc, rc.x + rc.y - rc.z, 0, cand);
+      }
+    };
+
+    // R_w in index order (Q1, Q2): only the bitmap words whose smallest s / reserve pass the current token and KV
+    // limits can hold an admissible candidate (rejections change no state, so the others are skipped whole)
+    auto wait_scan = [&]() {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        int cur = 0;
+        for (;;) {
+          if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining candidate fails
+          const int capT = chunked ? BIG : C - tok, capM = finiteM ? M - U : BIG;
+          const bool kvok = rmode == SIM_RESERVE_SEQ ? wmS[r] <= capM
+                                                     : (rmode == SIM_RESERVE_PEAK ? wmD[r] <= capM : Sctx <= capM);
+          const unsigned cb = __ballot_sync(FM, lane >= cur && wm[r] != 0u && wmS[r] <= capT && kvok);
+          if (!cb) break;
+          const int Lc = __ffs(cb) - 1;
+          cur = Lc + 1;
+          const unsigned word = __shfl_sync(FM, wm[r], Lc);
+          const int sl = (r * 32 + Lc) * 32 + lane;
+          const bool isw = (word >> lane) & 1u;
+          const int4 rc = isw ? s_rec[sl] : make_int4(0, 0, 0, 0);
+          const int sw = rc.x + rc.y, dkv = isw ? rnew(rc, sl) : 0;  // avail = s (m = 0)
+          const unsigned admm = admit_chunk(true, sl, rc, sw, dkv, isw);
+          const unsigned left = word & ~admm;
+          const bool lw = (left >> lane) & 1u;
+          const int ms = (int)__reduce_min_sync(FM, lw ? (unsigned)sw : (unsigned)BIG);
+          const int md_ = rmode == SIM_RESERVE_PEAK ? (int)__reduce_min_sync(FM, lw ? (unsigned)dkv : (unsigned)BIG) : BIG;
+          if (lane == Lc) wm[r] = left, wmS[r] = ms, wmD[r] = md_;
+        }
       }
     };
 
@@ -456,8 +481,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       }
       // apply: evict run positions [qs, nrun) (refill semantics P:1570)
       int fr = 0, evd = 0;
-      long long smo_ev = 0;
-      bool hitmin = false;
+      unsigned mev = 0;  // sum of the evicted decodes' m
       for (int q = qs + lane; q < nrun; q += 32) {
         const int sl = s_run[q];
         const int4 rc = s_rec[sl];
@@ -467,8 +491,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         fr += max(rc.w, m);
         if (dec) {
           evd++;
-          smo_ev += rc.z;
-          hitmin |= s_O[sl] - rc.y == Dmin;
+          mev += m;
         }
         atomicAdd(&npre[sl], 1ull);
         atomicAdd(&refill[sl], (unsigned long long)m);
@@ -478,11 +501,10 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       }
       fr = (int)__reduce_add_sync(FM, (unsigned)fr);
       evd = (int)__reduce_add_sync(FM, (unsigned)evd);
-      smo_ev = warp_sum_ll(smo_ev);
-      dmin_dirty |= __any_sync(FM, hitmin);
+      mev = __reduce_add_sync(FM, mev);
       n_vic = nrun - qs;
       n_rd -= evd;
-      SMO -= smo_ev;
+      SMO -= (long long)mev - (long long)evd * D;
       cut = qs;
       if (pa1 > qs) pa1 = qs;
       tok += a;
@@ -491,14 +513,13 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     };
 
     if (pfirst) {  // vLLM {R_w, R_r}: every running request is a decode (no chunking)
-      if (nW > 0) warp_np(1, w0, Lw);
+      if (nW > 0) wait_scan();
       if (n_rd > 0 && (hybrid || bph != PH_PRE)) decode_group();  // else every decode fails step 2
     } else {  // Sarathi {R_r^d, R_r^p, R_w}
       if (n_rd > 0) decode_group();
-      if (cut > n_rd) warp_np(2, 0, cut);  // running prefills survive (the run list holds cut entries)
-      if (nW > 0) warp_np(1, w0, Lw);
+      if (cut > n_rd) run_prefills(cut);  // running prefills survive (the run list holds cut entries)
+      if (nW > 0) wait_scan();
     }
-    if (wnext >= 0) wfirst = lo + wnext;
     __syncwarp();
 
     if (tok == 0) {  // B = {}: idle jump to the next arrival, not a step (Q21)
@@ -516,16 +537,15 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     // the decodes of B: the a heads before pa1, n_d = a, sum m = sum(m - D) + a D over them (Table 3 features)
     long long smo_out = 0;  // sum of m - D over the decodes left out of B (positions [pa1, cut): token budget)
     if (a > 0 && cut > pa1) {  // they do not advance: offsets lowered by one
-      long long so = 0;
+      unsigned so = 0, cnt = 0;
       for (int q = pa1 + lane; q < cut; q += 32) {
         const int sl = s_run[q];
         if (!is_dec(s_fl[sl])) continue;
         const int4 rc = s_rec[sl];
-        so += rc.z;
+        so += rc.z + D, cnt++;  // (its m)
         s_rec[sl] = make_int4(rc.x, rc.y - 1, rc.z - 1, rc.w);
       }
-      smo_out = warp_sum_ll(so);
-      dmin_dirty = true;
+      smo_out = (long long)__reduce_add_sync(FM, so) - (long long)__reduce_add_sync(FM, cnt) * D;
     }
     const int nd = a;
     const long long md = a > 0 ? (SMO - smo_out) + (long long)a * D : 0;
@@ -536,7 +556,8 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     unsigned N = 0, np_ = 0, cp = 0, mp = 0, freed = 0, ndone = 0, nfa = 0;
     int n_ev = 0, dm_new = BIG;
     bool moved = false;  // SRF: some retention key changed relative to the others (movers to merge back)
-    long long c2 = 0, mc = 0, pcm = 0, pce[SIM_MAX_COST] = {0, 0, 0, 0}, smo_new = 0;
+    long long c2 = 0, mc = 0, pcm = 0, pce[SIM_MAX_COST] = {0, 0, 0, 0};
+    unsigned m_new = 0;  // sum of m over the new decodes
     // SRF: a running prefill left out of B but before pa1 is overtaken by the decodes after it (m + 1): it moves
     // too (the block kernel re-sorts whenever nd != |R_r|)
     if (srf && !pfirst && a > 0 && pa1 > a) {
@@ -590,7 +611,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
             } else {  // the (re)fill completed: a running decode from now on, in epoch form
               nfa++;
               out = make_int4(rc.x, g - D, m - D, rc.w);
-              smo_new += m - D;
+              m_new += m;
               dm_new = min(dm_new, O - (g - D));
               if (srf && sg == 0) fl |= F_MOVE_L, moved = true;
             }
@@ -611,19 +632,20 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     freed = __reduce_add_sync(FM, freed), ndone = __reduce_add_sync(FM, ndone);
     moved = __any_sync(FM, moved);
     if (np_ > 0) {
-      c2 = warp_sum_ll(c2);
-      mc = warp_sum_ll(mc);
+      // (c, m < S < 2^18, at most CAP / 32 = 128 entries per lane: every per-lane sum is below 2^44)
+      c2 = warp_sum_u51(c2);
+      mc = warp_sum_u51(mc);
       if (anyTheo) {
-        pcm = warp_sum_ll(pcm);
+        pcm = warp_sum_u51(pcm);
 #pragma unroll
-        for (int k = 0; k < SIM_MAX_COST; k++) pce[k] = warp_sum_ll(pce[k]);
+        for (int k = 0; k < SIM_MAX_COST; k++) pce[k] = warp_sum_u51(pce[k]);
       }
     }
     // decode completions: the admitted decodes reaching g = O at this epoch (completion epoch O - (g - D) == D);
     // the new decodes of this step are not in the run list yet and complete later (their epoch > D)
-    if (a > 0 && (dmin_dirty || Dmin <= D)) {
+    if (a > 0 && Dmin <= D) {
       int dm = BIG, nd2 = 0, fr2 = 0;
-      long long so = 0;
+      unsigned so = 0;
       for (int q0 = 0; q0 < cut; q0 += 32) {
         const int q = q0 + lane;
         unsigned evc = 0;
@@ -638,7 +660,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
               s_fl[sl] = (f & ~ST_MASK) | ST_DONE;
               s_rec[sl] = make_int4(rc.x, O, rc.z + D, rc.w);
               fr2 += max(rc.w, rc.z + D);
-              so += rc.z;
+              so += rc.z + D;
               nd2++;
               evc = 2;
             } else {
@@ -652,15 +674,14 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       }
       const int ndd = (int)__reduce_add_sync(FM, (unsigned)nd2);
       freed += (unsigned)__reduce_add_sync(FM, (unsigned)fr2);
-      SMO -= warp_sum_ll(so);
-      Dmin = (int)__reduce_min_sync(FM, (unsigned)dm);  // (the run-list prefills turned decodes are in it)
-      dmin_dirty = false;
+      SMO -= (long long)__reduce_add_sync(FM, so) - (long long)ndd * D;
+      Dmin = (int)__reduce_min_sync(FM, (unsigned)dm);  // exact (the run-list prefills turned decodes are in it)
       n_rd -= ndd;
       ndone += ndd;
     }
     // the new decodes join the epoch sums
     if (nfa > 0) {
-      SMO += warp_sum_ll(smo_new);
+      SMO += (long long)__reduce_add_sync(FM, m_new) - (long long)nfa * D;
       Dmin = min(Dmin, (int)__reduce_min_sync(FM, (unsigned)dm_new));
       n_rd += (int)nfa;
     }
@@ -701,23 +722,18 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     }
     // this step's victims wait from the next step on: clear Q9's mark; R_w gains them (exact count; the smallest
     // s stays a lower bound after admissions, recounted every 32 admission steps)
-    if (n_vic > 0 || n_new > 0) {
-      int vmin = 0x7fffffff, vidx = 0x7fffffff;
-      for (int v = lane; v < n_vic; v += 32) {
-        const int sl = s_vic[v];
-        s_fl[sl] &= ~F_PRE;
-        const int4 rc = s_rec[sl];
-        vmin = min(vmin, rc.x + rc.y);
-        vidx = min(vidx, sl);
-      }
-      vmin = (int)__reduce_min_sync(FM, (unsigned)vmin);
-      vidx = (int)__reduce_min_sync(FM, (unsigned)vidx);
-      wfirst = min(wfirst, vidx);
-      nW = nW - n_new + n_vic;
-      minSW = min(minSW, vmin);
-      if (n_new > 0) wstale++;
-      if (wstale >= 32) w_dirty = true;
+    for (int v = 0; v < n_vic; v++) {
+      const int sl = s_vic[v];
+      const int4 rc = s_rec[sl];
+      const int sw = rc.x + rc.y, dk = rmode == SIM_RESERVE_PEAK ? rc.x + s_O[sl] - 1 : BIG;
+      const int w = sl >> 5;
+#pragma unroll
+      for (int r = 0; r < R; r++)
+        if (r == (w >> 5) && lane == (w & 31)) wm[r] |= 1u << (sl & 31), wmS[r] = min(wmS[r], sw), wmD[r] = min(wmD[r], dk);
+      if (lane == 0) s_fl[sl] &= ~F_PRE;
     }
+    nW = nW - n_new + n_vic;
+    __syncwarp();
 
     // ---- (4) steady decode run: step j had only decodes and no admission, preemption or completion; step j+1
     // repeats it exactly (waiting rejections persist: KV is monotone in U, tokens and phases unchanged) until the
@@ -725,19 +741,16 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     // when every running request was a decode of B and every waiting candidate fails the KV test already.
     {
       bool steady = ndone == 0 && np_ == 0 && nd > 0;
-      if (steady && n_vic > 0) steady = nd == nrun0 - n_vic && (nW == 0 || (finiteM && (long long)U + minSW > M));
+      if (steady && n_vic > 0) {
+        int ms = BIG;
+#pragma unroll
+        for (int r = 0; r < R; r++) ms = min(ms, wmS[r]);
+        ms = (int)__reduce_min_sync(FM, (unsigned)ms);  // the smallest s in R_w
+        steady = nd == nrun0 - n_vic && (nW == 0 || (finiteM && (long long)U + ms > M));
+      }
       long long Lr = 0;
       if (steady) {
-        if (dmin_dirty) {  // (a left-out decode may have held the smallest completion epoch)
-          int dm = BIG;
-          for (int q = lane; q < cut; q += 32) {
-            const int sl = s_run[q];
-            if (is_dec(s_fl[sl])) dm = min(dm, s_O[sl] - s_rec[sl].y);
-          }
-          Dmin = (int)__reduce_min_sync(FM, (unsigned)dm);
-          dmin_dirty = false;
-        }
-        Lr = (long long)Dmin - D;  // steps until the next completion epoch (reached at the run's last step)
+        Lr = (long long)Dmin - D;  // steps until the next completion epoch (at most: Dmin is a lower bound)
         if (finiteM && kv1) Lr = min(Lr, (long long)(M - U) / (long long)nd);
         Lr = min(Lr, max_steps - steps);
       }
@@ -794,7 +807,6 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
               s_rec[sl] = make_int4(rc.x, rc.y - (int)E, rc.z - (int)E, rc.w);
             }
             SMO -= (long long)nout * E;
-            dmin_dirty = true;
           }
           D += (int)E;
           steps += E;
@@ -807,7 +819,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
             const double c0 = __shfl_sync(FM, clk, 0), c1 = __shfl_sync(FM, clk, 1), c2_ = __shfl_sync(FM, clk, 2),
                          c3 = __shfl_sync(FM, clk, 3);
             int dm = BIG, nd2 = 0, fr2 = 0;
-            long long so = 0;
+            unsigned so = 0;
             for (int q = lane; q < cut; q += 32) {
               const int sl = s_run[q];
               const uint8_t f = s_fl[sl];
@@ -818,7 +830,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
                 s_fl[sl] = (f & ~ST_MASK) | ST_DONE;
                 s_rec[sl] = make_int4(rc.x, O, rc.z + D, rc.w);
                 fr2 += max(rc.w, rc.z + D);
-                so += rc.z;
+                so += rc.z + D;
                 nd2++;
                 td[sl] = c0;
                 if (K > 1) td[n + sl] = c1;
@@ -830,9 +842,8 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
             }
             nd2 = (int)__reduce_add_sync(FM, (unsigned)nd2);
             U -= (int)__reduce_add_sync(FM, (unsigned)fr2);
-            SMO -= warp_sum_ll(so);
+            SMO -= (long long)__reduce_add_sync(FM, so) - (long long)nd2 * D;
             Dmin = (int)__reduce_min_sync(FM, (unsigned)dm);
-            dmin_dirty = false;
             n_rd -= nd2;
             n_done += nd2;
             ndone += nd2;
@@ -894,10 +905,9 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         if (nmov <= 32) {
           unsigned long long mk = ~0ull;
           if (lane < nmov) mk = key_of(s_vic[lane]);
-          if (nmov > 1) {  // bitonic sort of the (<= 32) mover keys across the warp
-#pragma unroll
-            for (int k2 = 2; k2 <= 32; k2 <<= 1) {
-#pragma unroll
+          if (nmov > 1) {  // bitonic sort of the first 2^ceil(log2 nmov) lanes' keys (the rest hold ~0)
+            const int P2 = 1 << (32 - __clz(nmov - 1));
+            for (int k2 = 2; k2 <= P2; k2 <<= 1) {
               for (int j = k2 >> 1; j > 0; j >>= 1) {
                 const unsigned long long o = __shfl_xor_sync(FM, mk, j);
                 const bool up = (lane & k2) == 0, lower = (lane & j) == 0;
@@ -962,18 +972,6 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       }
       nrun = cnt;
       next = nx1;
-      // the oldest unfinished request bounds the window
-      while (lo < nx1) {
-        const int q = lo + lane;
-        const unsigned dm = __ballot_sync(FM, q < nx1 && (s_fl[q] & ST_MASK) == ST_DONE);
-        if (dm == FM) {
-          lo += 32;
-        } else {
-          lo += __ffs(~dm) - 1;  // the done prefix of this chunk
-          break;
-        }
-      }
-      lo = min(lo, nx1);
       __syncwarp();
     }
   }
