@@ -152,6 +152,8 @@ typedef struct {
   double mean_latency[SIM_MAX_COST]; /* mean t_done - T */
   double mean_ttft[SIM_MAX_COST];    /* mean t_first - T */
   double mean_tpot[SIM_MAX_COST];    /* mean (t_done - t_first)/(O-1) over O > 1 */
+  int64_t formed_steps;     /* implementation counter, not a method output: the steps whose batch the kernel formed
+                               explicitly; the rest (steps - formed_steps) were charged as steady decode runs */
 } sim_result_t;
 
 /* Per-request outputs.  Config i owns rows [row_off[i], row_off[i] + n_i) of

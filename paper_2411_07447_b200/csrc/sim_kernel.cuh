@@ -68,7 +68,7 @@ struct Scal {
   double clock[SIM_MAX_COST];
   sim_cost_model_t cm[SIM_MAX_COST];
   long long U, seq;
-  long long steps, preempt, entries, processed, sumU, pentries, idle, visits;
+  long long steps, preempt, entries, processed, sumU, pentries, idle, visits, formed;
   long long runL, runMD, last_nd;
   long long tr_ent, tr_ev;  // trace records written before this step
   int runEx;

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
   int D = 0, n_rd = 0, Dmin = BIG;
   long long SMO = 0;
   double Tnext = wl.T[0];  // arrival time of request `next`
-  long long steps = 0, preempt = 0, entries = 0, processed = 0, sumU = 0, pentries = 0, idle = 0, visits = 0;
+  long long steps = 0, preempt = 0, entries = 0, processed = 0, sumU = 0, pentries = 0, idle = 0, visits = 0, formed = 0;
   int exit_status = 0;
 
   auto is_dec = [&](uint8_t f) { return (f & (ST_MASK | F_FILLED)) == (ST_RUN | F_FILLED); };
@@ -694,6 +694,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       clk = dadd(clk, batch_time(H.cm[lane], f, 0));
     }
     steps++;
+    formed++;
     sumU += U;
     entries += np_ + nd;
     processed += N;
@@ -1024,6 +1025,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     r.prefill_entries = pentries;
     r.idle_jumps = idle;
     r.visits = visits;
+    r.formed_steps = formed;
     for (int k = K; k < SIM_MAX_COST; k++) r.makespan[k] = r.mean_latency[k] = r.mean_ttft[k] = r.mean_tpot[k] = 0.0;
   }
 }

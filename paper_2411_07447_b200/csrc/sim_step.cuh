@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
   if (tid == 0) {
     for (int k = 0; k < SIM_MAX_COST; k++) S.clock[k] = 0.0;
     S.U = S.seq = 0;
-    S.steps = S.preempt = S.entries = S.processed = S.sumU = S.pentries = S.idle = S.visits = 0;
+    S.steps = S.preempt = S.entries = S.processed = S.sumU = S.pentries = S.idle = S.visits = S.formed = 0;
     S.next = S.new_next = S.lo = S.n_done = S.n_run = 0;
     S.nrank = S.nW = S.minSW = S.n_ev = S.n_vic = S.nB = 0;
     if (KN) S.tr_ent = S.tr_ev = 0;
@@ -1348,6 +1348,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           }
 #endif
           S.steps++;
+          S.formed++;
           PROF_CNT(16, 1);
           S.sumU += U;
           S.entries += f.np + f.nd;
@@ -1652,6 +1653,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     r.prefill_entries = S.pentries;
     r.idle_jumps = S.idle;
     r.visits = S.visits;
+    r.formed_steps = S.formed;
     for (int k = K; k < SIM_MAX_COST; k++) r.makespan[k] = r.mean_latency[k] = r.mean_ttft[k] = r.mean_tpot[k] = 0.0;
   }
 }

@@ -58,7 +58,7 @@ class SimResult(ctypes.Structure):
                 ("idle_jumps", ctypes.c_int64), ("visits", ctypes.c_int64),
                 ("makespan", ctypes.c_double * SIM_MAX_COST),
                 ("mean_latency", ctypes.c_double * SIM_MAX_COST), ("mean_ttft", ctypes.c_double * SIM_MAX_COST),
-                ("mean_tpot", ctypes.c_double * SIM_MAX_COST)]
+                ("mean_tpot", ctypes.c_double * SIM_MAX_COST), ("formed_steps", ctypes.c_int64)]
 
 
 class SimBatchShape(ctypes.Structure):
@@ -104,7 +104,8 @@ TRACE_EVENT_DTYPE = np.dtype([("id", "<i4"), ("m", "<i4")])
 RESULT_DTYPE = np.dtype([("status", "<i4"), ("pad", "<i4"), ("steps", "<i8"), ("preemptions", "<i8"),
                          ("batch_entries", "<i8"), ("processed_tokens", "<i8"), ("sum_U", "<i8"),
                          ("prefill_entries", "<i8"), ("idle_jumps", "<i8"), ("visits", "<i8"), ("makespan", "<f8", (4,)),
-                         ("mean_latency", "<f8", (4,)), ("mean_ttft", "<f8", (4,)), ("mean_tpot", "<f8", (4,))])
+                         ("mean_latency", "<f8", (4,)), ("mean_ttft", "<f8", (4,)), ("mean_tpot", "<f8", (4,)),
+                         ("formed_steps", "<i8")])
 assert RESULT_DTYPE.itemsize == ctypes.sizeof(SimResult)
 
 _lib = None

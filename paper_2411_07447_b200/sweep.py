@@ -57,6 +57,75 @@ def varying_m_sweep(Ms=(100, 1_000, 10_000, 100_000, 1_000_000), O: int = 32, W:
     return cfgs, wls, cms, labels
 
 
+K4_LINEAR = ("llama3-8b_a100_linear", "llama3-8b_h100_linear", "llama3-70b_a100x4_linear", "llama3-70b_h100x4_linear")
+
+
+def full_sweep(seeds=range(10), grid_W=(32, 1024), M: int = 100_000, online: bool = True, hetero: bool = True):
+    """The north-star sweep (BASELINE.json north_star): BASELINE configs [1]-[5] in one list.
+
+    * [1] + [2]: the 6 grid presets x {NRF, SRF} x I, O in {1, 2, ..., 1024} x W in {32, 1024}, each schedule
+      charged under K = 4 cost models at once ({8B, 70B} x {A100, H100}, linear; offline schedules are
+      cost-model independent, PAPER.md:29) -- 2 x 1 452 simulations, 4 x that many configs;
+    * [3]: online LongForm-like and AzureConv-like traces x seeds x {vLLM (C = S), Sarathi
+      (C = 512)} x {NRF, SRF, SRF+Hist}, Llama-3-8B / A100, M = 100 000, S = 128K (PAPER.md:661);
+    * [4]: the same traces x Llama-3-70B on 4 x A100 and 4 x H100 x {NRF, SRF} x {M, infinite M} x {linear,
+      theoretical} (vLLM order; PAPER.md:3, 12-13, 672-675);
+    * [5]: W = 1024 heterogeneous mixes (ShareGPT-like, table-QA, text-to-SQL, their long-context variants, App. D
+      SILO+LISO and SISO+LILO pairs) x seeds x Rank_org / Rank_I / Rank_O.
+    Returns (cfgs, wls, cost_model_list, labels); labels are (config-class, name, workload) strings."""
+    pcms = simsweep.load_cost_models()
+    cost_names = list(K4_LINEAR) + ["llama3-70b_a100x4_theoretical", "llama3-70b_h100x4_theoretical"]
+    cms = [pcms[c] for c in cost_names]
+    cix = {c: i for i, c in enumerate(cost_names)}
+    wls, cfgs, labels = [], [], []
+
+    def add_wl(w):
+        wls.append(w)
+        return len(wls) - 1
+
+    vals = workloads.grid_values()
+    for W in grid_W:
+        base = len(wls)
+        for I in vals:
+            for O in vals:
+                add_wl(workloads.fixed(I, O, W))
+        for name in presets.GRID_PRESETS:
+            for pol in ("", "-srf"):
+                for j, (I, O) in enumerate([(I, O) for I in vals for O in vals]):
+                    cfgs.append(simsweep.preset_config(name + pol, M, workload=base + j,
+                                                       cost=tuple(cix[c] for c in K4_LINEAR)))
+                    labels.append(("grid", f"{name}{pol} W={W}", f"I={I} O={O}"))
+    if online:
+        S = 131072
+        for seed in seeds:
+            for kind, gen in (("longform", workloads.longform), ("azureconv", workloads.azureconv)):
+                wi = add_wl(gen(seed))
+                for name in ("vllm", "sarathi"):
+                    for pol in ("", "-srf", "-srf-hist"):
+                        cfgs.append(simsweep.preset_config(name + pol, M, S=S, workload=wi,
+                                                           cost=(cix["llama3-8b_a100_linear"],)))
+                        labels.append(("online-8B", f"{name}{pol}", f"{kind} s{seed}"))
+                for cm in ("llama3-70b_a100x4", "llama3-70b_h100x4"):
+                    for mode in ("linear", "theoretical"):
+                        for pol in ("", "-srf"):
+                            for MM in (M, -1):
+                                cfgs.append(simsweep.preset_config("vllm" + pol, MM, S=S, workload=wi,
+                                                                   cost=(cix[f"{cm}_{mode}"],)))
+                                labels.append(("online-70B", f"vllm{pol} {cm}_{mode} M={'inf' if MM < 0 else MM}",
+                                               f"{kind} s{seed}"))
+    if hetero:
+        for seed in seeds:
+            mixes = [workloads.sharegpt(seed), workloads.table_qa(seed), workloads.table_qa(seed, long_context=True),
+                     workloads.text_to_sql(seed), workloads.text_to_sql(seed, long_context=True),
+                     workloads.mix(("SILO", "LISO"), 1024, seed), workloads.mix(("SISO", "LILO"), 1024, seed)]
+            for w in mixes:
+                wi = add_wl(w)
+                for name in ("rank-org", "rank-i", "rank-o"):
+                    cfgs.append(simsweep.preset_config(name, M, workload=wi, cost=(cix["llama3-8b_a100_linear"],)))
+                    labels.append(("hetero", name, w.name))
+    return cfgs, wls, cms, labels
+
+
 def estimate(cfgs, wls) -> np.ndarray:
     """Step-count estimate per simulation (LPT key): max O + KV-time area / M + sum I / C (area = sum (I + O/2) O,
     or the reserve times O under the preemption-free reserves)."""
