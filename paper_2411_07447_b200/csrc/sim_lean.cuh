@@ -45,10 +45,14 @@ struct LHead {
   sim_cost_model_t cm[SIM_MAX_COST];
 };
 
-template <int CAP>
+// Per-slot arrays (41 B per slot): in shared memory right after LHead, or (GM: workloads of n > 4096 requests, up
+// to SIM_MAX_WINDOW) in a per-CTA arena of the caller's workspace, served from L1 / L2; a GM CTA keeps LHead and the
+// waiting bitmap (12 B per 32 slots) in shared memory.  Slots are request indices (n <= CAP: no ring).
+template <int CAP, bool GM>
 struct LLayout {
   static constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
-  static constexpr size_t rec = a16(sizeof(LHead));  // int4 {I, g | g - D, m | m - D, reserved}
+  static constexpr size_t head = a16(sizeof(LHead));
+  static constexpr size_t rec = GM ? 0 : head;       // int4 {I, g | g - D, m | m - D, reserved}
   static constexpr size_t O = rec + 16 * CAP;        // int32
   static constexpr size_t seq = O + 4 * CAP;         // int32 admission sequence number (Q6)
   static constexpr size_t c = seq + 4 * CAP;         // int32 c of this batch's prefill entries  \ u64 sort keys
@@ -58,7 +62,9 @@ struct LLayout {
   static constexpr size_t nw = run2 + 2 * CAP;       // int16 admitted from R_w this step, in admission order
   static constexpr size_t vic = nw + 2 * CAP;        // int16 preempted this step, then the SRF movers
   static constexpr size_t fl = vic + 2 * CAP;        // uint8 status and flags
-  static constexpr size_t bytes = a16(fl + CAP);     // 41 B per slot
+  static constexpr size_t arr_bytes = a16(fl + CAP) - rec;  // 41 B per slot
+  static constexpr size_t words = CAP / 32;                    // waiting bitmap (GM: in shared memory)
+  static constexpr size_t smem = GM ? head + 12 * words : a16(fl + CAP);
 };
 
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
@@ -78,15 +84,16 @@ __device__ __forceinline__ long long warp_sum_u51(unsigned long long v) {
 // the low bits so that sorting keys sorts slots
 template <int SLB>
 __device__ __forceinline__ unsigned long long srf_key(int m, int seq, int slot) {
-  return ((unsigned long long)(0x3FFFF - m) << 43) | ((unsigned long long)(unsigned)seq << SLB) | (unsigned)slot;
+  // bits: 18 of 0x3FFFF - m (m <= S < 2^18) | 31 of seq (< 2^31, SEQ_LIM) | SLB of slot: 49 + SLB <= 64
+  return ((unsigned long long)(0x3FFFF - m) << (31 + SLB)) | ((unsigned long long)(unsigned)seq << SLB) | (unsigned)slot;
 }
 
-template <int CAP>
+template <int CAP, bool GM>
 __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
-  using L = LLayout<CAP>;
+  using L = LLayout<CAP, GM>;
   constexpr unsigned FM = 0xffffffffu;
   constexpr int SLB = __builtin_ctz(CAP);
-  static_assert(SLB <= 12, "slot bits of the SRF key");
+  static_assert(SLB <= 15, "int16 slots; slot bits of the SRF key");
   constexpr long long SEQ_LIM = 0x7fffffffll - CAP;  // the int32 admission counter must not wrap
   constexpr int BIG = 0x3fffffff;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -95,18 +102,29 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
   const unsigned lt = (1u << lane) - 1u;
   const int ci = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
   if (kernel_variant(p.cfgs[ci], p.wls[p.cfgs[ci].workload].n, p.lean) != p.variant) return;
-  int4* s_rec = reinterpret_cast<int4*>(smem + L::rec);
-  int32_t* s_O = reinterpret_cast<int32_t*>(smem + L::O);
-  int32_t* s_seq = reinterpret_cast<int32_t*>(smem + L::seq);
-  int32_t* s_c = reinterpret_cast<int32_t*>(smem + L::c);
-  int32_t* s_ev = reinterpret_cast<int32_t*>(smem + L::ev);
-  double* s_dbuf = reinterpret_cast<double*>(smem + L::ev);                        // steady run: batch times
-  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem + L::c);  // SRF merge: CAP keys
-  int16_t* s_run = reinterpret_cast<int16_t*>(smem + L::run);
-  int16_t* s_run2 = reinterpret_cast<int16_t*>(smem + L::run2);
-  int16_t* s_new = reinterpret_cast<int16_t*>(smem + L::nw);
-  int16_t* s_vic = reinterpret_cast<int16_t*>(smem + L::vic);
-  uint8_t* s_fl = smem + L::fl;
+  unsigned char* arr = smem;
+  if constexpr (GM) {  // claim a per-CTA arena of the workspace (the stride of the block kernel's GM arenas)
+    int a0 = 0;
+    if (lane == 0) a0 = p.arena_base + (int)atomicAdd(reinterpret_cast<unsigned*>(p.ws + p.ctr_off), 1u);
+    a0 = __shfl_sync(FM, a0, 0);
+    arr = p.ws + WS_HEADER + (size_t)a0 * Smem<512, SIM_MAX_WINDOW>::arr_bytes;
+  }
+  int4* s_rec = reinterpret_cast<int4*>(arr + L::rec);
+  int32_t* s_O = reinterpret_cast<int32_t*>(arr + L::O);
+  int32_t* s_seq = reinterpret_cast<int32_t*>(arr + L::seq);
+  int32_t* s_c = reinterpret_cast<int32_t*>(arr + L::c);
+  int32_t* s_ev = reinterpret_cast<int32_t*>(arr + L::ev);
+  double* s_dbuf = reinterpret_cast<double*>(arr + L::ev);                        // steady run: batch times
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(arr + L::c);  // SRF merge: CAP keys
+  int16_t* s_run = reinterpret_cast<int16_t*>(arr + L::run);
+  int16_t* s_run2 = reinterpret_cast<int16_t*>(arr + L::run2);
+  int16_t* s_new = reinterpret_cast<int16_t*>(arr + L::nw);
+  int16_t* s_vic = reinterpret_cast<int16_t*>(arr + L::vic);
+  uint8_t* s_fl = arr + L::fl;
+  // GM: the waiting bitmap's words in shared memory: bits, smallest s, smallest PEAK reserve (BIG if empty)
+  unsigned* g_wb = reinterpret_cast<unsigned*>(smem + L::head);
+  int* g_ws = reinterpret_cast<int*>(g_wb + L::words);
+  int* g_wd = g_ws + L::words;
 
   const sim_config_t cfg = p.cfgs[ci];
   const sim_workload_t wl = p.wls[cfg.workload];
@@ -167,11 +185,31 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
   // the waiting group R_w as a bitmap: word w (32 slots) belongs to lane w % 32, row w / 32; per word the smallest
   // s and (PEAK reserve) the smallest initial reserve of its waiting requests (BIG if none) -- a chunk can hold an
   // admissible candidate only if these pass the step's token and KV limits
-  constexpr int R = CAP / 1024;
+  // (GM: the words live in shared memory, g_wb / g_ws / g_wd; lane l keeps a summary of words [32 l, 32 l + 32):
+  // gb = which of them hold a waiting request, gs / gd = their smallest s / reserve)
+  constexpr int R = GM ? 1 : CAP / 1024;
   unsigned wm[R];
   int wmS[R], wmD[R];
 #pragma unroll
   for (int r = 0; r < R; r++) wm[r] = 0u, wmS[r] = BIG, wmD[r] = BIG;
+  unsigned gb = 0u;
+  int gs = BIG, gd = BIG;
+  if constexpr (GM) {
+    for (int w = lane; w < (int)L::words; w += 32) g_wb[w] = 0u, g_ws[w] = BIG, g_wd[w] = BIG;
+    __syncwarp();
+  }
+  // R_w gains request slot sl (s, reserve dk): one word's bit and minima (and its summary lane)
+  auto wait_add = [&](int sl, int sw, int dk) {
+    const int w = sl >> 5;
+    if constexpr (GM) {
+      if (lane == 0) g_wb[w] |= 1u << (sl & 31), g_ws[w] = min(g_ws[w], sw), g_wd[w] = min(g_wd[w], dk);
+      if (lane == (w >> 5)) gb |= 1u << (w & 31), gs = min(gs, sw), gd = min(gd, dk);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; r++)
+        if (r == (w >> 5) && lane == (w & 31)) wm[r] |= 1u << (sl & 31), wmS[r] = min(wmS[r], sw), wmD[r] = min(wmD[r], dk);
+    }
+  };
   // decode epochs: a running decode holds rec.y = g - D, rec.z = m - D; n_rd of them, SMO = the sum of their m - D,
   // Dmin = a lower bound of their smallest completion epoch O - (g - D) (exact after every completion scan;
   // evictions and left-out decodes only raise the true minimum)
@@ -212,10 +250,16 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         const int md_ = rmode == SIM_RESERVE_PEAK
                             ? (int)__reduce_min_sync(FM, in ? (unsigned)(s_rec[sl].x + s_O[sl] - 1) : (unsigned)BIG)
                             : BIG;
+        if constexpr (GM) {
+          if (lane == 0) g_wb[w] |= bits, g_ws[w] = min(g_ws[w], ms), g_wd[w] = min(g_wd[w], md_);
+          if (lane == (w >> 5)) gb |= 1u << (w & 31), gs = min(gs, ms), gd = min(gd, md_);
+        } else {
 #pragma unroll
-        for (int r = 0; r < R; r++)
-          if (r == (w >> 5) && lane == (w & 31)) wm[r] |= bits, wmS[r] = min(wmS[r], ms), wmD[r] = min(wmD[r], md_);
+          for (int r = 0; r < R; r++)
+            if (r == (w >> 5) && lane == (w & 31)) wm[r] |= bits, wmS[r] = min(wmS[r], ms), wmD[r] = min(wmD[r], md_);
+        }
       }
+      __syncwarp();
       nW += nx1 - next;
     }
     if (n_done == n) {
@@ -342,31 +386,74 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
 
     // R_w in index order (Q1, Q2): only the bitmap words whose smallest s / reserve pass the current token and KV
     // limits can hold an admissible candidate (rejections change no state, so the others are skipped whole)
+    auto kv_pass = [&](int ms, int md_, int capM) {  // a word (or group) can hold a candidate passing the KV test
+      return rmode == SIM_RESERVE_SEQ ? ms <= capM : (rmode == SIM_RESERVE_PEAK ? md_ <= capM : Sctx <= capM);
+    };
+    // one bitmap word w (32 slots, `word` = its waiting bits): admit its candidates; returns the bits left waiting
+    // and their minima
+    auto wait_word = [&](int w, unsigned word, int& ms, int& md_) -> unsigned {
+      const int sl = w * 32 + lane;
+      const bool isw = (word >> lane) & 1u;
+      const int4 rc = isw ? s_rec[sl] : make_int4(0, 0, 0, 0);
+      const int sw = rc.x + rc.y, dkv = isw ? rnew(rc, sl) : 0;  // avail = s (m = 0)
+      const unsigned admm = admit_chunk(true, sl, rc, sw, dkv, isw);
+      const unsigned left = word & ~admm;
+      const bool lw = (left >> lane) & 1u;
+      ms = (int)__reduce_min_sync(FM, lw ? (unsigned)sw : (unsigned)BIG);
+      md_ = rmode == SIM_RESERVE_PEAK ? (int)__reduce_min_sync(FM, lw ? (unsigned)dkv : (unsigned)BIG) : BIG;
+      return left;
+    };
     auto wait_scan = [&]() {
+      if constexpr (GM) {  // two levels: summary lanes, then the 32 words of the first passing lane
+        int curL = 0, curW = 0;  // next word to visit: 32 curL + curW
+        for (;;) {
+          if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;
+          const int capT = chunked ? BIG : C - tok, capM = finiteM ? M - U : BIG;
+          const unsigned lb = __ballot_sync(FM, lane >= curL && gb != 0u && gs <= capT && kv_pass(gs, gd, capM));
+          if (!lb) return;
+          const int Lg = __ffs(lb) - 1;
+          const int wj = 32 * Lg + lane;
+          const unsigned bj = g_wb[wj];
+          const int sj = g_ws[wj], dj = g_wd[wj];
+          const unsigned wbm = __ballot_sync(FM, bj != 0u && sj <= capT && kv_pass(sj, dj, capM) && (Lg > curL || lane >= curW));
+          if (!wbm) {
+            curL = Lg + 1, curW = 0;
+            continue;
+          }
+          const int Wj = __ffs(wbm) - 1, w = 32 * Lg + Wj;
+          const unsigned word = __shfl_sync(FM, bj, Wj);
+          int ms, md_;
+          const unsigned left = wait_word(w, word, ms, md_);
+          if (left != word) {  // admissions: the word and its group's summary change
+            if (lane == 0) g_wb[w] = left, g_ws[w] = ms, g_wd[w] = md_;
+            __syncwarp();
+            const unsigned b2 = g_wb[wj];
+            const int s2 = g_ws[wj], d2 = g_wd[wj];
+            const unsigned nb = __ballot_sync(FM, b2 != 0u);
+            const int gs2 = (int)__reduce_min_sync(FM, (unsigned)s2), gd2 = (int)__reduce_min_sync(FM, (unsigned)d2);
+            if (lane == Lg) gb = nb, gs = gs2, gd = gd2;
+          }
+          curL = Lg, curW = Wj + 1;
+          if (curW == 32) curL++, curW = 0;
+          if (chunked && tok >= C) return;
+        }
+      } else {
 #pragma unroll
       for (int r = 0; r < R; r++) {
         int cur = 0;
         for (;;) {
           if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining candidate fails
           const int capT = chunked ? BIG : C - tok, capM = finiteM ? M - U : BIG;
-          const bool kvok = rmode == SIM_RESERVE_SEQ ? wmS[r] <= capM
-                                                     : (rmode == SIM_RESERVE_PEAK ? wmD[r] <= capM : Sctx <= capM);
-          const unsigned cb = __ballot_sync(FM, lane >= cur && wm[r] != 0u && wmS[r] <= capT && kvok);
+          const unsigned cb = __ballot_sync(FM, lane >= cur && wm[r] != 0u && wmS[r] <= capT && kv_pass(wmS[r], wmD[r], capM));
           if (!cb) break;
           const int Lc = __ffs(cb) - 1;
           cur = Lc + 1;
           const unsigned word = __shfl_sync(FM, wm[r], Lc);
-          const int sl = (r * 32 + Lc) * 32 + lane;
-          const bool isw = (word >> lane) & 1u;
-          const int4 rc = isw ? s_rec[sl] : make_int4(0, 0, 0, 0);
-          const int sw = rc.x + rc.y, dkv = isw ? rnew(rc, sl) : 0;  // avail = s (m = 0)
-          const unsigned admm = admit_chunk(true, sl, rc, sw, dkv, isw);
-          const unsigned left = word & ~admm;
-          const bool lw = (left >> lane) & 1u;
-          const int ms = (int)__reduce_min_sync(FM, lw ? (unsigned)sw : (unsigned)BIG);
-          const int md_ = rmode == SIM_RESERVE_PEAK ? (int)__reduce_min_sync(FM, lw ? (unsigned)dkv : (unsigned)BIG) : BIG;
+          int ms, md_;
+          const unsigned left = wait_word(r * 32 + Lc, word, ms, md_);
           if (lane == Lc) wm[r] = left, wmS[r] = ms, wmD[r] = md_;
         }
+      }
       }
     };
 
@@ -726,11 +813,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     for (int v = 0; v < n_vic; v++) {
       const int sl = s_vic[v];
       const int4 rc = s_rec[sl];
-      const int sw = rc.x + rc.y, dk = rmode == SIM_RESERVE_PEAK ? rc.x + s_O[sl] - 1 : BIG;
-      const int w = sl >> 5;
-#pragma unroll
-      for (int r = 0; r < R; r++)
-        if (r == (w >> 5) && lane == (w & 31)) wm[r] |= 1u << (sl & 31), wmS[r] = min(wmS[r], sw), wmD[r] = min(wmD[r], dk);
+      wait_add(sl, rc.x + rc.y, rmode == SIM_RESERVE_PEAK ? rc.x + s_O[sl] - 1 : BIG);
       if (lane == 0) s_fl[sl] &= ~F_PRE;
     }
     nW = nW - n_new + n_vic;
@@ -743,7 +826,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     {
       bool steady = ndone == 0 && np_ == 0 && nd > 0;
       if (steady && n_vic > 0) {
-        int ms = BIG;
+        int ms = GM ? gs : BIG;
 #pragma unroll
         for (int r = 0; r < R; r++) ms = min(ms, wmS[r]);
         ms = (int)__reduce_min_sync(FM, (unsigned)ms);  // the smallest s in R_w

@@ -64,14 +64,14 @@ __host__ __device__ inline bool has_knobs(const sim_config_t& c) {
 constexpr int N_GENERAL = 2 * N_SIZES;
 // the lean one-warp kernel (sim_lean.cuh) for the configurations that dominate the north-star sweep: the vLLM /
 // Sarathi presets (prefill-first without chunking, or decode-first), NRF / SRF / PF, no knob, no SRF+Hist, no trace
-constexpr int V_LEAN = N_GENERAL;  // + 0: n <= 1024, + 1: n <= 4096 (state in shared memory)
-constexpr int N_VARIANTS = N_GENERAL + 2;
+constexpr int V_LEAN = N_GENERAL;  // + 0: n <= 1024, + 1: n <= 4096 (state in shared memory), + 2: n <= 32768 (arena)
+constexpr int N_VARIANTS = N_GENERAL + 3;
 __host__ __device__ inline bool lean_ok(const sim_config_t& c, int n) {
-  return !has_knobs(c) && c.replacement != SIM_SRF_HIST && n <= 4096 &&
+  return !has_knobs(c) && c.replacement != SIM_SRF_HIST && n <= SIM_MAX_WINDOW &&
          ((c.order == SIM_ORDER_PREFILL_FIRST && !c.chunked) || c.order == SIM_ORDER_DECODE_FIRST);
 }
 __host__ __device__ inline int kernel_variant(const sim_config_t& c, int n, int lean) {
-  if (lean && lean_ok(c, n)) return V_LEAN + (n <= 1024 ? 0 : 1);
+  if (lean && lean_ok(c, n)) return V_LEAN + (n <= 1024 ? 0 : (n <= 4096 ? 1 : 2));
   return variant_of(n) + (has_knobs(c) ? N_SIZES : 0);
 }
 
@@ -116,16 +116,17 @@ Variant make_variant() {
   using L = Smem<NT, CAP>;
   return Variant{NT, CAP, GM ? L::scal : L::bytes, GM ? L::arr_bytes : 0, sim_kernel<NT, CAP, IPT_, GM, KN>};
 }
-template <int CAP>
+template <int CAP, bool GM>
 Variant make_lean() {
-  return Variant{32, CAP, LLayout<CAP>::bytes, 0, sim_lean_kernel<CAP>};
+  return Variant{32, CAP, LLayout<CAP, GM>::smem, GM ? Smem<512, SIM_MAX_WINDOW>::arr_bytes : 0, sim_lean_kernel<CAP, GM>};
 }
 
 static Variant g_variants[N_VARIANTS] = {
     make_variant<SIM_NT_SMALL, 1024, SIM_IPT_SMALL, false, false>(), make_variant<512, 4096, 4, false, false>(),
     make_variant<512, SIM_MAX_WINDOW, 4, true, false>(),           make_variant<SIM_NT_SMALL, 1024, SIM_IPT_SMALL, false, true>(),
     make_variant<512, 4096, 4, false, true>(),                     make_variant<512, SIM_MAX_WINDOW, 4, true, true>(),
-    make_lean<1024>(),                                             make_lean<4096>()};
+    make_lean<1024, false>(),                                      make_lean<4096, false>(),
+    make_lean<SIM_MAX_WINDOW, true>()};
 
 // SIMSWEEP_LEAN=0 in the environment routes every config to the block kernel (parity tests run both kernels)
 static int lean_enabled() {
@@ -284,7 +285,7 @@ static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_
   }
   int launches = 0;
   // the large-window variants first: their simulations are the longest
-  static const int launch_order[N_VARIANTS] = {2, 2 + N_SIZES, V_LEAN + 1, 1, 1 + N_SIZES, V_LEAN, 0, N_SIZES};
+  static const int launch_order[N_VARIANTS] = {2, 2 + N_SIZES, V_LEAN + 2, V_LEAN + 1, 1, 1 + N_SIZES, V_LEAN, 0, N_SIZES};
   for (int vi = 0; vi < N_VARIANTS; vi++) {
     const int v = launch_order[vi];
     if (!cnt[v]) continue;
@@ -299,8 +300,9 @@ static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_
       g_attr_set[dev] |= 1u << v;
     }
     kp.variant = v;
-    kp.arena_base = v == 2 + N_SIZES ? cnt[2] : 0;  // the two GM variants share the workspace: disjoint arenas
-    kp.ctr_off = v == 2 + N_SIZES ? 64 : 0;
+    // the three GM variants share the workspace: disjoint arenas, one counter each
+    kp.arena_base = v == 2 + N_SIZES ? cnt[2] : (v == V_LEAN + 2 ? cnt[2] + cnt[2 + N_SIZES] : 0);
+    kp.ctr_off = v == 2 + N_SIZES ? 64 : (v == V_LEAN + 2 ? 128 : 0);
     cudaStream_t s = nneed > 1 ? ax.s[v] : main;
     if (nneed > 1 && cudaStreamWaitEvent(s, ax.fork, 0) != cudaSuccess) return SIM_ECUDA;
     void* args[] = {&kp};

@@ -93,3 +93,52 @@ def test_holdings_capacity_boundary():
     # the same workloads with a finite M are simulated (U <= M < 2^30)
     fin = (cfg(0, 0, 0, 0, big, 100_000_000, S=131072), workloads.fixed(65536, 2, 32768), A100)
     assert_parity([fin])
+
+
+def _with_lean(flag, fn):
+    import os
+    old = os.environ.get("SIMSWEEP_LEAN")
+    os.environ["SIMSWEEP_LEAN"] = flag
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ["SIMSWEEP_LEAN"]
+        else:
+            os.environ["SIMSWEEP_LEAN"] = old
+
+
+@pytest.mark.parametrize("block", range(2))
+def test_block_kernel_still_matches(block):
+    """The block kernel (sim_step.cuh) keeps every configuration it owns (rank orders, knobs, SRF+Hist, traces);
+    with SIMSWEEP_LEAN=0 it also runs the ones the lean kernel owns, so both stay parity-checked on the same
+    cases: random contention configs and full-size grid cells against the oracle."""
+    cases = []
+    for seed in range(12000 + block * 50, 12000 + block * 50 + 50):
+        rng = np.random.default_rng(seed)
+        Wn = int(rng.integers(8, 600))
+        wl = workloads.random_small(seed, Wn, max_len=int(rng.integers(4, 200)), online=bool(rng.integers(0, 2)), S=512)
+        o_ = int(rng.integers(0, 2))
+        r = int(rng.integers(0, 2))
+        chunked = int(rng.integers(0, 2)) if o_ == 1 else 0
+        hybrid = int(rng.integers(0, 2))
+        peak = int((wl.I.astype(int) + wl.O - 1).max())
+        C = int(rng.integers(max(1, peak // 4), 2 * peak + 1)) if chunked else int(rng.integers(peak, 3 * peak + 1))
+        M = int(rng.integers(peak, 6 * peak + 1))
+        cases.append((cfg(o_, hybrid, chunked, r, C, M, S=512), wl, A100))
+    for nm in ("vllm-srf", "sarathi"):
+        cases.append((simsweep.preset_config(nm, 100_000), workloads.fixed(128, 1024, 1024), A100))
+    g_block, _ = _with_lean("0", lambda: assert_parity(cases))
+    g_lean, _ = assert_parity(cases)
+    for f in ("steps", "preemptions", "batch_entries", "processed_tokens", "sum_U", "visits"):
+        assert np.array_equal(g_block.results[f], g_lean.results[f]), f
+    assert g_block.t_done.tobytes() == g_lean.t_done.tobytes()
+
+
+def test_lean_large_window_azureconv():
+    """The lean kernel's arena variant (n > 4096: workload state in the caller's workspace, the waiting bitmap in
+    shared memory) on the AzureConv-like trace at full size (N = 19 700) under vLLM / Sarathi x NRF / SRF / PF."""
+    wl = workloads.azureconv(2)
+    cases = [(simsweep.preset_config(nm, 100_000, S=131072), wl, A100)
+             for nm in ("vllm", "vllm-srf", "sarathi", "sarathi-srf", "vllm-pf")]
+    assert_parity(cases, processes=len(cases))
