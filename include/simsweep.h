@@ -343,18 +343,20 @@ int sim_operator_costs(const sim_cost_model_t* cms, int32_t n_cms, const sim_bat
  * prefills unless the request's last (re)fill completed).  Batches with sum c = 0 are not considered (a
  * preemption can always ride with the next batch; readings Q43-Q45).  Solved exactly on the GPU by parallel
  * relaxation rounds over the dense state space (every reachable state, fp64 path sums), so the result is the
- * minimum over ALL schedules: a lower bound for every simulated preset. */
+ * minimum over ALL schedules: a lower bound for every simulated preset.  Identical requests (same I and O) are
+ * interchangeable, so a state is stored once per multiset of their local states (`states` counts those). */
 #define SIM_OPT_MAX_N 4
+#define SIM_OPT_NO_PREEMPT 1
 typedef struct {
   int32_t n;                   /* requests, 1..SIM_OPT_MAX_N */
   int32_t I[SIM_OPT_MAX_N];    /* >= 1 */
   int32_t O[SIM_OPT_MAX_N];    /* >= 1 */
-  int32_t pad;
+  int32_t flags;               /* bit 0 (SIM_OPT_NO_PREEMPT): e = 0 always -- the optimum over preemption-free schedules */
   int64_t C;                   /* token limit per batch, >= 1 */
   int64_t M;                   /* KV limit per batch, >= 0 (finite) */
 } sim_opt_problem_t;
 typedef struct {
-  int32_t status;  /* 0 ok, 1 unreachable (some I + O - 1 > M), 2 state space too large (> 2^25 states) */
+  int32_t status;  /* 0 ok, 1 unreachable (some I + O - 1 > M), 2 state space too large (> 2^28 states) */
   int32_t rounds;  /* relaxation rounds until no state improved */
   int64_t states;  /* reachable states */
   double optimum;  /* min over schedules of sum_j d_j (seconds); 0 unless status 0 */

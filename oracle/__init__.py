@@ -253,18 +253,20 @@ class OracleOpt(ctypes.Structure):
                 ("optimum", ctypes.c_double)]
 
 
-def optimum(I, O, C: int, M: int, cost: OracleCost):
-    """Exact CSP optimum (Dijkstra): -> (status 'ok' | 'unreachable', reachable states, min sum_j d_j)."""
+def optimum(I, O, C: int, M: int, cost: OracleCost, no_preempt: bool = False):
+    """Exact CSP optimum (Dijkstra; identical requests merged): -> (status 'ok' | 'unreachable', reachable states,
+    min sum_j d_j).  no_preempt: the optimum over preemption-free schedules (e = 0 always)."""
     Ia = np.ascontiguousarray(I, np.int32)
     Oa = np.ascontiguousarray(O, np.int32)
     out = OracleOpt()
     L = lib()
     L.oracle_optimum.restype = ctypes.c_int
     L.oracle_optimum.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
-                                 ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(OracleCost), ctypes.POINTER(OracleOpt)]
+                                 ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(OracleCost),
+                                 ctypes.POINTER(OracleOpt)]
     rc = L.oracle_optimum(len(Ia), Ia.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                          Oa.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), int(C), int(M), ctypes.byref(cost),
-                          ctypes.byref(out))
+                          Oa.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), int(C), int(M), int(bool(no_preempt)),
+                          ctypes.byref(cost), ctypes.byref(out))
     if rc < 0:
         raise ValueError(f"oracle_optimum call error {rc}")
     return ("ok" if out.status == 0 else "unreachable"), int(out.states), float(out.optimum)

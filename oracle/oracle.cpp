@@ -589,17 +589,37 @@ struct OptReq {
   bool filled, done;
 };
 
-int oracle_optimum(int32_t n, const int32_t* I, const int32_t* O, int64_t C, int64_t M, const oracle_cost_t* cm,
+int oracle_optimum(int32_t n, const int32_t* I, const int32_t* O, int64_t C, int64_t M, int32_t no_preempt,
+                   const oracle_cost_t* cm,
                    oracle_opt_t* out) {
   if (n < 1 || !I || !O || !cm || !out || C < 1 || M < 0) return -1;
   for (int i = 0; i < n; i++)
     if (I[i] < 1 || O[i] < 1) return -5;
   using State = std::vector<OptReq>;
+  // Requests with the same (I, O) are interchangeable: permuting them maps every schedule to one of the same
+  // cost, so a state is identified up to such permutations -- its key lists each request's (g, filled, m) pair
+  // with the pairs of every group of identical requests sorted (the canonical representative)
+  std::vector<std::vector<int>> groups;
+  for (int i = 0; i < n; i++) {
+    bool placed = false;
+    for (auto& gr : groups)
+      if (I[gr[0]] == I[i] && O[gr[0]] == O[i]) {
+        gr.push_back(i);
+        placed = true;
+        break;
+      }
+    if (!placed) groups.push_back({i});
+  }
   auto key = [&](const State& st) {
     std::vector<int64_t> k;
-    for (const OptReq& r : st) {
-      k.push_back(r.done ? -1 : 2 * r.g + (r.filled ? 1 : 0));
-      k.push_back(r.done ? 0 : r.m);
+    for (const auto& gr : groups) {
+      std::vector<std::pair<int64_t, int64_t>> pr;
+      for (int i : gr) {
+        const OptReq& r = st[i];
+        pr.push_back({r.done ? -1 : 2 * r.g + (r.filled ? 1 : 0), r.done ? 0 : r.m});
+      }
+      std::sort(pr.begin(), pr.end());
+      for (auto& x : pr) k.push_back(x.first), k.push_back(x.second);
     }
     return k;
   };
@@ -656,7 +676,7 @@ int oracle_optimum(int32_t n, const int32_t* I, const int32_t* O, int64_t C, int
       const int64_t s = I[i] + r.g;
       v[i] = r;  // idle: c = 0, e = 0
       rec(i + 1, sum_c, sum_m + r.m);
-      if (r.m > 0) {  // preempt: e = 1, m := 0, c = 0 (Eq. (4)-(5))
+      if (r.m > 0 && !no_preempt) {  // preempt: e = 1, m := 0, c = 0 (Eq. (4)-(5)); off: preemption-free schedules
         v[i] = OptReq{r.g, 0, false, false};
         rec(i + 1, sum_c, sum_m);
       }

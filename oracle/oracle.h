@@ -86,7 +86,8 @@ typedef struct {
   int64_t states;
   double optimum; /* min over schedules of sum_j d_j (seconds) */
 } oracle_opt_t;
-int oracle_optimum(int32_t n, const int32_t* I, const int32_t* O, int64_t C, int64_t M, const oracle_cost_t* cm,
+int oracle_optimum(int32_t n, const int32_t* I, const int32_t* O, int64_t C, int64_t M, int32_t no_preempt,
+                   const oracle_cost_t* cm,
                    oracle_opt_t* out);
 
 #ifdef __cplusplus

@@ -43,6 +43,8 @@ constexpr uint8_t F_MOVE_L = 64;  // SRF: an entry whose retention key moved rel
 
 struct LHead {
   sim_cost_model_t cm[SIM_MAX_COST];
+  int hist[18 * 18];  // SRF+Hist: log2 histogram of (I, O) at completions (Q31)
+  int pred[18];       // SRF+Hist: predicted output length per I bucket (recomputed after completions)
 };
 
 // Per-slot arrays (41 B per slot): in shared memory right after LHead, or (GM: workloads of n > 4096 requests, up
@@ -132,7 +134,8 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
   const bool finiteM = cfg.M >= 0, hybrid = cfg.hybrid != 0, chunked = cfg.chunked != 0;
   const int M = finiteM ? (int)cfg.M : 0, C = (int)cfg.C;  // host-validated <= 2^30
   const bool pfirst = cfg.order == SIM_ORDER_PREFILL_FIRST;  // {R_w, R_r} (never chunked here), else {R_r^d, R_r^p, R_w}
-  const bool srf = cfg.replacement == SIM_SRF;
+  const bool srf = cfg.replacement == SIM_SRF || cfg.replacement == SIM_SRF_HIST;  // SRF order (victims, visits)
+  const bool hist = cfg.replacement == SIM_SRF_HIST && finiteM;  // SRF+Hist deferral (Q31)
   const int rmode = cfg.reserve, Sctx = cfg.S;
   const long long max_steps = cfg.max_steps;
   const bool kv1 = rmode == SIM_RESERVE_SEQ;  // a decode needs one KV (else its PEAK / CONTEXT reserve covers it, Q39)
@@ -180,6 +183,9 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     }
   __syncwarp();
 
+  for (int i = lane; i < 18 * 18; i += 32) H.hist[i] = 0;
+  bool pred_dirty = true;  // SRF+Hist: the histogram changed since the predictions were made
+  __syncwarp();
   double clk = 0.0;  // lane k < K: the clock of cost model k
   int U = 0, seq = 0, next = 0, n_done = 0, nrun = 0, nW = 0;
   // the waiting group R_w as a bitmap: word w (32 slots) belongs to lane w % 32, row w / 32; per word the smallest
@@ -280,6 +286,24 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
 
     // ---- (2) a3-a8: GetNextBatch (steps 2-4) ----
     int tok = 0, n_new = 0, n_pb = 0, bph = -1, n_vic = 0;
+    int n_running = nrun;  // running requests (admissions in, victims out), for the SRF+Hist deferral
+    long long Rs = 0;      // SRF+Hist: sum of max(O_hat(I) - g, 0) over the running requests (Q31)
+    // SRF+Hist: the predictions of the current histogram and Rs over the running requests at run positions < end
+    auto hist_sum = [&](int end) {
+      if (pred_dirty) {
+        if (lane < 18) H.pred[lane] = hist_pred_row(H.hist, lane);
+        pred_dirty = false;
+        __syncwarp();
+      }
+      unsigned long long r = 0;
+      for (int q = lane; q < end; q += 32) {
+        const int sl = s_run[q];
+        const int4 rc = s_rec[sl];
+        const int g = is_dec(s_fl[sl]) ? rc.y + D : rc.y;
+        r += (unsigned)max(H.pred[bucket_of(rc.x)] - g, 0);
+      }
+      Rs = warp_sum_u51(r);
+    };
     int a = 0;          // decodes admitted: the heads at run positions < pa1
     int pa1 = 0;        // run position of head a+1 (or the end of the list)
     int cut = nrun;     // run positions >= cut were evicted this step
@@ -294,14 +318,19 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     // Returns the lanes admitted.
     auto admit_chunk = [&](bool waiting, int sl, const int4& rc, int avail, int dkv, bool alive) -> unsigned {
       const bool scand = waiting && !kv1;  // KV deltas differ from c under PEAK / CONTEXT: scan them too
+      const bool hw = hist && waiting;      // SRF+Hist deferral of a waiting candidate (Q31)
+      const int rem = hw && alive ? max(H.pred[bucket_of(rc.x)] - rc.y, 0) : 0;
+      const int sq = rc.x + rc.y;  // s
       bool admitted = false;
       for (;;) {
         const int rt = C - tok;
-        const bool fit = alive && rt >= 1 && (chunked || avail <= rt) && (!finiteM || U + dkv <= M);
+        const bool anyRun0 = n_running > 0;
+        bool fit = alive && rt >= 1 && (chunked || avail <= rt) && (!finiteM || U + dkv <= M);
+        if (hw) fit = fit && !(anyRun0 && (long long)U + Rs + sq + rem > M);  // deferred alone
         const unsigned fm = __ballot_sync(FM, fit);
         if (!fm) break;
-        const int cc = fit ? avail : 0, dk = fit ? dkv : 0;
-        int xc = cc, xd = dk;
+        const int cc = fit ? avail : 0, dk = fit ? dkv : 0, rr = fit ? rem : 0;
+        int xc = cc, xd = dk, xr = rr;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int yc = __shfl_up_sync(FM, xc, o);
@@ -310,8 +339,12 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
             const int yd = __shfl_up_sync(FM, xd, o);
             if (lane >= o) xd += yd;
           }
+          if (hw) {
+            const int yr = __shfl_up_sync(FM, xr, o);
+            if (lane >= o) xr += yr;
+          }
         }
-        const int ec = xc - cc, ek = __popc(fm & lt);
+        const int ec = xc - cc, ek = __popc(fm & lt), er = xr - rr;
         const int ed = waiting ? (scand ? xd - dk : ec) : 0;  // SEQ: a waiting admission reserves exactly c = s
         bool brk = false, crop = false;
         if (fit) {
@@ -321,6 +354,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
           else
             brk = avail > prt;
           if (finiteM) brk |= U + ed + dkv > M;
+          if (hw) brk |= (anyRun0 || ek > 0) && (long long)U + ed + Rs + er + sq + rem > M;  // deferred here
           if (crop && prt <= 0) brk = true;
         }
         const unsigned bm = __ballot_sync(FM, brk), cm = __ballot_sync(FM, crop && !brk);
@@ -346,16 +380,19 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         const int lastl = stop > 0 ? min(stop, 32) - 1 : 0;
         const int addc = stop > 0 ? __shfl_sync(FM, xc, lastl) : 0;
         const int addd = (scand && stop > 0) ? __shfl_sync(FM, xd, lastl) : addc;
-        int cropc = 0, crops = 0;
+        const int addr = (hw && stop > 0) ? __shfl_sync(FM, xr, lastl) : 0;
+        int cropc = 0, crops = 0, cropr = 0;
         if (cropped) {
           cropc = __shfl_sync(FM, rt - ec, cl);
           crops = __shfl_sync(FM, dkv, cl);
+          if (hw) cropr = __shfl_sync(FM, rem, cl);
         }
         const int nall = nadm + (cropped ? 1 : 0);
         tok += addc + cropc;
         if (waiting) {
           U += addd + crops;
-          seq += nall, n_new += nall;
+          seq += nall, n_new += nall, n_running += nall;
+          Rs += addr + cropr;
         } else {
           n_pb += nall;
         }
@@ -600,12 +637,19 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     };
 
     if (pfirst) {  // vLLM {R_w, R_r}: every running request is a decode (no chunking)
-      if (nW > 0) wait_scan();
+      if (nW > 0) {
+        if (hist) hist_sum(nrun);
+        wait_scan();
+      }
       if (n_rd > 0 && (hybrid || bph != PH_PRE)) decode_group();  // else every decode fails step 2
     } else {  // Sarathi {R_r^d, R_r^p, R_w}
       if (n_rd > 0) decode_group();
       if (cut > n_rd) run_prefills(cut);  // running prefills survive (the run list holds cut entries)
-      if (nW > 0) wait_scan();
+      if (nW > 0) {
+        n_running = cut;  // (this step's victims are waiting)
+        if (hist) hist_sum(cut);
+        wait_scan();
+      }
     }
     __syncwarp();
 
@@ -695,6 +739,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
               freed += max(rc.w, m);
               ndone++;
               out = make_int4(rc.x, g, m, rc.w);
+              if (hist) atomicAdd(&H.hist[bucket_of(rc.x) * 18 + bucket_of(O)], 1);
             } else {  // the (re)fill completed: a running decode from now on, in epoch form
               nfa++;
               out = make_int4(rc.x, g - D, m - D, rc.w);
@@ -750,6 +795,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
               so += rc.z + D;
               nd2++;
               evc = 2;
+              if (hist) atomicAdd(&H.hist[bucket_of(rc.x) * 18 + bucket_of(O)], 1);
             } else {
               dm = min(dm, ce);
             }
@@ -916,6 +962,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
                 fr2 += max(rc.w, rc.z + D);
                 so += rc.z + D;
                 nd2++;
+                if (hist) atomicAdd(&H.hist[bucket_of(rc.x) * 18 + bucket_of(O)], 1);
                 td[sl] = c0;
                 if (K > 1) td[n + sl] = c1;
                 if (K > 2) td[2 * (long long)n + sl] = c2_;
@@ -936,6 +983,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       }
     }
 
+    if (hist && ndone > 0) pred_dirty = true;  // (warp-uniform: the histogram gained this step's completions)
     // ---- (5) the run list for the next step (retention order) ----
     {
       int cnt = cut;  // the evicted suffix is cut off

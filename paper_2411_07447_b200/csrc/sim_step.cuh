@@ -936,7 +936,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
                               (chunked ? tok >= C : minSW > C - tok);
             const long long q1 = max(minSW, 1);  // at most 128 admissions possible (no 64-bit division)
             const bool few = (chunked ? (long long)(C - tok) <= 128 : (long long)(C - tok) < 129 * q1) ||
-                             (finiteM && (long long)(M - U) < 129 * q1);
+                             (finiteM && (long long)(M - U) < 129 * (long long)blk((int)q1));  // (KV in blocks when paged)
             if (wrej) {
               wdone = 1;
             } else if (few || nx1 - lo <= WARP_MAX) {
@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             // at most 128 admissions possible (floor(x / q) <= 128 <=> x < 129 q): warp-level admission
             const long long q1 = max(minSW, 1);
             const bool few = (chunked ? (long long)(C - tok) <= 128 : (long long)(C - tok) < 129 * q1) ||
-                             (finiteM && (long long)(M - U) < 129 * q1);
+                             (finiteM && (long long)(M - U) < 129 * (long long)blk((int)q1));  // (KV in blocks when paged)
             if (few || nx1 - lo <= WARP_MAX) mode = 2, lim = wend;
           }
         } else if (!rank) {

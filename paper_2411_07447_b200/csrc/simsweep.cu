@@ -66,8 +66,10 @@ constexpr int N_GENERAL = 2 * N_SIZES;
 // Sarathi presets (prefill-first without chunking, or decode-first), NRF / SRF / PF, no knob, no SRF+Hist, no trace
 constexpr int V_LEAN = N_GENERAL;  // + 0: n <= 1024, + 1: n <= 4096 (state in shared memory), + 2: n <= 32768 (arena)
 constexpr int N_VARIANTS = N_GENERAL + 3;
+// (n > 4096 with M infinite: every arrival is admitted at once, so the run list is as long as the window and the
+// O(|R_r|) passes of completions and SRF merges dominate; the block kernel spreads them over 512 threads)
 __host__ __device__ inline bool lean_ok(const sim_config_t& c, int n) {
-  return !has_knobs(c) && c.replacement != SIM_SRF_HIST && n <= SIM_MAX_WINDOW &&
+  return !has_knobs(c) && n <= SIM_MAX_WINDOW && (n <= 4096 || c.M >= 0) &&
          ((c.order == SIM_ORDER_PREFILL_FIRST && !c.chunked) || c.order == SIM_ORDER_DECODE_FIRST);
 }
 __host__ __device__ inline int kernel_variant(const sim_config_t& c, int n, int lean) {
@@ -721,32 +723,55 @@ int sim_optimum(const sim_opt_problem_t* probs, int32_t n_probs, const sim_cost_
                 int32_t device) {
   if (!probs || !out || n_probs <= 0) return SIM_EINVAL;
   if (int rc = validate_cms(cm, 1)) return rc;
-  constexpr long long MAX_STATES = 1ll << 25;
+  constexpr long long MAX_STATES = 1ll << 28;  // canonical states: 8 B of distance + 2 flags each (2.5 GB)
   std::vector<OptDev> P(n_probs);
-  std::vector<long long> nst(n_probs);
+  std::vector<long long> nst(n_probs), start_of(n_probs);
   long long cap = 0;
   for (int q = 0; q < n_probs; q++) {
     const sim_opt_problem_t& pr = probs[q];
     if (pr.n < 1 || pr.n > OPT_MAXN || pr.C < 1 || pr.M < 0) return SIM_EINVAL;
     OptDev& d = P[q];
     memset(&d, 0, sizeof(d));
-    d.n = pr.n, d.C = pr.C, d.M = pr.M;
-    long long total = 1;
+    if (pr.flags & ~SIM_OPT_NO_PREEMPT) return SIM_EINVAL;
+    d.n = pr.n, d.C = pr.C, d.M = pr.M, d.nopre = (pr.flags & SIM_OPT_NO_PREEMPT) ? 1 : 0;
+    // requests sorted by (I, O) so that identical ones are adjacent (a group); the optimum does not depend on the
+    // order of the requests
+    std::vector<std::pair<int, int>> req;
     for (int i = 0; i < pr.n; i++) {
       if (pr.I[i] < 1 || pr.O[i] < 1 || pr.O[i] > OPT_MAXO || pr.I[i] > (1 << 20)) return SIM_EINVAL;
-      d.I[i] = pr.I[i], d.O[i] = pr.O[i];
+      req.push_back({pr.I[i], pr.O[i]});
+    }
+    std::sort(req.begin(), req.end());
+    for (int i = 0; i < pr.n; i++) {
+      d.I[i] = req[i].first, d.O[i] = req[i].second;
       long long b = 1;  // local id 0 = done; block g holds the I+g unfilled states (+ the filled one for g >= 1)
-      for (int g = 0; g < pr.O[i]; g++) {
-        d.base[i][g] = (int)b;
-        b += pr.I[i] + g + (g >= 1 ? 1 : 0);
+      for (int g = 0; g < d.O[i]; g++) {
+        d.base[i][g] = (int)std::min<long long>(b, MAX_STATES + 1);
+        b += d.I[i] + g + (g >= 1 ? 1 : 0);
         if (b > MAX_STATES) break;
       }
-      d.base[i][pr.O[i]] = (int)std::min<long long>(b, MAX_STATES + 1);
+      d.base[i][d.O[i]] = (int)std::min<long long>(b, MAX_STATES + 1);
       d.ns[i] = b;
-      d.stride[i] = total;
-      total = (total > MAX_STATES || b > MAX_STATES) ? MAX_STATES + 1 : total * b;
+    }
+    long long total = 1, start = 0;
+    for (int i = 0; i < pr.n;) {
+      int j = i;
+      while (j < pr.n && d.I[j] == d.I[i] && d.O[j] == d.O[i]) j++;
+      const int k = j - i, g = d.ng++;
+      d.gs[g] = i, d.gk[g] = k;
+      d.gstride[g] = total;
+      // radix: multisets of size k from ns local states, binom(ns + k - 1, k) (overflow-safe test first)
+      const long long ns = d.ns[i];
+      long long radix = ns > MAX_STATES ? MAX_STATES + 1 : 1;
+      for (int t = 0; t < k && radix <= MAX_STATES; t++) radix = radix * (ns + t) / (t + 1);
+      int ones[OPT_MAXN];
+      for (int t = 0; t < k; t++) ones[t] = 1;  // every request at (g = 0, m = 0): local id 1
+      if (total <= MAX_STATES && radix <= MAX_STATES) start += opt_rank(ones, k) * total;
+      total = (total > MAX_STATES || radix > MAX_STATES || total * radix > MAX_STATES) ? MAX_STATES + 1 : total * radix;
+      i = j;
     }
     nst[q] = total;
+    start_of[q] = start;
     if (total <= MAX_STATES) cap = std::max(cap, total);
   }
   int ndev = 0;
@@ -781,8 +806,7 @@ int sim_optimum(const sim_opt_problem_t* probs, int32_t n_probs, const sim_cost_
     const long long ns = nst[q];
     const int threads = 256, blocks = (int)std::min<long long>((ns + threads - 1) / threads, 148 * 16);
     opt_fill_kernel<<<blocks, threads>>>(dist, cur, nxt, ns);
-    long long start = 0;
-    for (int i = 0; i < d.n; i++) start += d.stride[i];  // every request at (g = 0, m = 0): local id 1
+    const long long start = start_of[q];
     const unsigned long long zero = 0ull;
     const unsigned char one = 1;
     const long long one_ll = 1;

@@ -76,7 +76,10 @@ SIM_OPT_MAX_N = 4
 
 class SimOptProblem(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("I", ctypes.c_int32 * SIM_OPT_MAX_N), ("O", ctypes.c_int32 * SIM_OPT_MAX_N),
-                ("pad", ctypes.c_int32), ("C", ctypes.c_int64), ("M", ctypes.c_int64)]
+                ("flags", ctypes.c_int32), ("C", ctypes.c_int64), ("M", ctypes.c_int64)]
+
+
+OPT_NO_PREEMPT = 1  # SIM_OPT_NO_PREEMPT: the optimum over preemption-free schedules
 
 
 class SimOptResult(ctypes.Structure):
@@ -514,10 +517,12 @@ def sim_operator_costs(cms, shapes, device: int = -1) -> np.ndarray:
 OPT_STATUS = {0: "ok", 1: "unreachable", 2: "too_large"}
 
 
-def sim_optimum(problems, cm: SimCostModel, device: int = -1):
-    """problems: [(I list, O list, C, M)] -> [(status, rounds, reachable states, optimum seconds)]."""
+def sim_optimum(problems, cm: SimCostModel, device: int = -1, no_preempt: bool = False):
+    """problems: [(I list, O list, C, M)] -> [(status, rounds, reachable states, optimum seconds)].
+    no_preempt: the optimum over preemption-free schedules."""
     arr = (SimOptProblem * len(problems))()
     for q, (I, O, C, M) in enumerate(problems):
+        arr[q].flags = OPT_NO_PREEMPT if no_preempt else 0
         assert 1 <= len(I) == len(O) <= SIM_OPT_MAX_N
         arr[q].n = len(I)
         for i, (a, b) in enumerate(zip(I, O)):

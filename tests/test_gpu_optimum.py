@@ -62,3 +62,36 @@ def test_paper_csp_shape_lower_bounds_every_preset():
         g = simsweep.sim_sweep(cfgs, [wl], [cm])
         ms = [float(g.results["makespan"][i][0]) for i in range(len(cfgs)) if g.status(i) == "ok"]
         assert ms and min(ms) >= opt
+
+
+@pytest.mark.parametrize("name", ["llama3-8b_a100_theoretical", "unit"])
+def test_preemption_free_optimum_bit_exact(name):
+    probs = random_problems(101 + len(name), k=30)
+    pc = simsweep.unit_cost(1.0) if name == "unit" else PCMS[name]
+    oc = o.unit_cost(1.0) if name == "unit" else OCMS[name]
+    got = simsweep.sim_optimum(probs, pc, no_preempt=True)
+    for (I, O, C, M), (st, _, states, opt) in zip(probs, got):
+        assert (st, states, opt) == o.optimum(I, O, C, M, oc, no_preempt=True), (I, O, C, M)
+
+
+def test_identical_requests_merged_on_the_gpu():
+    # four identical requests: one multiset per state (oracle pins: tests/test_oracle_optimum.py)
+    U = simsweep.unit_cost(1.0)
+    got = simsweep.sim_optimum([([1, 1], [1, 1], 4096, 10), ([2, 2], [1, 1], 4096, 10), ([3] * 4, [4] * 4, 4096, 8)], U)
+    assert [(g[0], g[2], g[3]) for g in got[:2]] == [("ok", 3, 1.0), ("ok", 6, 1.0)]
+    assert got[2][:1] == ("ok",) and (got[2][2], got[2][3]) == o.optimum([3] * 4, [4] * 4, 4096, 8, o.unit_cost(1.0))[1:]
+
+
+def test_paper_csp_shape_preemption_free():
+    """PAPER.md:454-467 (O = W = 4, M = max(2I, I + O - 1), A100 8B theoretical): the exact optimum and the optimum
+    over preemption-free schedules (identical requests merged: I = 16 has at most 1.4e6 canonical states against 3.0e7
+    ordered ones).  The optimum never exceeds the preemption-free one nor any simulated preset."""
+    cm = PCMS["llama3-8b_a100_theoretical"]
+    for I in (4, 8, 16):
+        M = max(2 * I, I + 3)
+        (st, _, states, opt), = simsweep.sim_optimum([([I] * 4, [4] * 4, 4096, M)], cm)
+        (st2, _, _, free), = simsweep.sim_optimum([([I] * 4, [4] * 4, 4096, M)], cm, no_preempt=True)
+        assert st == st2 == "ok" and opt <= free
+        g = simsweep.sim_sweep([simsweep.preset_config(n + p, M) for n in presets.GRID_PRESETS for p in ("", "-srf", "-pf")],
+                               [workloads.fixed(I, 4, 4)], [cm])
+        assert min(float(g.results["makespan"][i][0]) for i in range(len(g.results)) if g.status(i) == "ok") >= opt

@@ -83,3 +83,50 @@ def test_no_preset_beats_the_optimum(seed):
                     r = o.run(cfg, I, O, np.zeros(W), cm)
                     if r.status == "ok":
                         assert opt <= float(r.makespan[0]), (order, chunked, hybrid, repl)
+
+
+def test_identical_requests_are_merged():
+    # identical requests are interchangeable (a permutation of them maps every schedule to one of the same cost),
+    # so the search stores a state once per multiset of their local states.  By hand, unit cost, ample C and M:
+    #  two (I=1, O=1): {both waiting, one done, both done} = 3 states; one batch serves both.
+    #  three (I=1, O=1): 4 states (0..3 done).
+    #  two (I=2, O=1): local states {done, m=0, m=1} -> every multiset of size 2 of them is reachable from (0, 0)
+    #  by some batch: binom(3 + 1, 2) = 6 states; one batch (c = 2 each) serves both.
+    assert o.optimum([1, 1], [1, 1], 4096, 10, UNIT) == ("ok", 3, 1.0)
+    assert o.optimum([1, 1, 1], [1, 1, 1], 4096, 10, UNIT) == ("ok", 4, 1.0)
+    assert o.optimum([2, 2], [1, 1], 4096, 10, UNIT) == ("ok", 6, 1.0)
+    # a mixed instance: the identical pair is merged, the third request is not
+    st, n3, _ = o.optimum([2, 2, 1], [1, 1, 1], 4096, 10, UNIT)
+    assert st == "ok" and n3 == 6 * 2  # (pair multisets) x (third request: waiting / done)
+
+
+def test_preemption_free_optimum():
+    # Example A without preemption (e = 0 always): r1, r2 = (2, 4), M = 6 -- both cannot run to their peak 5 + 5
+    # together, so one finishes first: 4 batches for r1 (prefill + 3 decodes) and 4 for r2 after it, or
+    # interleavings that never beat that: 8 ("preemption can be optimal": 6 < 8)
+    assert o.optimum([2, 2], [4, 4], 4096, 6, UNIT, no_preempt=True)[2] == 8.0
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_preemption_free_optimum_bounds(seed):
+    # the preemption-free optimum is >= the optimum (fewer schedules) and <= every PF preset (each PF schedule
+    # is a preemption-free schedule satisfying Eq. (4)-(7))
+    rng = np.random.default_rng(3000 + seed)
+    W = int(rng.integers(1, 4))
+    I = rng.integers(1, 4, size=W).astype(np.int32)
+    O = rng.integers(1, 4, size=W).astype(np.int32)
+    peak = int((I + O - 1).max())
+    M = int(rng.integers(peak, 2 * peak + 2))
+    C = int(rng.integers(1, int(I.sum()) + 2))
+    cm = [UNIT, CMS["llama3-8b_a100_linear"]][seed % 2]
+    _, _, opt = o.optimum(I, O, C, M, cm)
+    st, _, free = o.optimum(I, O, C, M, cm, no_preempt=True)
+    assert st == "ok" and opt <= free
+    for order in ("prefill_first", "decode_first"):
+        for chunked in (0, 1):
+            if not chunked and peak > C:
+                continue
+            cfg = o.make_config(order, 1, chunked, "pf", C=C, M=M, reserve="peak")
+            r = o.run(cfg, I, O, np.zeros(W), cm)
+            if r.status == "ok":
+                assert free <= float(r.makespan[0])
