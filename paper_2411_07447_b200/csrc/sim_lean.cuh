@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
   for (;;) {
     // ---- (1) a2: GetNewRequests (Alg. 1 line 3): all T <= clock, inclusive (Q21) ----
     int nx1 = next;
-    if (next < n && Tnext <= __shfl_sync(FM, clk, 0)) {
+    if (next < n && Tnext <= __shfl_sync(FM, clk, 0)) {  // (offline: next == n after the first step)
       const double clk0 = __shfl_sync(FM, clk, 0);
       for (;;) {
         const int idx = nx1 + lane;
@@ -623,9 +623,11 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         s_fl[sl] = ST_WAIT | F_PRE | (f & F_FIRST);
         s_vic[q - qs] = (int16_t)sl;
       }
-      fr = (int)__reduce_add_sync(FM, (unsigned)fr);
-      evd = (int)__reduce_add_sync(FM, (unsigned)evd);
-      mev = __reduce_add_sync(FM, mev);
+      if (qs < nrun) {
+        fr = (int)__reduce_add_sync(FM, (unsigned)fr);
+        evd = (int)__reduce_add_sync(FM, (unsigned)evd);
+        mev = __reduce_add_sync(FM, mev);
+      }
       n_vic = nrun - qs;
       n_rd -= evd;
       SMO -= (long long)mev - (long long)evd * D;
@@ -758,10 +760,13 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         n_ev += __popc(eb);
       }
     }
-    nfa = __reduce_add_sync(FM, nfa);
-    N = __reduce_add_sync(FM, N) + (unsigned)a;
-    np_ = __reduce_add_sync(FM, np_), cp = __reduce_add_sync(FM, cp), mp = __reduce_add_sync(FM, mp);
-    freed = __reduce_add_sync(FM, freed), ndone = __reduce_add_sync(FM, ndone);
+    if (n_pb + n_new > 0) {  // (a step of decodes only has nothing to reduce here)
+      nfa = __reduce_add_sync(FM, nfa);
+      N = __reduce_add_sync(FM, N);
+      np_ = __reduce_add_sync(FM, np_), cp = __reduce_add_sync(FM, cp), mp = __reduce_add_sync(FM, mp);
+      freed = __reduce_add_sync(FM, freed), ndone = __reduce_add_sync(FM, ndone);
+    }
+    N += (unsigned)a;
     moved = __any_sync(FM, moved);
     if (np_ > 0) {
       // (c, m < S < 2^18, at most CAP / 32 = 128 entries per lane: every per-lane sum is below 2^44)
@@ -837,7 +842,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     U -= (int)freed;
 
     // event times (first token, completion) under every cost model
-    {
+    if (n_ev > 0) {
       const double c0 = __shfl_sync(FM, clk, 0), c1 = __shfl_sync(FM, clk, 1), c2_ = __shfl_sync(FM, clk, 2),
                    c3 = __shfl_sync(FM, clk, 3);
       __syncwarp();
@@ -988,6 +993,28 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     {
       int cnt = cut;  // the evicted suffix is cut off
       int nmov = 0;   // SRF: entries whose keys moved, taken out into s_vic
+      auto key_of = [&](int sl) { return srf_key<SLB>(m_of(s_rec[sl], s_fl[sl]), s_seq[sl], sl); };
+      if (moved && ndone == 0) {
+        // the moved entries often stay in order (a chunk leaves a prefill behind the decodes): if each one is in
+        // order with both neighbours, the list is sorted (the others kept their relative order) and stays as is
+        bool ok = true;
+        for (int q0 = 0; q0 < cnt; q0 += 32) {
+          const int q = q0 + lane;
+          if (q < cnt) {
+            const int sl = s_run[q];
+            if (s_fl[sl] & F_MOVE_L) {
+              const unsigned long long k = key_of(sl);
+              if (q > 0 && key_of(s_run[q - 1]) >= k) ok = false;
+              if (q + 1 < cnt && key_of(s_run[q + 1]) <= k) ok = false;
+            }
+          }
+        }
+        if (__all_sync(FM, ok)) {
+          for (int q = lane; q < cnt; q += 32) s_fl[s_run[q]] &= ~F_MOVE_L;
+          moved = false;
+          __syncwarp();
+        }
+      }
       if (ndone > 0 || moved) {  // stable in-place compaction: drop completions (and take out the SRF movers)
         int w = 0;
         for (int q0 = 0; q0 < cnt; q0 += 32) {
@@ -1032,7 +1059,6 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       __syncwarp();
       if (nmov > 0) {  // SRF: merge the movers back into the (still sorted) kept list by (m desc, seq)
         const int nk = cnt;
-        auto key_of = [&](int sl) { return srf_key<SLB>(m_of(s_rec[sl], s_fl[sl]), s_seq[sl], sl); };
         bool merged = false;
         if (nmov <= 32) {
           unsigned long long mk = ~0ull;
