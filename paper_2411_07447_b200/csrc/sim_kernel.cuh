@@ -79,6 +79,8 @@ struct Scal {
   int cf_red[32][10];
   int pa, cut, h_pre, vmin, wstale, wfirst;
   int vt, status, any_pre, cur, wbuilt, arena;
+  int idle_st;       // status of an idle jump (not S.status: thread 0 rewrites that at the next loop top)
+  int wf_new, wf_vic;  // this step's new first waiting position / smallest victim index, committed at step end
   int w_dirty, p_dirty, r_dirty, o_dirty, rank_dirty, removals;
   long long r_Rs;  // scalars handed back by thread 0 after a break
   int r_tok, r_U, r_seq, r_new, r_running, r_bph, r_nB, r_wdone, r_wblk;
@@ -88,6 +90,14 @@ struct Scal {
   int hist[18 * 18];
   int pred[18];
 };
+
+// thread 0, at the end of a step: the first window position that may hold a waiting request.  Warp 0 finds it
+// during GetNextBatch (wf_new) while other warps may still read S.wfirst for this step, so it is staged and
+// committed here together with the step's victims (wf_vic), which wait from the next step on.
+__device__ __forceinline__ void wfirst_commit(Scal& S) {
+  S.wfirst = min(S.wf_new >= 0 ? S.wf_new : S.wfirst, S.wf_vic);
+  S.wf_new = -1, S.wf_vic = 0x7fffffff;
+}
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }

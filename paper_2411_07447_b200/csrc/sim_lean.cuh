@@ -104,6 +104,23 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
   const unsigned lt = (1u << lane) - 1u;
   const int ci = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
   if (kernel_variant(p.cfgs[ci], p.wls[p.cfgs[ci].workload].n, p.lean) != p.variant) return;
+#ifdef SIMSWEEP_PROFILE  // per-simulation start / end / SM (tools/timeline.py); not in the product build
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  struct ProfEnd {
+    int ci;
+    unsigned long long t0;
+    __device__ ~ProfEnd() {
+      if (threadIdx.x == 0 && ci < PROF_MAX_CFG) {
+        unsigned long long t1;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_prof[ci][14] = (long long)t0, g_prof[ci][15] = (long long)t1, g_prof[ci][9] = smid;
+      }
+    }
+  } prof_end{ci, t_start};
+#endif
   unsigned char* arr = smem;
   if constexpr (GM) {  // claim a per-CTA arena of the workspace (the stride of the block kernel's GM arenas)
     int a0 = 0;
@@ -462,6 +479,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
           int ms, md_;
           const unsigned left = wait_word(w, word, ms, md_);
           if (left != word) {  // admissions: the word and its group's summary change
+            __syncwarp();  // (every lane has read the words of this group)
             if (lane == 0) g_wb[w] = left, g_ws[w] = ms, g_wd[w] = md_;
             __syncwarp();
             const unsigned b2 = g_wb[wj];
@@ -1016,6 +1034,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         }
       }
       if (ndone > 0 || moved) {  // stable in-place compaction: drop completions (and take out the SRF movers)
+        __syncwarp();  // (the completion scans read s_run)
         int w = 0;
         for (int q0 = 0; q0 < cnt; q0 += 32) {
           const int q = q0 + lane;

@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     S.w_dirty = S.p_dirty = 1;
     S.wstale = 0;
     S.wfirst = 0;
+    S.wf_new = -1, S.wf_vic = 0x7fffffff, S.idle_st = 0;
   }
   if (tid < K) S.cm[tid] = p.cms[cfg.cost[tid]];
   for (int i = tid; i < 18 * 18; i += NT) S.hist[i] = 0;
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       S.h_pre = 0;
       S.cut = nrun;
       S.n_vic = 0;
-      S.nrank = nrank;
+      if (nrank != S.nrank) S.nrank = nrank;  // (changed only after the rank helpers' barriers)
       S.visits += nP;
     }
     PROF_MARK(1);
@@ -803,10 +804,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           if (wcont) wnext = min(i0 + 32, b1);
           continue;
         }
-        const int4 rc = s_rec[sl < 0 ? 0 : sl];
-        const uint8_t fl = s_fl[sl < 0 ? 0 : sl];
+        const int4 rc = sl >= 0 ? s_rec[sl] : make_int4(0, 0, 0, 0);  // (no dummy loads: lanes of one warp write)
+        const uint8_t fl = sl >= 0 ? s_fl[sl] : (uint8_t)0;
         const int s = rc.x + rc.y, avail = s - rc.z;
-        const int rtok = overWin ? rnew(rc, sl < 0 ? 0 : sl) : 0;  // the initial reserve >= s >= c (Q13), tokens
+        const int rtok = (overWin && sl >= 0) ? rnew(rc, sl) : 0;  // the initial reserve >= s >= c (Q13), tokens
         const int dkv = blk(rtok);                                   // its KV delta (blocks when paged)
         const int rem = (hist && overWin) ? max(S.pred[bucket_of(rc.x)] - rc.y, 0) : 0;
         bool alive = sl >= 0, admitted = false;
@@ -945,7 +946,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             }
           }
           if (lane == 0) {
-            if (wnext >= 0) S.wfirst = lo + wnext;
+            if (wnext >= 0) S.wf_new = lo + wnext;
             S.r_tok = tok, S.r_U = U, S.r_seq = seq, S.r_Rs = Rs, S.r_nB = nB;
             S.r_new = n_new, S.r_running = n_running, S.r_bph = bph, S.r_wdone = wdone, S.r_wblk = wblk;
           }
@@ -993,7 +994,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
             if (lane == 0) {
               S.r_tok = tok, S.r_U = U, S.r_seq = seq, S.r_Rs = Rs, S.r_nB = nB;
               S.r_new = n_new, S.r_running = n_running, S.r_bph = bph, S.r_wblk = wblk;
-              if (wnext >= 0) S.wfirst = lo + wnext;
+              if (wnext >= 0) S.wf_new = lo + wnext;
             }
           }
           TMARK(65);
@@ -1176,8 +1177,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
     TMARK(21);
     if (tok == 0) {   // B = {}: idle jump to the next arrival, not a step (Q21)
       if (tid == 0) {
+        wfirst_commit(S);
+        S.idle_st = 0;
         if (S.any_pre)
-          S.status = SIM_S_DEADLOCK;
+          S.idle_st = SIM_S_DEADLOCK;
         else if (nx1 < n) {
           S.clock[0] = fmax(S.clock[0], wl.T[nx1]);
           S.idle++;
@@ -1187,10 +1190,10 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           S.rank_dirty = 0;
           S.p_dirty = 0;
         } else
-          S.status = SIM_S_DEADLOCK;
+          S.idle_st = SIM_S_DEADLOCK;
       }
       __syncthreads();
-      exit_status = S.status;
+      exit_status = S.idle_st;
       if (exit_status) break;
       continue;
     }
@@ -1306,7 +1309,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         vidx = (int)__reduce_min_sync(FM, (unsigned)vidx);
         if (lane == 0) {
           S.vmin = vmin;
-          S.wfirst = min(S.wfirst, vidx);  // this step's victims wait from the next step on
+          S.wf_vic = min(S.wf_vic, vidx);  // this step's victims wait from the next step on
         }
       }
       __syncthreads();
@@ -1573,7 +1576,9 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
       TMARK(51);
       if (moved)
         for (int q = tid; q < cnt; q += NT) s_rpos[rl[q]] = (int16_t)q;
+      __syncwarp();  // (warp 0's lanes read S.n_ev for the event pass without a barrier since)
       if (tid == 0) {
+        wfirst_commit(S);
         S.n_run = cnt;
         S.next = nx1;
         S.n_ev = 0;

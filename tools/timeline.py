@@ -1,5 +1,5 @@
 """Per-simulation start/end timeline of one grid sweep (profiling build): is the sweep bound by its
-critical path or by aggregate work?   python tools/timeline.py"""
+critical path or by aggregate work?   python tools/timeline.py [--full] [out.npz]"""
 import ctypes, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -9,7 +9,9 @@ import numpy as np, torch
 from paper_2411_07447_b200 import simsweep, sweep
 L = simsweep.lib()
 L.sim_debug_read.argtypes = [ctypes.c_void_p, ctypes.c_int32]
-cfgs, wls, cms, labels = sweep.grid_sweep()
+full = "--full" in sys.argv
+sys.argv = [a for a in sys.argv if a != "--full"]
+cfgs, wls, cms, labels = sweep.full_sweep() if full else sweep.grid_sweep()
 order = sweep.partition_lpt(sweep.estimate(cfgs, wls), 1)[0]
 ds = simsweep.DeviceSweep(cfgs, wls, cms, order=np.asarray(order, np.int32))
 ds.launch(); torch.cuda.synchronize(); ds.launch(); torch.cuda.synchronize()
@@ -36,7 +38,10 @@ est = sweep.estimate(cfgs, wls)
 rank = {c: r for r, c in enumerate(order)}
 for i in idx:
     print(f"  {labels[i]!s:32s} {st[i]:7.2f} {du[i]:7.2f} {en[i]:7.2f} {int(res['steps'][i]):7d} {rank[i]:5d} {est[i]:9.0f}")
-hist = np.histogram(st, bins=[0, 1, 5, 10, 20, 40, 80])[0]
-print("start-time histogram [0,1,5,10,20,40,80] ms:", hist)
+bins = [0, 1, 5, 10, 20, 40, 80, 160, 320, 640, 1280]
+print(f"start-time histogram {bins} ms:", np.histogram(st, bins=bins)[0])
+print("longest-duration simulations:  label  start  duration  end  steps  launch-rank  est")
+for i in np.argsort(-du)[:25]:
+    print(f"  {labels[i]!s:32s} {st[i]:7.2f} {du[i]:7.2f} {en[i]:7.2f} {int(res['steps'][i]):7d} {rank[i]:5d} {est[i]:9.0f}")
 if len(sys.argv) > 1:  # save per-simulation start/duration/steps for offline comparison
     np.savez(sys.argv[1], st=st, du=du, steps=np.asarray(res["steps"]), labels=np.asarray([str(l) for l in labels]))
