@@ -141,6 +141,66 @@ __device__ double batch_time(const sim_cost_model_t& cm, const Feat& f, int k) {
   return dmul(i2d(cm.layers), t);
 }
 
+// The same d_j evaluated by a whole warp (lean kernel): lane 8k + j computes term j of model k's Eq. (3) sum (j < 4:
+// the matmuls, 4: prefill attention, 5: decode attention, 6: the All_Reduce time), two divisions per lane instead of
+// up to fourteen on one lane; lane k < K then adds its model's terms in the order of batch_time above (the same
+// dadd sequence, so the same bits) or evaluates its linear model.  Every lane passes the same features; pceil[k] is
+// model k's.  Returns d_j of model `lane` in lanes < K (0 elsewhere).  Warp-collective.
+__device__ __forceinline__ double batch_time_warp(const sim_cost_model_t* cms, int K, const Feat& f, bool anyTheo) {
+  const int lane = threadIdx.x & 31;
+  double term = 0.0;
+  if (anyTheo) {
+    const int k = lane >> 3, j = lane & 7;
+    if (k < K && j < 7 && cms[k].mode == 1) {
+      const sim_cost_model_t& cm = cms[k];
+      const long long h = cm.h, ff = cm.f, H = cm.H, NQ = cm.NQ, NKV = cm.NKV, N = f.N;
+      const long long qo = (NQ + 2 * NKV) * H, ao = NQ * H;
+      const long long s1m = f.md + f.nd;
+      const long long pce = k == 0 ? f.pceil[0] : (k == 1 ? f.pceil[1] : (k == 2 ? f.pceil[2] : f.pceil[3]));
+      // branch-free selection of the term's FLOPs F and elements R (exact integers, any association)
+      const long long a_in = j == 0 ? h : (j == 1 ? ao : (j == 2 ? h : ff));
+      const long long a_out = j == 0 ? qo : (j == 1 ? h : (j == 2 ? 2 * ff : h));
+      const long long A = j == 4 ? f.pcm : s1m, B = j == 4 ? f.cp : f.nd, Cc = j == 4 ? pce : s1m;
+      const long long F = j < 4 ? 2 * N * a_in * a_out
+                                : (j < 6 ? 4 * H * NQ * A : 2 * (long long)cm.e * N * h * (long long)(cm.tp - 1));
+      const long long R = j < 4 ? a_in * a_out + N * a_in + N * a_out : 2 * H * NQ * B + 2 * NQ * A + 2 * H * NKV * Cc;
+      // roof: fmax(F / flops, e R / bw); All_Reduce: (F / tp) / link_bw
+      const double q1 = ddiv(i2d(F), j == 6 ? i2d(cm.tp) : cm.flops);
+      const double q2 = ddiv(j == 6 ? q1 : i2d(R * (long long)cm.e), j == 6 ? cm.link_bw : cm.bw);
+      term = j == 6 ? q2 : fmax(q1, q2);
+    }
+  }
+  const int src = 8 * (lane < 4 ? lane : 0);
+  double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0, t4 = 0.0, t5 = 0.0, t6 = 0.0;
+  if (anyTheo) {
+    t0 = __shfl_sync(0xffffffffu, term, src), t1 = __shfl_sync(0xffffffffu, term, src + 1);
+    t2 = __shfl_sync(0xffffffffu, term, src + 2), t3 = __shfl_sync(0xffffffffu, term, src + 3);
+    t4 = __shfl_sync(0xffffffffu, term, src + 4), t5 = __shfl_sync(0xffffffffu, term, src + 5);
+    t6 = __shfl_sync(0xffffffffu, term, src + 6);
+  }
+  double d = 0.0;
+  if (lane < K) {
+    const sim_cost_model_t& cm = cms[lane];
+    if (cm.mode == 1) {
+      double t = 0.0;
+      t = dadd(t, t0);
+      t = dadd(t, t1);
+      t = dadd(t, t2);
+      t = dadd(t, t3);
+      if (f.np > 0) t = dadd(t, t4);
+      if (f.nd > 0) t = dadd(t, t5);
+      if (cm.tp > 1) {
+        t = dadd(t, t6);
+        t = dadd(t, t6);
+      }
+      d = dmul(i2d(cm.layers), t);
+    } else {
+      d = batch_time(cm, f, 0);
+    }
+  }
+  return d;
+}
+
 __device__ __forceinline__ int bucket_of(int x) {  // floor(log2 x), capped at 17
   int b = 31 - __clz(x);
   return b > 17 ? 17 : b;

@@ -347,18 +347,26 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         const unsigned fm = __ballot_sync(FM, fit);
         if (!fm) break;
         const int cc = fit ? avail : 0, dk = fit ? dkv : 0, rr = fit ? rem : 0;
-        int xc = cc, xd = dk, xr = rr;
+        int xc = cc, xd = dk, xr = rr;  // inclusive prefix sums over the lanes that fit alone
+        if ((fm & (fm - 1)) == 0) {       // one lane fits (the contended steps): its values from lane L on
+          const int L = __ffs(fm) - 1;
+          xc = __shfl_sync(FM, cc, L);
+          if (scand) xd = __shfl_sync(FM, dk, L);
+          if (hw) xr = __shfl_sync(FM, rr, L);
+          if (lane < L) xc = 0, xd = 0, xr = 0;
+        } else {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int yc = __shfl_up_sync(FM, xc, o);
-          if (lane >= o) xc += yc;
-          if (scand) {
-            const int yd = __shfl_up_sync(FM, xd, o);
-            if (lane >= o) xd += yd;
-          }
-          if (hw) {
-            const int yr = __shfl_up_sync(FM, xr, o);
-            if (lane >= o) xr += yr;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int yc = __shfl_up_sync(FM, xc, o);
+            if (lane >= o) xc += yc;
+            if (scand) {
+              const int yd = __shfl_up_sync(FM, xd, o);
+              if (lane >= o) xd += yd;
+            }
+            if (hw) {
+              const int yr = __shfl_up_sync(FM, xr, o);
+              if (lane >= o) xr += yr;
+            }
           }
         }
         const int ec = xc - cc, ek = __popc(fm & lt), er = xr - rr;
@@ -842,12 +850,13 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       n_rd += (int)nfa;
     }
     // a9: lane k < K charges cost model k; clock += d_j (one fp64 add, Q36)
-    if (lane < K) {
+    {
       Feat f;
       f.N = N, f.np = np_, f.cp = cp, f.mp = mp, f.nd = nd, f.md = md, f.c2 = c2, f.mc = mc, f.pcm = pcm;
-      f.pceil[0] = lane == 0 ? pce[0] : (lane == 1 ? pce[1] : (lane == 2 ? pce[2] : pce[3]));  // this lane's model
-      f.pceil[1] = f.pceil[2] = f.pceil[3] = 0;
-      clk = dadd(clk, batch_time(H.cm[lane], f, 0));
+#pragma unroll
+      for (int k = 0; k < SIM_MAX_COST; k++) f.pceil[k] = pce[k];
+      const double d = batch_time_warp(H.cm, K, f, anyTheo);  // lane-parallel Eq. (3) terms (same bits)
+      if (lane < K) clk = dadd(clk, d);
     }
     steps++;
     formed++;
@@ -1077,10 +1086,17 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       }
       __syncwarp();
       if (nmov > 0) {  // SRF: merge the movers back into the (still sorted) kept list by (m desc, seq)
+        // The movers are sorted on their own (in lanes when <= 32, else bitonic in s_key), each finds its insertion
+        // point ins_t = #{kept j : key_j < key_t} by binary search, and the kept list is shifted in place range by
+        // range from its end (range t = [ins_t, ins_t+1) moves by t + 1): O(nmov log nmov + entries moved / 32),
+        // never a sort of the whole list.
         const int nk = cnt;
-        bool merged = false;
-        if (nmov <= 32) {
-          unsigned long long mk = ~0ull;
+        const bool small = nmov <= 32;
+        unsigned long long mk = ~0ull;  // small: lane t holds mover t's key (sorted)
+        int ins = nk;                   // small: lane t holds ins_t
+        bool append;
+        const unsigned long long tail = nk > 0 ? key_of(s_run[nk - 1]) : 0ull;
+        if (small) {
           if (lane < nmov) mk = key_of(s_vic[lane]);
           if (nmov > 1) {  // bitonic sort of the first 2^ceil(log2 nmov) lanes' keys (the rest hold ~0)
             const int P2 = 1 << (32 - __clz(nmov - 1));
@@ -1092,44 +1108,25 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
               }
             }
           }
-          const unsigned long long tail = nk > 0 ? key_of(s_run[nk - 1]) : 0ull;
-          const unsigned long long mk0 = __shfl_sync(FM, mk, 0);
-          if (nk == 0 || mk0 > tail) {  // every mover goes after the kept tail: append in key order
+          append = nk == 0 || __shfl_sync(FM, mk, 0) > tail;
+          if (append) {
             if (lane < nmov) s_run[nk + lane] = (int16_t)(mk & (CAP - 1));
-          } else {  // ins_t = #{kept j : key_j < key_t} by binary search, then shift the kept entries
-            int ins = nk;
-            if (lane < nmov) {
-              int lo2 = 0, hi2 = nk;
-              while (lo2 < hi2) {
-                const int mid = (lo2 + hi2) >> 1;
-                if (key_of(s_run[mid]) < mk)
-                  lo2 = mid + 1;
-                else
-                  hi2 = mid;
-              }
-              ins = lo2;
+          } else if (lane < nmov) {
+            int lo2 = 0, hi2 = nk;
+            while (lo2 < hi2) {
+              const int mid = (lo2 + hi2) >> 1;
+              if (key_of(s_run[mid]) < mk)
+                lo2 = mid + 1;
+              else
+                hi2 = mid;
             }
-            for (int q0 = 0; q0 < nk; q0 += 32) {
-              const int q = q0 + lane;
-              int sh = 0;
-              for (int t = 0; t < nmov; t++) sh += __shfl_sync(FM, ins, t) <= q ? 1 : 0;
-              if (q < nk) s_run2[q + sh] = s_run[q];
-            }
-            if (lane < nmov) s_run2[ins + lane] = (int16_t)(mk & (CAP - 1));
-            __syncwarp();
-            int16_t* t = s_run;
-            s_run = s_run2;
-            s_run2 = t;
+            ins = lo2;
           }
-          merged = true;
-        }
-        if (!merged) {  // many movers (e.g. a large first admission): sort the whole list by key (bitonic)
-          const int tot = nk + nmov;
-          for (int q = lane; q < nk; q += 32) s_key[q] = key_of(s_run[q]);
-          for (int t = lane; t < nmov; t += 32) s_key[nk + t] = key_of(s_vic[t]);
+        } else {
+          for (int t = lane; t < nmov; t += 32) s_key[t] = key_of(s_vic[t]);
           int P2 = 1;
-          while (P2 < tot) P2 <<= 1;
-          for (int q = tot + lane; q < P2; q += 32) s_key[q] = ~0ull;
+          while (P2 < nmov) P2 <<= 1;
+          for (int t = nmov + lane; t < P2; t += 32) s_key[t] = ~0ull;
           __syncwarp();
           for (int k2 = 2; k2 <= P2; k2 <<= 1) {
             for (int j = k2 >> 1; j > 0; j >>= 1) {
@@ -1143,7 +1140,46 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
               __syncwarp();
             }
           }
-          for (int q = lane; q < tot; q += 32) s_run[q] = (int16_t)(s_key[q] & (CAP - 1));
+          append = nk == 0 || s_key[0] > tail;
+          for (int t = lane; t < nmov; t += 32) {
+            const unsigned long long kt = s_key[t];
+            if (append) {
+              s_run[nk + t] = (int16_t)(kt & (CAP - 1));
+            } else {
+              int lo2 = 0, hi2 = nk;
+              while (lo2 < hi2) {
+                const int mid = (lo2 + hi2) >> 1;
+                if (key_of(s_run[mid]) < kt)
+                  lo2 = mid + 1;
+                else
+                  hi2 = mid;
+              }
+              s_vic[t] = (int16_t)(kt & (CAP - 1));  // mover t in key order
+              s_run2[t] = (int16_t)lo2;              // its insertion point
+            }
+          }
+        }
+        __syncwarp();
+        if (!append) {
+          int hi = nk;
+          for (int t = nmov - 1; t >= 0; t--) {  // range t = [ins_t, hi) moves up by t + 1 (from its top down)
+            const int lo = small ? __shfl_sync(FM, ins, t) : (int)s_run2[t];
+            for (int top = hi; top > lo; top -= 32) {
+              const int q = top - 1 - lane;
+              const bool ok = q >= lo;
+              const int16_t v = ok ? s_run[q] : (int16_t)0;
+              __syncwarp();
+              if (ok) s_run[q + t + 1] = v;
+              __syncwarp();
+            }
+            hi = lo;
+          }
+          if (small) {
+            if (lane < nmov) s_run[ins + lane] = (int16_t)(mk & (CAP - 1));
+          } else {
+            for (int t = lane; t < nmov; t += 32) s_run[s_run2[t] + t] = s_vic[t];
+          }
+          __syncwarp();
         }
         cnt = nk + nmov;
       }

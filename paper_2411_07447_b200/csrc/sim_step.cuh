@@ -1327,6 +1327,16 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
         for (int z = 0; z < 19; z++) tt[z] = __shfl_sync(FM, v, z);
       }
       TMARK(34);
+      double dk[SIM_MAX_COST] = {0.0, 0.0, 0.0, 0.0};  // d_j per cost model (warp 0, lane-parallel Eq. (3) terms)
+      if (wid == 0) {
+        Feat f;
+        f.N = tt[0], f.np = tt[1], f.cp = tt[2], f.mp = tt[3], f.nd = tt[4], f.md = tt[5];
+        f.c2 = tt[11], f.mc = tt[12], f.pcm = tt[13];
+        f.pceil[0] = tt[14], f.pceil[1] = tt[15], f.pceil[2] = tt[16], f.pceil[3] = tt[17];
+        const double d = batch_time_warp(S.cm, K, f, anyTheo);
+#pragma unroll
+        for (int k = 0; k < SIM_MAX_COST; k++) dk[k] = __shfl_sync(FM, d, k);
+      }
       if (tid == 0) {
         const int vmin = S.vmin;
         {
@@ -1335,7 +1345,7 @@ __global__ void __launch_bounds__(NT, (CAP <= 1024 ? (NT <= 128 ? 3 : 512 / NT) 
           f.c2 = tt[11], f.mc = tt[12], f.pcm = tt[13];
           f.pceil[0] = tt[14], f.pceil[1] = tt[15], f.pceil[2] = tt[16], f.pceil[3] = tt[17];
           const double start = trc ? S.clock[0] : 0.0;
-          for (int k = 0; k < K; k++) S.clock[k] = dadd(S.clock[k], batch_time(S.cm[k], f, k));  // Q36
+          for (int k = 0; k < K; k++) S.clock[k] = dadd(S.clock[k], dk[k]);  // Q36
           if (trc) {  // (d_j under cost[0] evaluated again: the same expression, the same bits)
             if (S.steps < p.tr.cap_steps)
               p.tr.steps[S.steps] = sim_trace_step_t{S.steps, nB, S.n_vic, (long long)U, (long long)tok, start,

@@ -66,10 +66,11 @@ constexpr int N_GENERAL = 2 * N_SIZES;
 // Sarathi presets (prefill-first without chunking, or decode-first), NRF / SRF / PF, no knob, no SRF+Hist, no trace
 constexpr int V_LEAN = N_GENERAL;  // + 0: n <= 1024, + 1: n <= 4096 (state in shared memory), + 2: n <= 32768 (arena)
 constexpr int N_VARIANTS = N_GENERAL + 3;
-// (n > 4096 with M infinite: every arrival is admitted at once, so the run list is as long as the window and the
-// O(|R_r|) passes of completions and SRF merges dominate; the block kernel spreads them over 512 threads)
+// (n > 4096 with M infinite runs here too: its run list can be as long as the window, but the SRF merge shifts the
+// kept list range by range instead of sorting it, and a 512-thread block-kernel CTA holds a whole SM's register file
+// for the simulation's duration, 0.5-0.75 s for the 70B AzureConv runs of the north-star sweep)
 __host__ __device__ inline bool lean_ok(const sim_config_t& c, int n) {
-  return !has_knobs(c) && n <= SIM_MAX_WINDOW && (n <= 4096 || c.M >= 0) &&
+  return !has_knobs(c) && n <= SIM_MAX_WINDOW &&
          ((c.order == SIM_ORDER_PREFILL_FIRST && !c.chunked) || c.order == SIM_ORDER_DECODE_FIRST);
 }
 __host__ __device__ inline int kernel_variant(const sim_config_t& c, int n, int lean) {
@@ -237,6 +238,21 @@ static int validate_configs(const sim_config_t* cfgs, int32_t n_cfgs, const int3
   return 0;
 }
 
+// Shared-memory carveout preference of the global-arena variants (percent): small, so that L1 keeps their per-slot
+// arrays.  An SM's L1 / shared split cannot change while CTAs are resident, so the SMs that host an arena simulation
+// take no shared-memory-resident CTA until it ends; measured on the north-star sweep (tools/timeline.py --full):
+// 10 % -> 439 ms, 50 % -> 437 ms, 100 % -> 535 ms (the arena simulations slow down with a 28 KB L1).
+// SIMSWEEP_GM_CARVEOUT overrides (tools).
+static int arena_carveout() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SIMSWEEP_GM_CARVEOUT");
+    v = e ? atoi(e) : 10;
+    if (v < 0 || v > 100) v = 10;
+  }
+  return v;
+}
+
 static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, int32_t n_wls,
                         const sim_config_t* d_cfgs, const sim_workload_t* d_wls, const sim_cost_model_t* d_cms,
                         int32_t n_cms, const int32_t* d_order, const int64_t* d_row_off, const int64_t* d_tim_off,
@@ -298,7 +314,8 @@ static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_
         return SIM_ECUDA;
       // shared-memory resident state: the largest carveout, so that more CTAs fit per SM; the global-arena
       // variant keeps the carveout small and leaves the rest of the 256 KB to L1
-      cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout, V.arena ? 10 : 100);
+      cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           V.arena ? arena_carveout() : 100);
       g_attr_set[dev] |= 1u << v;
     }
     kp.variant = v;

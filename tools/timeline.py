@@ -38,6 +38,15 @@ est = sweep.estimate(cfgs, wls)
 rank = {c: r for r, c in enumerate(order)}
 for i in idx:
     print(f"  {labels[i]!s:32s} {st[i]:7.2f} {du[i]:7.2f} {en[i]:7.2f} {int(res['steps'][i]):7d} {rank[i]:5d} {est[i]:9.0f}")
+import collections
+cls = collections.Counter()
+for i in range(len(cfgs)):
+    lb = labels[i]
+    key = f"{lb[0]} {lb[1].split()[0]} {lb[1].split()[1] if lb[0] == 'online-70B' else ''} {lb[2].split()[0] if full else ''}"
+    cls[key] += du[i]
+print("sum of simulation durations by class (ms):")
+for k, v in cls.most_common(20):
+    print(f"  {k:70s} {v:10.1f}")
 bins = [0, 1, 5, 10, 20, 40, 80, 160, 320, 640, 1280]
 print(f"start-time histogram {bins} ms:", np.histogram(st, bins=bins)[0])
 print("longest-duration simulations:  label  start  duration  end  steps  launch-rank  est")
