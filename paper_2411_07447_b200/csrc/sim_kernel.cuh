@@ -164,10 +164,14 @@ __device__ __forceinline__ double batch_time_warp(const sim_cost_model_t* cms, i
       const long long F = j < 4 ? 2 * N * a_in * a_out
                                 : (j < 6 ? 4 * H * NQ * A : 2 * (long long)cm.e * N * h * (long long)(cm.tp - 1));
       const long long R = j < 4 ? a_in * a_out + N * a_in + N * a_out : 2 * H * NQ * B + 2 * NQ * A + 2 * H * NKV * Cc;
-      // roof: fmax(F / flops, e R / bw); All_Reduce: (F / tp) / link_bw
-      const double q1 = ddiv(i2d(F), j == 6 ? i2d(cm.tp) : cm.flops);
-      const double q2 = ddiv(j == 6 ? q1 : i2d(R * (long long)cm.e), j == 6 ? cm.link_bw : cm.bw);
-      term = j == 6 ? q2 : fmax(q1, q2);
+      // roof: fmax(F / flops, e R / bw); All_Reduce: (F / tp) / link_bw.  Only the terms batch_time adds are
+      // evaluated: a zero numerator would take the division's slow path (and the term is not summed anyway).
+      const bool used = j < 4 || (j == 4 && f.np > 0) || (j == 5 && f.nd > 0) || (j == 6 && cm.tp > 1);
+      if (used) {
+        const double q1 = ddiv(i2d(F), j == 6 ? i2d(cm.tp) : cm.flops);
+        const double q2 = ddiv(j == 6 ? q1 : i2d(R * (long long)cm.e), j == 6 ? cm.link_bw : cm.bw);
+        term = j == 6 ? q2 : fmax(q1, q2);
+      }
     }
   }
   const int src = 8 * (lane < 4 ? lane : 0);

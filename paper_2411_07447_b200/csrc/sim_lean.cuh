@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       Rs = warp_sum_u51(r);
     };
     int a = 0;          // decodes admitted: the heads at run positions < pa1
+    int pf0 = 0;        // run position of the front-most running prefill (set by run_prefills; movers lie at >= pf0)
     int pa1 = 0;        // run position of head a+1 (or the end of the list)
     int cut = nrun;     // run positions >= cut were evicted this step
     auto rnew = [&](const int4& rc, int sl) -> int {  // the reserve taken at (re)admission (Table 2, Q13, Q39)
@@ -431,7 +432,25 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
 
     // the running prefills at run positions [0, b1), in retention order (decode-first: R_r^p)
     auto run_prefills = [&](int b1) {
-      for (int i0 = 0; i0 < b1; i0 += 32) {
+      // [0, b1) holds n_rd decodes and b1 - n_rd running prefills (victims are cut off, completions compacted):
+      // find the front-most prefill from the tail (SRF / NRF keep the prefills in progress near the tail)
+      int p0 = 0;
+      {
+        const int need = b1 - n_rd;
+        int found = 0;
+        for (int top = b1 - 1; top >= 0; top -= 32) {
+          const int q = top - lane;
+          const bool c = q >= 0 ? (s_fl[s_run[q]] & (ST_MASK | F_PRE | F_FILLED)) == ST_RUN : false;
+          const unsigned bb = __ballot_sync(FM, c);
+          found += __popc(bb);
+          if (found >= need) {
+            if (bb) p0 = top - (31 - __clz(bb));
+            break;
+          }
+        }
+      }
+      pf0 = p0;
+      for (int i0 = p0; i0 < b1; i0 += 32) {
         if ((!hybrid && bph == PH_DEC) || (chunked && tok >= C)) return;  // every remaining candidate fails
         const int i = i0 + lane;
         int sl = 0;
@@ -545,89 +564,107 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         a = T;
         pa1 = pfirst ? T : nth_head(T + 1);  // prefill-first: every running request is a decode
       } else {
-        // walk from the tail: lane j <-> run position top - j; RSx = the holdings behind the chunk, HSi = its heads
-        // behind it; head i (i = k - #heads behind p_i) passes iff i <= T and F + RS(p_i + 1) >= i
-        int RSx = 0, HSi = 0, lastfail = nrun;
-        bool lastfail_t = false, found = false, kvstop = false;
-        a = 0;
-        for (int top = nrun - 1; top >= 0; top -= 32) {
-          const int q = top - lane;
-          int held = 0, head = 0;
-          if (q >= 0) {
-            const int sl = s_run[q];
-            const int4 rc = s_rec[sl];
-            head = is_dec(s_fl[sl]) ? 1 : 0;
-            held = max(rc.w, head ? rc.z + D : rc.z);
-          }
-          int xs = held, xh = head;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int ys = __shfl_up_sync(FM, xs, o), yh = __shfl_up_sync(FM, xh, o);
-            if (lane >= o) xs += ys, xh += yh;
-          }
-          const int rsx = RSx + xs - held, i = k - (HSi + xh) + 1;
-          const bool tfail = i > T, kfail = F + rsx < i;
-          const unsigned hb = __ballot_sync(FM, head);
-          const unsigned pb = __ballot_sync(FM, head && !tfail && !kfail);
-          if (pb) {  // the tail-most passing head is head a; head a+1 is the nearest failing head behind it
-            const int La = __ffs(pb) - 1;
-            a = __shfl_sync(FM, i, La);
-            const unsigned behind = hb & ((1u << La) - 1u);
-            if (behind) {
-              const int Lf = 31 - __clz(behind);
-              pa1 = top - Lf;
-              kvstop = __shfl_sync(FM, (int)tfail, Lf) == 0;
-            } else {
-              pa1 = lastfail;
-              kvstop = lastfail < nrun && !lastfail_t;
+        // one-victim fast path (the thrash steps): the last two run entries are decodes (heads k-1, k at positions
+        // nrun-2, nrun-1) and head k-1 passes (k-1 <= T, F + held(tail) >= k-1): a = k-1, head k fails (F < k, or
+        // k > T), and the minimal suffix is the tail alone (or empty if F >= a and the token budget stopped head k)
+        bool fast = false;
+        if (nrun >= 2) {
+          const int st = s_run[nrun - 1], s2 = s_run[nrun - 2];
+          if (is_dec(s_fl[st]) && is_dec(s_fl[s2]) && k - 1 <= T) {
+            const int4 rt = s_rec[st];
+            if (F + max(rt.w, rt.z + D) >= k - 1) {
+              a = k - 1;
+              pa1 = nrun - 1;
+              qs = (k <= T || F < a) ? nrun - 1 : nrun;  // (k <= T: head k stopped by the KV, self-preempts, Q8)
+              fast = true;
             }
-            if (top == nrun - 1 && F < a) {  // q* from the same registers: the tail-most q with F + RS(q) >= a
-              const unsigned qb = __ballot_sync(FM, q >= 0 && F + RSx + xs >= a);
-              if (qb) qs = top - (__ffs(qb) - 1);
-            }
-            found = true;
-            break;
           }
-          if (hb) {  // every head of this chunk fails; its front-most one has the lowest rank so far
-            const int Lf = 31 - __clz(hb);
-            lastfail = top - Lf;
-            lastfail_t = __shfl_sync(FM, (int)tfail, Lf) != 0;
-          }
-          RSx += __shfl_sync(FM, xs, 31);
-          HSi += __shfl_sync(FM, xh, 31);
         }
-        if (!found) {  // even head 1 fails
+        if (!fast) {
+          // walk from the tail: lane j <-> run position top - j; RSx = the holdings behind the chunk, HSi = its heads
+          // behind it; head i (i = k - #heads behind p_i) passes iff i <= T and F + RS(p_i + 1) >= i
+          int RSx = 0, HSi = 0, lastfail = nrun;
+          bool lastfail_t = false, found = false, kvstop = false;
           a = 0;
-          pa1 = lastfail;
-          kvstop = lastfail < nrun && !lastfail_t;
-        }
-        if (F < a && qs == nrun) {  // q* = the tail-most q with F + RS(q) >= a (walk the tail again)
-          int rs = 0;
           for (int top = nrun - 1; top >= 0; top -= 32) {
             const int q = top - lane;
-            int held = 0;
+            int held = 0, head = 0;
             if (q >= 0) {
               const int sl = s_run[q];
               const int4 rc = s_rec[sl];
-              held = max(rc.w, is_dec(s_fl[sl]) ? rc.z + D : rc.z);
+              head = is_dec(s_fl[sl]) ? 1 : 0;
+              held = max(rc.w, head ? rc.z + D : rc.z);
             }
-            int xs = held;
-#pragma unroll
+            int xs = held, xh = head;
+  #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-              const int ys = __shfl_up_sync(FM, xs, o);
-              if (lane >= o) xs += ys;
+              const int ys = __shfl_up_sync(FM, xs, o), yh = __shfl_up_sync(FM, xh, o);
+              if (lane >= o) xs += ys, xh += yh;
             }
-            const unsigned qb = __ballot_sync(FM, q >= 0 && F + rs + xs >= a);
-            if (qb) {
-              qs = top - (__ffs(qb) - 1);
+            const int rsx = RSx + xs - held, i = k - (HSi + xh) + 1;
+            const bool tfail = i > T, kfail = F + rsx < i;
+            const unsigned hb = __ballot_sync(FM, head);
+            const unsigned pb = __ballot_sync(FM, head && !tfail && !kfail);
+            if (pb) {  // the tail-most passing head is head a; head a+1 is the nearest failing head behind it
+              const int La = __ffs(pb) - 1;
+              a = __shfl_sync(FM, i, La);
+              const unsigned behind = hb & ((1u << La) - 1u);
+              if (behind) {
+                const int Lf = 31 - __clz(behind);
+                pa1 = top - Lf;
+                kvstop = __shfl_sync(FM, (int)tfail, Lf) == 0;
+              } else {
+                pa1 = lastfail;
+                kvstop = lastfail < nrun && !lastfail_t;
+              }
+              if (top == nrun - 1 && F < a) {  // q* from the same registers: the tail-most q with F + RS(q) >= a
+                const unsigned qb = __ballot_sync(FM, q >= 0 && F + RSx + xs >= a);
+                if (qb) qs = top - (__ffs(qb) - 1);
+              }
+              found = true;
               break;
             }
-            rs += __shfl_sync(FM, xs, 31);
+            if (hb) {  // every head of this chunk fails; its front-most one has the lowest rank so far
+              const int Lf = 31 - __clz(hb);
+              lastfail = top - Lf;
+              lastfail_t = __shfl_sync(FM, (int)tfail, Lf) != 0;
+            }
+            RSx += __shfl_sync(FM, xs, 31);
+            HSi += __shfl_sync(FM, xh, 31);
           }
+          if (!found) {  // even head 1 fails
+            a = 0;
+            pa1 = lastfail;
+            kvstop = lastfail < nrun && !lastfail_t;
+          }
+          if (F < a && qs == nrun) {  // q* = the tail-most q with F + RS(q) >= a (walk the tail again)
+            int rs = 0;
+            for (int top = nrun - 1; top >= 0; top -= 32) {
+              const int q = top - lane;
+              int held = 0;
+              if (q >= 0) {
+                const int sl = s_run[q];
+                const int4 rc = s_rec[sl];
+                held = max(rc.w, is_dec(s_fl[sl]) ? rc.z + D : rc.z);
+              }
+              int xs = held;
+  #pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int ys = __shfl_up_sync(FM, xs, o);
+                if (lane >= o) xs += ys;
+              }
+              const unsigned qb = __ballot_sync(FM, q >= 0 && F + rs + xs >= a);
+              if (qb) {
+                qs = top - (__ffs(qb) - 1);
+                break;
+              }
+              rs += __shfl_sync(FM, xs, 31);
+            }
+          }
+          // if the KV stopped the walk at head a+1 and it lies before q*, it evicts everything behind it and
+          // self-preempts (Q8): the suffix starts at pa1
+          if (kvstop && pa1 < qs) qs = pa1;
         }
-        // if the KV stopped the walk at head a+1 and it lies before q*, it evicts everything behind it and
-        // self-preempts (Q8): the suffix starts at pa1
-        if (kvstop && pa1 < qs) qs = pa1;
       }
       // apply: evict run positions [qs, nrun) (refill semantics P:1570)
       int fr = 0, evd = 0;
@@ -719,9 +756,9 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
     unsigned m_new = 0;  // sum of m over the new decodes
     // SRF: a running prefill left out of B but before pa1 is overtaken by the decodes after it (m + 1): it moves
     // too (the block kernel re-sorts whenever nd != |R_r|)
-    if (srf && !pfirst && a > 0 && pa1 > a) {
+    if (srf && !pfirst && a > 0 && pa1 > a && n_pb < cut - n_rd) {  // (some running prefill is not in B)
       bool mv = false;
-      for (int q = lane; q < pa1; q += 32) {
+      for (int q = pf0 + lane; q < pa1; q += 32) {
         const int sl = s_run[q];
         const uint8_t f = s_fl[sl];
         if ((f & (ST_MASK | F_FILLED | F_INB_L)) == ST_RUN) s_fl[sl] = f | F_MOVE_L, mv = true;
@@ -1025,7 +1062,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         // the moved entries often stay in order (a chunk leaves a prefill behind the decodes): if each one is in
         // order with both neighbours, the list is sorted (the others kept their relative order) and stays as is
         bool ok = true;
-        for (int q0 = 0; q0 < cnt; q0 += 32) {
+        for (int q0 = pf0; q0 < cnt; q0 += 32) {  // (every mover is a running prefill: at >= pf0)
           const int q = q0 + lane;
           if (q < cnt) {
             const int sl = s_run[q];
@@ -1037,15 +1074,16 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
           }
         }
         if (__all_sync(FM, ok)) {
-          for (int q = lane; q < cnt; q += 32) s_fl[s_run[q]] &= ~F_MOVE_L;
+          for (int q = pf0 + lane; q < cnt; q += 32) s_fl[s_run[q]] &= ~F_MOVE_L;
           moved = false;
           __syncwarp();
         }
       }
       if (ndone > 0 || moved) {  // stable in-place compaction: drop completions (and take out the SRF movers)
         __syncwarp();  // (the completion scans read s_run)
-        int w = 0;
-        for (int q0 = 0; q0 < cnt; q0 += 32) {
+        const int c0 = ndone > 0 ? 0 : pf0;  // without completions the entries before the first mover stay
+        int w = c0;
+        for (int q0 = c0; q0 < cnt; q0 += 32) {
           const int q = q0 + lane;
           int sl = 0;
           uint8_t f = 0;
