@@ -567,15 +567,25 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         // one-victim fast path (the thrash steps): the last two run entries are decodes (heads k-1, k at positions
         // nrun-2, nrun-1) and head k-1 passes (k-1 <= T, F + held(tail) >= k-1): a = k-1, head k fails (F < k, or
         // k > T), and the minimal suffix is the tail alone (or empty if F >= a and the token budget stopped head k)
+        // (Sarathi: a running prefill at the tail -- the chunk in progress, smallest m -- and head k before it: if
+        // k <= T and F + held(tail) >= k, every head passes, a = k, and the minimal suffix is the tail alone)
         bool fast = false;
         if (nrun >= 2) {
           const int st = s_run[nrun - 1], s2 = s_run[nrun - 2];
-          if (is_dec(s_fl[st]) && is_dec(s_fl[s2]) && k - 1 <= T) {
+          const uint8_t ft = s_fl[st];
+          if (is_dec(s_fl[s2])) {
             const int4 rt = s_rec[st];
-            if (F + max(rt.w, rt.z + D) >= k - 1) {
-              a = k - 1;
-              pa1 = nrun - 1;
-              qs = (k <= T || F < a) ? nrun - 1 : nrun;  // (k <= T: head k stopped by the KV, self-preempts, Q8)
+            if (is_dec(ft)) {
+              if (k - 1 <= T && F + max(rt.w, rt.z + D) >= k - 1) {
+                a = k - 1;
+                pa1 = nrun - 1;
+                qs = (k <= T || F < a) ? nrun - 1 : nrun;  // (k <= T: head k stopped by the KV, self-preempts, Q8)
+                fast = true;
+              }
+            } else if (k <= T && F + max(rt.w, rt.z) >= k) {
+              a = k;
+              pa1 = nrun;
+              qs = nrun - 1;  // (F < k = a: the suffix is not empty)
               fast = true;
             }
           }
