@@ -775,16 +775,16 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       }
       moved |= __any_sync(FM, mv);
     }
-    // the prefill entries: this batch's running prefills (s_run2) and admissions (s_new)
-    for (int sg = 0; sg < 2; sg++) {
-      const int16_t* list = sg == 0 ? s_run2 : s_new;
-      const int len = sg == 0 ? n_pb : n_new;
+    // the prefill entries: this batch's running prefills (s_run2) then its admissions (s_new), one index space
+    {
+      const int len = n_pb + n_new;
       for (int e0 = 0; e0 < len; e0 += 32) {
         const int e = e0 + lane;
+        const bool sg0 = e < n_pb;  // a running prefill (its retention key moves under SRF)
         unsigned evc = 0;
         int sl = 0;
         if (e < len) {
-          sl = list[e];
+          sl = sg0 ? s_run2[e] : s_new[e - n_pb];
           uint8_t fl = s_fl[sl];
           const int4 rc = s_rec[sl];
           const int O = s_O[sl];
@@ -820,9 +820,9 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
               out = make_int4(rc.x, g - D, m - D, rc.w);
               m_new += m;
               dm_new = min(dm_new, O - (g - D));
-              if (srf && sg == 0) fl |= F_MOVE_L, moved = true;
+              if (srf && sg0) fl |= F_MOVE_L, moved = true;
             }
-          } else if (srf && sg == 0) {
+          } else if (srf && sg0) {
             fl |= F_MOVE_L, moved = true;  // a chunk: its key moved (the admissions are merged anyway)
           }
           s_rec[sl] = out;

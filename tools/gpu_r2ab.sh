@@ -1,0 +1,6 @@
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 300 > gpurun_out/r2ab_gputests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r2ab_gputests.log
+timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/r2ab_bench_grid.json 2> gpurun_out/r2ab_bench_grid.err
+SIMSWEEP_LEAN_SPEC=0 timeout 600 python bench.py --no-cpu-baseline --no-e2e --no-critical > gpurun_out/r2ab_bench_grid_nospec.json 2>&1
+timeout 900 python bench.py --workload full --steps 3 --no-cpu-baseline --no-e2e > gpurun_out/r2ab_bench_full.json 2> gpurun_out/r2ab_bench_full.err
+timeout 600 python tools/timeline.py > gpurun_out/r2ab_timeline_grid.txt 2>&1
+timeout 900 python tools/timeline.py --full > gpurun_out/r2ab_timeline_full.txt 2>&1
