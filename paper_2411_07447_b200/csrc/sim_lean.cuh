@@ -347,15 +347,39 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         if (hw) fit = fit && !(anyRun0 && (long long)U + Rs + sq + rem > M);  // deferred alone
         const unsigned fm = __ballot_sync(FM, fit);
         if (!fm) break;
+        if ((fm & (fm - 1)) == 0) {  // one lane L fits alone (the contended steps): nothing can break it --
+          // it is admitted whole, or cropped to the budget left (chunked); then no other lane fits (U, tok only
+          // grew), which ends the pass exactly as the general round below would
+          const int L = __ffs(fm) - 1;
+          const int av = __shfl_sync(FM, avail, L), dk1 = __shfl_sync(FM, dkv, L);
+          const int c1 = (chunked && av > rt) ? rt : av;
+          if (lane == L) {
+            s_c[sl] = c1;
+            if (waiting) {
+              s_seq[sl] = seq + 1;
+              s_rec[sl] = make_int4(rc.x, rc.y, 0, dkv);
+              s_fl[sl] = ST_RUN | (s_fl[sl] & F_FIRST);
+              s_new[n_new] = (int16_t)sl;
+            } else {
+              s_fl[sl] |= F_INB_L;
+              s_run2[n_pb] = (int16_t)sl;
+            }
+            admitted = true;
+          }
+          tok += c1;
+          if (waiting) {
+            U += dk1;  // (SEQ: the reserve is s = c; PEAK / CONTEXT: the initial reserve; cropped: the reserve too)
+            seq++, n_new++, n_running++;
+            if (hw) Rs += __shfl_sync(FM, rem, L);
+          } else {
+            n_pb++;
+          }
+          if (bph < 0) bph = PH_PRE;
+          break;
+        }
         const int cc = fit ? avail : 0, dk = fit ? dkv : 0, rr = fit ? rem : 0;
         int xc = cc, xd = dk, xr = rr;  // inclusive prefix sums over the lanes that fit alone
-        if ((fm & (fm - 1)) == 0) {       // one lane fits (the contended steps): its values from lane L on
-          const int L = __ffs(fm) - 1;
-          xc = __shfl_sync(FM, cc, L);
-          if (scand) xd = __shfl_sync(FM, dk, L);
-          if (hw) xr = __shfl_sync(FM, rr, L);
-          if (lane < L) xc = 0, xd = 0, xr = 0;
-        } else {
+        {
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const int yc = __shfl_up_sync(FM, xc, o);
