@@ -347,11 +347,14 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
         if (hw) fit = fit && !(anyRun0 && (long long)U + Rs + sq + rem > M);  // deferred alone
         const unsigned fm = __ballot_sync(FM, fit);
         if (!fm) break;
-        if ((fm & (fm - 1)) == 0) {  // one lane L fits alone (the contended steps): nothing can break it --
-          // it is admitted whole, or cropped to the budget left (chunked); then no other lane fits (U, tok only
-          // grew), which ends the pass exactly as the general round below would
-          const int L = __ffs(fm) - 1;
-          const int av = __shfl_sync(FM, avail, L), dk1 = __shfl_sync(FM, dkv, L);
+        const int L = __ffs(fm) - 1;
+        const int av = __shfl_sync(FM, avail, L);
+        if ((fm & (fm - 1)) == 0 || av >= rt) {
+          // one lane L fits alone (the contended steps), or the first fitting lane takes the whole budget left:
+          // nothing can break L (no earlier lane is admitted in this round) -- it is admitted whole, or cropped to
+          // the budget (chunked); then no other lane can be admitted (U, tok only grew; or no token is left),
+          // which ends the pass exactly as the general round below would
+          const int dk1 = __shfl_sync(FM, dkv, L);
           const int c1 = (chunked && av > rt) ? rt : av;
           if (lane == L) {
             s_c[sl] = c1;
