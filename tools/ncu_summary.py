@@ -27,7 +27,7 @@ want = {
     "sm_cycles_elapsed_avg": ("sm__cycles_elapsed.avg", 1),
     "smem_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 1),
 }
-out = {"round": 1, "tag": tag, "kernel": get.get("Kernel Name", "?"), "command": cmd,
+out = {"round": 2, "tag": tag, "kernel": get.get("Kernel Name", "?"), "command": cmd,
        "capture": "ncu --set full --clock-control none --import-source on -k regex:sim_ -s 1 -c 1"}
 for k, (m, sc) in want.items():
     try:
