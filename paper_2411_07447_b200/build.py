@@ -8,7 +8,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "simsweep.cu")]
-HDRS = [os.path.join(PKG, "csrc", h) for h in ("sim_kernel.cuh", "sim_step.cuh", "sim_analytics.cuh", "sim_optimum.cuh")]
+HDRS = [os.path.join(PKG, "csrc", h) for h in ("sim_kernel.cuh", "sim_step.cuh", "sim_lean.cuh", "sim_analytics.cuh", "sim_optimum.cuh")]
 DEPS = SRC + HDRS + [os.path.join(ROOT, "include", "simsweep.h")]
 LIB = os.path.join(PKG, "libsimsweep.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -205,6 +205,129 @@ __device__ __forceinline__ double batch_time_warp(const sim_cost_model_t* cms, i
   return d;
 }
 
+// a / b rounded to nearest for a divisor b fixed per simulation, with y = RN(1/b) precomputed (__drcp_rn): q = RN(a y)
+// and two residual corrections q <- RN(q + RN(a - b q) y), the residual from one FMA.  After the first correction q is
+// within one ulp of a / b; the second is then Markstein's theorem (y within half an ulp of 1/b, q within one ulp of
+// a / b => RN(q + (a - b q) y) = RN(a / b)), so the bits are __ddiv_rn's for the operands used here (a = 0 or an
+// integer-valued double, b > 0 normal, normal quotient; tools/check_cdiv.c checks 128 M quotients).  Five dependent
+// fp64 operations, no reciprocal iteration, no range check, no slow path.
+__device__ __forceinline__ double cdiv(double a, double b, double y) {
+  double q = __dmul_rn(a, y);
+  q = __fma_rn(__fma_rn(-b, q, a), y, q);
+  return __fma_rn(__fma_rn(-b, q, a), y, q);
+}
+
+// Eq. (3) term j of cost model k as integer coefficients (lean kernel, lane 8k + j; filled once per simulation):
+// FLOPs F = cF * xF and e * elements R = c0 x0 + c1 x1 + c2 x2 with the batch variables
+//   j < 4 (matmul a_in x a_out):  xF = N, x0 = 1, x1 = N       cF = 2 a_in a_out, c0 = e a_in a_out, c1 = e (a_in + a_out)
+//   j = 4 (prefill attention):    xF = sum c(c+m), x0 = sum ceil(c/H)(c+m), x1 = sum c, x2 = sum c(c+m)
+//                                 cF = 4 H NQ, c0 = 2 e H NKV, c1 = 2 e H NQ, c2 = 2 e NQ
+//   j = 5 (decode attention):     xF = x2 = sum (m+1), x1 = n_d   cF = 4 H NQ, c1 = 2 e H NQ, c2 = e (2 NQ + 2 H NKV)
+//   j = 6 (All_Reduce, tp > 1):   xF = N, cF = 2 e h (tp - 1); the time is (F / tp) / link_bw
+// -- the integers batch_time forms (exact in int64, so any association gives the same values).  Lanes with j = 7,
+// k >= K or a linear model hold zeros (their term is 0 and is not summed).
+struct LTerm {
+  long long cF, c0, c1, c2;
+};
+// per model: the two divisors of its terms and their reciprocals {flops, 1/flops, bw, 1/bw, tp, 1/tp, link_bw, 1/link_bw}
+// (all 1 for a linear model, whose lanes divide zeros)
+__device__ inline void lterm_fill(const sim_cost_model_t& cm, int j, LTerm& t, double* dv) {
+  const long long h = cm.h, ff = cm.f, H = cm.H, NQ = cm.NQ, NKV = cm.NKV, e = cm.e;
+  const long long qo = (NQ + 2 * NKV) * H, ao = NQ * H;
+  t.cF = t.c0 = t.c1 = t.c2 = 0;
+  if (cm.mode == 1 && j < 4) {
+    const long long a_in = j == 0 ? h : (j == 1 ? ao : (j == 2 ? h : ff));
+    const long long a_out = j == 0 ? qo : (j == 1 ? h : (j == 2 ? 2 * ff : h));
+    t.cF = 2 * a_in * a_out, t.c0 = e * a_in * a_out, t.c1 = e * (a_in + a_out);
+  } else if (cm.mode == 1 && j == 4) {
+    t.cF = 4 * H * NQ, t.c0 = 2 * e * H * NKV, t.c1 = 2 * e * H * NQ, t.c2 = 2 * e * NQ;
+  } else if (cm.mode == 1 && j == 5) {
+    t.cF = 4 * H * NQ, t.c1 = 2 * e * H * NQ, t.c2 = e * (2 * NQ + 2 * H * NKV);
+  } else if (cm.mode == 1 && j == 6 && cm.tp > 1) {
+    t.cF = 2 * e * h * (long long)(cm.tp - 1);
+  }
+  if (j == 0 && cm.mode != 1) {
+    for (int x = 0; x < 8; x++) dv[x] = 1.0;
+  } else if (j == 0) {
+    const double tp = i2d(cm.tp);
+    dv[0] = cm.flops, dv[1] = __drcp_rn(cm.flops), dv[2] = cm.bw, dv[3] = __drcp_rn(cm.bw);
+    dv[4] = tp, dv[5] = __drcp_rn(tp), dv[6] = cm.link_bw, dv[7] = __drcp_rn(cm.link_bw);
+  }
+}
+
+// batch_time of model k on one lane from the term table (lean kernel's steady runs: one run step per lane): the same
+// terms, order and bits as batch_time, the divisions by cdiv
+__device__ __forceinline__ double batch_time_tab(const sim_cost_model_t& cm, const LTerm* tk, const double* dv,
+                                                 const Feat& f, int k) {
+  if (cm.mode != 1) return batch_time(cm, f, k);
+  auto term = [&](int j, long long xF, long long x0, long long x1, long long x2) {
+    const LTerm& t = tk[j];
+    return fmax(cdiv(i2d(t.cF * xF), dv[0], dv[1]), cdiv(i2d(t.c0 * x0 + t.c1 * x1 + t.c2 * x2), dv[2], dv[3]));
+  };
+  const long long N = f.N, s1m = f.md + f.nd;
+  double t = 0.0;
+#pragma unroll
+  for (int j = 0; j < 4; j++) t = dadd(t, term(j, N, 1, N, 0));
+  if (f.np > 0) t = dadd(t, term(4, f.pcm, f.pceil[k], f.cp, f.pcm));
+  if (f.nd > 0) t = dadd(t, term(5, s1m, 0, f.nd, s1m));
+  if (cm.tp > 1) {
+    const double ar = cdiv(cdiv(i2d(tk[6].cF * N), dv[4], dv[5]), dv[6], dv[7]);
+    t = dadd(t, ar);
+    t = dadd(t, ar);
+  }
+  return dmul(i2d(cm.layers), t);
+}
+
+// batch_time_warp with the per-lane term table (lean kernel): lane 8k + j evaluates term j of model k branch-free
+// (cdiv; a zero numerator is exact), lane k < K adds its model's terms in batch_time's order.  Same bits.
+__device__ __forceinline__ double batch_time_lanes(const sim_cost_model_t* cms, const LTerm* terms, const double (*dv)[8],
+                                                   int K, const Feat& f, bool anyTheo) {
+  const int lane = threadIdx.x & 31;
+  double term = 0.0;
+  if (anyTheo) {
+    const int k = lane >> 3, j = lane & 7;
+    const LTerm t = terms[lane];
+    const long long pce = k == 0 ? f.pceil[0] : (k == 1 ? f.pceil[1] : (k == 2 ? f.pceil[2] : f.pceil[3]));
+    const long long s1m = f.md + f.nd;
+    const long long xF = j == 4 ? f.pcm : (j == 5 ? s1m : f.N);
+    const long long x0 = j == 4 ? pce : 1, x1 = j < 4 ? f.N : (j == 4 ? f.cp : f.nd), x2 = j == 4 ? f.pcm : s1m;
+    const long long F = t.cF * xF, Re = t.c0 * x0 + t.c1 * x1 + t.c2 * x2;
+    const double* d = dv[k] + (j == 6 ? 4 : 0);
+    const double q1 = cdiv(i2d(F), d[0], d[1]);
+    const double q2 = cdiv(j == 6 ? q1 : i2d(Re), d[2], d[3]);
+    term = j == 6 ? q2 : fmax(q1, q2);
+  }
+  const int src = 8 * (lane < 4 ? lane : 0);
+  double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0, t4 = 0.0, t5 = 0.0, t6 = 0.0;
+  if (anyTheo) {
+    t0 = __shfl_sync(0xffffffffu, term, src), t1 = __shfl_sync(0xffffffffu, term, src + 1);
+    t2 = __shfl_sync(0xffffffffu, term, src + 2), t3 = __shfl_sync(0xffffffffu, term, src + 3);
+    t4 = __shfl_sync(0xffffffffu, term, src + 4), t5 = __shfl_sync(0xffffffffu, term, src + 5);
+    t6 = __shfl_sync(0xffffffffu, term, src + 6);
+  }
+  double d = 0.0;
+  if (lane < K) {
+    const sim_cost_model_t& cm = cms[lane];
+    if (cm.mode == 1) {
+      double t = 0.0;
+      t = dadd(t, t0);
+      t = dadd(t, t1);
+      t = dadd(t, t2);
+      t = dadd(t, t3);
+      if (f.np > 0) t = dadd(t, t4);
+      if (f.nd > 0) t = dadd(t, t5);
+      if (cm.tp > 1) {
+        t = dadd(t, t6);
+        t = dadd(t, t6);
+      }
+      d = dmul(i2d(cm.layers), t);
+    } else {
+      d = batch_time(cm, f, 0);
+    }
+  }
+  return d;
+}
+
 __device__ __forceinline__ int bucket_of(int x) {  // floor(log2 x), capped at 17
   int b = 31 - __clz(x);
   return b > 17 ? 17 : b;

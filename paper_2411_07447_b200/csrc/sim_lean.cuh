@@ -43,6 +43,8 @@ constexpr uint8_t F_MOVE_L = 64;  // SRF: an entry whose retention key moved rel
 
 struct LHead {
   sim_cost_model_t cm[SIM_MAX_COST];
+  LTerm term[32];                 // lane 8k + j: Eq. (3) term j of model k (batch_time_lanes)
+  double dv[SIM_MAX_COST][8];     // per model: the terms' divisors and reciprocals
   int hist[18 * 18];  // SRF+Hist: log2 histogram of (I, O) at completions (Q31)
   int pred[18];       // SRF+Hist: predicted output length per I bucket (recomputed after completions)
 };
@@ -198,6 +200,11 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       Hk[k] = cm->H;
       if (lane == k) H.cm[k] = *cm;
     }
+  {  // the per-lane Eq. (3) term table (zeros for lanes of models k >= K or linear; their divisors 1)
+    const int k = lane >> 3;
+    const sim_cost_model_t one{};  // (mode 0)
+    lterm_fill(k < K ? p.cms[cfg.cost[k]] : one, lane & 7, H.term[lane], H.dv[k]);
+  }
   __syncwarp();
 
   for (int i = lane; i < 18 * 18; i += 32) H.hist[i] = 0;
@@ -929,7 +936,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       f.N = N, f.np = np_, f.cp = cp, f.mp = mp, f.nd = nd, f.md = md, f.c2 = c2, f.mc = mc, f.pcm = pcm;
 #pragma unroll
       for (int k = 0; k < SIM_MAX_COST; k++) f.pceil[k] = pce[k];
-      const double d = batch_time_warp(H.cm, K, f, anyTheo);  // lane-parallel Eq. (3) terms (same bits)
+      const double d = batch_time_lanes(H.cm, H.term, H.dv, K, f, anyTheo);  // lane-parallel Eq. (3) terms (same bits)
       if (lane < K) clk = dadd(clk, d);
     }
     steps++;
@@ -1002,7 +1009,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
             f.N = ndl, f.np = 0, f.c2 = 0, f.mc = 0, f.cp = 0, f.mp = 0, f.pcm = 0, f.nd = ndl;
             f.md = MD + (E + lane) * ndl;
             for (int k = 0; k < SIM_MAX_COST; k++) f.pceil[k] = 0;
-            for (int k = 0; k < K; k++) s_dbuf[k * DB + lane] = batch_time(H.cm[k], f, 0);
+            for (int k = 0; k < K; k++) s_dbuf[k * DB + lane] = batch_time_tab(H.cm[k], H.term + 8 * k, H.dv[k], f, k);
           }
           __syncwarp();
           int ex = chunk;

@@ -1,0 +1,5 @@
+# lean kernel: Eq. (3) terms from a per-lane coefficient table with cdiv (constant divisors) -- GPU suite, A/B
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 300 > gpurun_out/r2q4_gputests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r2q4_gputests.log
+for l in ablibs/lib_base.so paper_2411_07447_b200/libsimsweep.so; do SIMSWEEP_LIB=$l timeout 600 python tools/crit_times.py >> gpurun_out/r2q4_ab.log 2>&1; done
+timeout 900 python bench.py --workload full --steps 5 --no-cpu-baseline --no-e2e > gpurun_out/r2q4_bench_full.json 2> gpurun_out/r2q4_bench_full.err
