@@ -240,15 +240,30 @@ static int validate_configs(const sim_config_t* cfgs, int32_t n_cfgs, const int3
 
 // Shared-memory carveout preference of the global-arena variants (percent): small, so that L1 keeps their per-slot
 // arrays.  An SM's L1 / shared split cannot change while CTAs are resident, so the SMs that host an arena simulation
-// take no shared-memory-resident CTA until it ends; measured on the north-star sweep (tools/timeline.py --full):
-// 10 % -> 439 ms, 50 % -> 437 ms, 100 % -> 535 ms (the arena simulations slow down with a 28 KB L1).
+// take no shared-memory-resident CTA until it ends.  15 % is the smallest split that holds two lean arena CTAs per
+// SM, so all 220 arena simulations of the north-star sweep start at once instead of 148 + a second wave after
+// ~160 ms; measured on that sweep (tools/timeline.py --full, profiling build, profiles/r2q6_timelines.md):
+// 10 % -> 367.6 ms (148 arena simulations at t = 0), 15 % -> 334.8, 20 % -> 337.5, 30 % -> 334.7, 50 % -> 337.6
+// (the sweep equals its longest simulation from 15 % on); round 1: 100 % -> 535 ms (a 28 KB L1).
 // SIMSWEEP_GM_CARVEOUT overrides (tools).
 static int arena_carveout() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SIMSWEEP_GM_CARVEOUT");
-    v = e ? atoi(e) : 10;
-    if (v < 0 || v > 100) v = 10;
+    v = e ? atoi(e) : 15;
+    if (v < 0 || v > 100) v = 15;
+  }
+  return v;
+}
+
+// Carveout of the shared-memory-resident variants (percent, default 100: the most CTAs per SM).
+// SIMSWEEP_SMEM_CARVEOUT overrides (tools: fewer co-resident simulations per SM).
+static int smem_carveout() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SIMSWEEP_SMEM_CARVEOUT");
+    v = e ? atoi(e) : 100;
+    if (v < 0 || v > 100) v = 100;
   }
   return v;
 }
@@ -315,7 +330,7 @@ static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_
       // shared-memory resident state: the largest carveout, so that more CTAs fit per SM; the global-arena
       // variant keeps the carveout small and leaves the rest of the 256 KB to L1
       cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           V.arena ? arena_carveout() : 100);
+                           V.arena ? arena_carveout() : smem_carveout());
       g_attr_set[dev] |= 1u << v;
     }
     kp.variant = v;
