@@ -142,3 +142,59 @@ def test_lean_large_window_azureconv():
     cases = [(simsweep.preset_config(nm, 100_000, S=131072), wl, A100)
              for nm in ("vllm", "vllm-srf", "sarathi", "sarathi-srf", "vllm-pf")]
     assert_parity(cases, processes=len(cases))
+
+
+_FULL = {}
+CRITICAL = ["online-70B vllm-srf llama3-70b_a100x4_theoretical M=100000 azureconv s9",
+            "online-70B vllm-srf llama3-70b_a100x4_theoretical M=100000 azureconv s3",
+            "online-70B vllm llama3-70b_a100x4_theoretical M=100000 azureconv s4"]
+
+
+def _full_oracle_job(i):
+    """Simulation i of sweep.full_sweep() on the CPU oracle (the parent builds the sweep before forking)."""
+    import oracle as o
+    cfgs, wls, ocost = _FULL["sweep"]
+    c, w = cfgs[i], wls[cfgs[i].workload]
+    oc = o.make_config(c.order, c.hybrid, c.chunked, c.replacement, C=c.C, M=c.M, S=c.S, max_steps=c.max_steps,
+                       n_cost=c.n_cost, reserve=c.reserve)
+    return i, o.run(oc, w.I, w.O, w.T, [ocost[c.cost[k]] for k in range(c.n_cost)])
+
+
+def test_full_sweep_bench_launch_sampled():
+    """The north-star sweep (BASELINE configs [1]-[5], sweep.full_sweep: 3554 simulations, K = 4 grids, online
+    LongForm / AzureConv runs, heterogeneous mixes) in bench.py's launch configuration: one sim_sweep_device call
+    over device-resident inputs in LPT order, every kernel variant running concurrently.  Compared with the oracle on
+    a sample: every 31st simulation with n <= 4096, and of the AzureConv-size (arena variant) runs the three
+    longest-estimated, the measured critical path (bench.py config.critical_path: the 70B A100x4 theoretical runs
+    below) and every 40th of the rest; integers bit-exact, per-request times 0 ULP for every cost model, means 1e-9
+    relative."""
+    import multiprocessing as mp
+    import os
+
+    import oracle as o
+    import torch
+
+    from paper_2411_07447_b200 import sweep
+    from parity import compare
+
+    cfgs, wls, cms, labels = sweep.full_sweep()
+    order = sweep.partition_lpt(sweep.estimate(cfgs, wls), 1)[0]
+    ds = simsweep.DeviceSweep(cfgs, wls, cms, device="cuda", order=np.asarray(order, np.int32))
+    ds.launch()
+    torch.cuda.synchronize()
+    g = ds.fetch()
+    small = [i for i in order if wls[cfgs[i].workload].n <= 4096]
+    big = [i for i in order if wls[cfgs[i].workload].n > 4096]
+    crit = [i for i in big if " ".join(map(str, labels[i])) in CRITICAL]
+    sample = small[::31] + big[:3] + crit + [i for i in big[3::40] if i not in crit]
+    ocms = o.load_cost_models()
+    names = {bytes(v): k for k, v in simsweep.load_cost_models().items()}
+    _FULL["sweep"] = (cfgs, wls, [ocms[names[bytes(c)]] for c in cms])
+    jobs = sorted(sample, key=lambda i: -(wls[cfgs[i].workload].n > 4096))  # the long oracle runs first
+    with mp.get_context("fork").Pool(min(len(os.sched_getaffinity(0)), len(jobs))) as pool:
+        ors = dict(pool.map(_full_oracle_job, jobs, chunksize=1))
+    bad = []
+    for i in sample:
+        bad += compare(g, ors, i, label=" ".join(map(str, labels[i])))
+    assert len(crit) == len(CRITICAL) and all(g.status(i) == "ok" for i in crit)
+    assert bad == [], "\n".join(bad[:40])
