@@ -366,6 +366,16 @@ typedef struct {
 int sim_optimum(const sim_opt_problem_t* probs, int32_t n_probs, const sim_cost_model_t* cm, sim_opt_result_t* out,
                 int32_t device);
 
+/* Occupancy of the lean shared-memory kernel (configurations with n <= 1024 requests): how many of its
+ * one-warp simulations share an SM.  Every simulation is one dependent chain, so a sweep whose length is set by a
+ * few long simulations runs fastest with few per SM (the long ones lose less to their neighbours' issue slots and
+ * instruction-cache footprint than the sweep gains from concurrency: BASELINE configs[1] 24.89 ms at 5 per SM,
+ * 23.95-24.13 at 2, 26.09 at 1); a sweep of many equally long simulations needs the concurrency.  k = 1 .. 5 fixes
+ * it (5 = the shared-memory maximum); k = 0 (the default) picks 2 when the launch has at most 32 such simulations
+ * per SM, else 5.  Process-wide, host-only; applies to later sim_sweep / sim_sweep_device calls.  Returns 0, or
+ * SIM_EINVAL for k outside 0 .. 5. */
+int sim_set_lean_ctas_per_sm(int32_t k);
+
 const char* sim_strerror(int code);
 const char* sim_version(void);
 

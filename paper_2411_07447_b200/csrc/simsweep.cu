@@ -256,7 +256,7 @@ static int arena_carveout() {
   return v;
 }
 
-// Carveout of the shared-memory-resident variants (percent, default 100: the most CTAs per SM).
+// Carveout of the shared-memory-resident block-kernel variants (percent, default 100: the most CTAs per SM).
 // SIMSWEEP_SMEM_CARVEOUT overrides (tools: fewer co-resident simulations per SM).
 static int smem_carveout() {
   static int v = -1;
@@ -266,6 +266,22 @@ static int smem_carveout() {
     if (v < 0 || v > 100) v = 100;
   }
   return v;
+}
+// Carveout of the lean n <= 1024 variant: CTAs per SM (sim_set_lean_ctas_per_sm; 0 = auto: two per SM for at most
+// 32 simulations per SM, else the maximum).  A CTA takes 45.2 KB + 1 KB; the shared-memory configurations are
+// 64 / 100 / 164 / 196 / 228 KB, so k CTAs per SM need 28 / 44 / 72 / 86 / 100 % of the 228 KB.  Measured on the
+// grid (tools/gpu_r2q16.sh .. gpu_r2q18.sh, tools/gpu_r2g.sh): 1 per SM 26.09 ms, 2: 23.95-24.13, 3: 24.65,
+// 5: 24.89-25.05; full sweep 2 per SM 316-320 ms against 331-350 at 5.  SIMSWEEP_LEAN_CARVEOUT (percent) overrides.
+static int g_lean_k = 0;
+static int lean_carveout(int n_lean, int nsm) {
+  const char* e = getenv("SIMSWEEP_LEAN_CARVEOUT");
+  if (e) {
+    const int v = atoi(e);
+    return v < 0 || v > 100 ? 100 : v;
+  }
+  static const int pct[6] = {100, 28, 44, 72, 86, 100};
+  const int k = g_lean_k ? g_lean_k : (n_lean <= 32 * nsm ? 2 : 5);
+  return pct[k];
 }
 
 static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, int32_t n_wls,
@@ -329,9 +345,21 @@ static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_
         return SIM_ECUDA;
       // shared-memory resident state: the largest carveout, so that more CTAs fit per SM; the global-arena
       // variant keeps the carveout small and leaves the rest of the 256 KB to L1
-      cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           V.arena ? arena_carveout() : smem_carveout());
+      if (v != V_LEAN)
+        cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             V.arena ? arena_carveout() : smem_carveout());
       g_attr_set[dev] |= 1u << v;
+    }
+    if (v == V_LEAN) {  // its occupancy depends on the launch (sim_set_lean_ctas_per_sm): set when it changes
+      static int last[64];
+      int nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      const int cv = lean_carveout(cnt[v], nsm);
+      if (last[dev] != cv + 1) {
+        if (cudaFuncSetAttribute((const void*)V.fn, cudaFuncAttributePreferredSharedMemoryCarveout, cv) != cudaSuccess)
+          return SIM_ECUDA;
+        last[dev] = cv + 1;
+      }
     }
     kp.variant = v;
     // the three GM variants share the workspace: disjoint arenas, one counter each
@@ -350,6 +378,12 @@ static int launch_sweep(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_
 }
 
 extern "C" {
+
+int sim_set_lean_ctas_per_sm(int32_t k) {
+  if (k < 0 || k > 5) return SIM_EINVAL;
+  g_lean_k = k;
+  return 0;
+}
 
 int sim_sweep_device(const sim_config_t* h_cfgs, int32_t n_cfgs, const int32_t* h_wls_n, int32_t n_wls,
                      const sim_config_t* d_cfgs, const sim_workload_t* d_wls, const sim_cost_model_t* d_cms,

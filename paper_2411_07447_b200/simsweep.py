@@ -140,6 +140,7 @@ def lib() -> ctypes.CDLL:
         L.sim_run_traced.restype = ctypes.c_int
         L.sim_run_traced.argtypes = [P(SimConfig), P(SimWorkload), ctypes.c_int32, P(SimCostModel), ctypes.c_int32,
                                      P(SimResult), SimRequestOut, P(SimTrace), ctypes.c_int32]
+        L.sim_set_lean_ctas_per_sm.argtypes = [ctypes.c_int32]
         L.sim_workspace_bytes.restype = ctypes.c_int64
         L.sim_workspace_bytes.argtypes = [P(SimConfig), ctypes.c_int32, P(ctypes.c_int32)]
         L.sim_request_rows.restype = ctypes.c_int
@@ -167,7 +168,12 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED_SYMBOLS = ["sim_sweep", "sim_sweep_device", "sim_validate", "sim_run_traced", "sim_workspace_bytes",
                     "sim_request_rows", "sim_strerror", "sim_version", "sim_batch_times", "sim_slo_frontier",
-                    "sim_kv_break_even", "sim_operator_costs", "sim_optimum"]
+                    "sim_kv_break_even", "sim_operator_costs", "sim_optimum", "sim_set_lean_ctas_per_sm"]
+
+
+def set_lean_ctas_per_sm(k: int) -> None:
+    """sim_set_lean_ctas_per_sm: simulations of the lean n <= 1024 kernel per SM (1..5), 0 = auto (include/simsweep.h)."""
+    _check(lib().sim_set_lean_ctas_per_sm(int(k)))
 
 
 def strerror(code: int) -> str:

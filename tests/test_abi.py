@@ -205,3 +205,14 @@ def test_operator_costs_rejects_bad_input(L):
     bad.bw = 0.0
     with pytest.raises(simsweep.SimError, match="cost"):
         simsweep.sim_operator_costs([bad], [(1, 1, 0, 0, 0)])
+
+
+def test_lean_ctas_per_sm_setter(L):
+    """sim_set_lean_ctas_per_sm is host-only: 0 (auto) .. 5 accepted, anything else SIM_EINVAL."""
+    for k in range(6):
+        assert L.sim_set_lean_ctas_per_sm(k) == 0
+    assert L.sim_set_lean_ctas_per_sm(-1) == -1  # SIM_EINVAL
+    assert L.sim_set_lean_ctas_per_sm(6) == -1
+    assert L.sim_set_lean_ctas_per_sm(0) == 0
+    with pytest.raises(simsweep.SimError):
+        simsweep.set_lean_ctas_per_sm(9)
