@@ -26,6 +26,13 @@ for n in (40, 1500, 4200):  # CAP 1024 / 4096 / arena
     for nm, kw in (("vllm-srf", {}), ("sarathi", {}), ("vllm", {"knobs": simsweep.KNOB_HOL, "max_seqs": 8}),
                    ("rank-i", {}), ("sarathi-srf-hist", {}), ("vllm-pf", {})):
         cases.append((simsweep.preset_config(nm, 60, S=64, **kw), small(n, n, online=n > 1000), A100))
+# the Eq. (3) roofline models (the lean kernel's per-lane term table, cdiv) and K = 4 mixed models
+THEO = ["llama3-70b_a100x4_theoretical"]
+K4 = ["llama3-8b_a100_linear", "llama3-8b_h100_theoretical", "llama3-70b_a100x4_linear", "llama3-70b_h100x4_theoretical"]
+for n in (40, 1500, 4200):
+    cases.append((simsweep.preset_config("vllm-srf", 60, S=64), small(n + 1, n, online=n > 1000), THEO))
+    cases.append((simsweep.preset_config("sarathi", 60, S=64), small(n + 2, n, online=n > 1000), THEO))
+cases.append((simsweep.preset_config("sarathi-srf", 60, S=64), small(7, 40), K4))
 g, ors = run_case_list(cases)
 bad = []
 for i in range(len(cases)):
