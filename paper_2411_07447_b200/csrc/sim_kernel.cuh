@@ -229,13 +229,6 @@ __device__ __forceinline__ double cdiv(double a, double b, double y) {
 struct LTerm {
   long long cF, c0, c1, c2;
 };
-#ifdef SIMSWEEP_TV
-// the batch variables a term reads, by index into batch_time_lanes' per-step vector
-// {1, N, sum c(c+m), sum c, n_d, sum (m+1), sum ceil(c/H_k)(c+m) for k = 0..3}; lane 8k + j: 4 bits each (xF, x0, x1, x2)
-__device__ inline int lterm_index(int k, int j) {
-  return j < 4 ? (1 | 0 << 4 | 1 << 8) : (j == 4 ? (2 | (6 + k) << 4 | 3 << 8 | 2 << 12) : (j == 5 ? (5 | 4 << 8 | 5 << 12) : 1));
-}
-#endif
 // per model: the two divisors of its terms and their reciprocals {flops, 1/flops, bw, 1/bw, tp, 1/tp, link_bw, 1/link_bw}
 // (all 1 for a linear model, whose lanes divide zeros)
 __device__ inline void lterm_fill(const sim_cost_model_t& cm, int j, LTerm& t, double* dv) {
@@ -288,27 +281,16 @@ __device__ __forceinline__ double batch_time_tab(const sim_cost_model_t& cm, con
 // batch_time_warp with the per-lane term table (lean kernel): lane 8k + j evaluates term j of model k branch-free
 // (cdiv; a zero numerator is exact), lane k < K adds its model's terms in batch_time's order.  Same bits.
 __device__ __forceinline__ double batch_time_lanes(const sim_cost_model_t* cms, const LTerm* terms, const double (*dv)[8],
-                                                   int K, const Feat& f, bool anyTheo, long long* tv = nullptr) {
+                                                   int K, const Feat& f, bool anyTheo) {
   const int lane = threadIdx.x & 31;
   double term = 0.0;
   if (anyTheo) {
     const int k = lane >> 3, j = lane & 7;
     const LTerm t = terms[lane];
-#ifdef SIMSWEEP_TV
-    __syncwarp();  // (the previous step's reads of tv are done)
-    if (lane == 0) {
-      tv[0] = 1, tv[1] = f.N, tv[2] = f.pcm, tv[3] = f.cp, tv[4] = f.nd, tv[5] = f.md + f.nd;
-      tv[6] = f.pceil[0], tv[7] = f.pceil[1], tv[8] = f.pceil[2], tv[9] = f.pceil[3];
-    }
-    __syncwarp();
-    const int ix = lterm_index(k, j);
-    const long long xF = tv[ix & 15], x0 = tv[(ix >> 4) & 15], x1 = tv[(ix >> 8) & 15], x2 = tv[(ix >> 12) & 15];
-#else
     const long long pce = k == 0 ? f.pceil[0] : (k == 1 ? f.pceil[1] : (k == 2 ? f.pceil[2] : f.pceil[3]));
     const long long s1m = f.md + f.nd;
     const long long xF = j == 4 ? f.pcm : (j == 5 ? s1m : f.N);
     const long long x0 = j == 4 ? pce : 1, x1 = j < 4 ? f.N : (j == 4 ? f.cp : f.nd), x2 = j == 4 ? f.pcm : s1m;
-#endif
     const long long F = t.cF * xF, Re = t.c0 * x0 + t.c1 * x1 + t.c2 * x2;
     const double* d = dv[k] + (j == 6 ? 4 : 0);
     const double q1 = cdiv(i2d(F), d[0], d[1]);

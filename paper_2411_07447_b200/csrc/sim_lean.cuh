@@ -45,9 +45,6 @@ struct LHead {
   sim_cost_model_t cm[SIM_MAX_COST];
   LTerm term[32];                 // lane 8k + j: Eq. (3) term j of model k (batch_time_lanes)
   double dv[SIM_MAX_COST][8];     // per model: the terms' divisors and reciprocals
-#ifdef SIMSWEEP_TV
-  long long tv[10];               // batch_time_lanes: this step's batch variables
-#endif
   int hist[18 * 18];  // SRF+Hist: log2 histogram of (I, O) at completions (Q31)
   int pred[18];       // SRF+Hist: predicted output length per I bucket (recomputed after completions)
 };
@@ -939,11 +936,7 @@ __global__ void __launch_bounds__(32, 1) sim_lean_kernel(KParams p) {
       f.N = N, f.np = np_, f.cp = cp, f.mp = mp, f.nd = nd, f.md = md, f.c2 = c2, f.mc = mc, f.pcm = pcm;
 #pragma unroll
       for (int k = 0; k < SIM_MAX_COST; k++) f.pceil[k] = pce[k];
-      #ifdef SIMSWEEP_TV
-      const double d = batch_time_lanes(H.cm, H.term, H.dv, K, f, anyTheo, H.tv);
-#else
-      const double d = batch_time_lanes(H.cm, H.term, H.dv, K, f, anyTheo);
-#endif  // lane-parallel Eq. (3) terms (same bits)
+      const double d = batch_time_lanes(H.cm, H.term, H.dv, K, f, anyTheo);  // lane-parallel Eq. (3) terms (same bits)
       if (lane < K) clk = dadd(clk, d);
     }
     steps++;
