@@ -1,3 +1,7 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r2i_gputests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r2i_gputests.log
-timeout 300 python tools/sim_times.py --only grid > gpurun_out/r2i_simtimes.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:sim_lean -s 1 -c 1 -o gpurun_out/r2i_lean python tools/one_sim.py vllm-srf 128 1024 > gpurun_out/r2i_ncu.log 2>&1
+# round-2 closing check of the tree as committed: GPU suite, smoke, both bench lines
+set -x
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/r2i_gputests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r2i_gputests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2i_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r2i_smoke.log
+timeout 900 python bench.py > gpurun_out/r2i_bench_grid.json 2> gpurun_out/r2i_bench_grid.err
+timeout 1200 python bench.py --workload full --steps 5 > gpurun_out/r2i_bench_full.json 2> gpurun_out/r2i_bench_full.err
