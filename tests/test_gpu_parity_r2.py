@@ -198,3 +198,19 @@ def test_full_sweep_bench_launch_sampled():
         bad += compare(g, ors, i, label=" ".join(map(str, labels[i])))
     assert len(crit) == len(CRITICAL) and all(g.status(i) == "ok" for i in crit)
     assert bad == [], "\n".join(bad[:40])
+
+
+def test_lean_occupancy_knob_keeps_results():
+    """sim_set_lean_ctas_per_sm changes only how many simulations share an SM: a grid slice run at 1, 2, 5 per SM
+    and the auto rule gives byte-identical results and per-request outputs (and the first one equals the oracle)."""
+    cases = [(simsweep.preset_config(nm, 100_000), workloads.fixed(I, O, 1024), A100)
+             for nm in ("vllm-srf", "sarathi") for I, O in ((16, 64), (128, 256))]
+    outs = []
+    try:
+        for k in (1, 2, 5, 0):
+            simsweep.set_lean_ctas_per_sm(k)
+            g, _ = run_case_list(cases) if outs else assert_parity(cases)
+            outs.append((g.results.tobytes(), g.t_first.tobytes(), g.t_done.tobytes(), g.n_preempt.tobytes()))
+    finally:
+        simsweep.set_lean_ctas_per_sm(0)
+    assert all(o == outs[0] for o in outs[1:])
